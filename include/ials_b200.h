@@ -1,0 +1,144 @@
+/*
+ * ials_b200.h -- C ABI of the B200-native iALS++ block solver (libials_b200.so).
+ *
+ * The reference (blockals 0.1.0, /root/reference/pkg/src/blockals) is a pure
+ * Python/NumPy package and has no FFI.  Its drop-in boundary is its Python
+ * API; every entry point below replaces the numerical core of one reference
+ * function, and the host mirror (paper_2110_14044_b200/*.py, bound with
+ * ctypes) keeps the reference names, argument meaning and error behaviour:
+ *
+ *   ials_predictions       <- compute_predictions   model.py:153-165
+ *   ials_partial_gramian   <- partial_gramian       linalg.py:39-45
+ *   ials_side_pass         <- _newton_side_pass     solvers.py:152-186
+ *                             (+ _solve_rows :101-114, SingularMatrixError linalg.py:18-28)
+ *   ials_epoch             <- ialspp_epoch          solvers.py:340-375
+ *   ials_loss_terms        <- compute_loss          model.py:168-188 (device reductions)
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (memory owned by the caller,
+ *     e.g. torch tensors); no function allocates device memory except the
+ *     session (error word).  Scratch comes from the caller's workspace, sized
+ *     with ials_workspace_bytes().
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*) and does not synchronise the host.
+ *   - Return 0 on success or a negative IALS_E_* code.  The last error text
+ *     is available from ials_last_error().  A singular block Hessian does not
+ *     fail the launch: it sets the session's device error word, read back
+ *     with ials_check_singular() (which synchronises the stream).
+ *   - Factor tables are row-major fp32 with leading dimension ld >= d.
+ *   - Indices are int32 (|S| < 2^31 is checked by the host mirror).
+ */
+#ifndef IALS_B200_H
+#define IALS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IALS_OK 0
+#define IALS_E_INVALID (-1)   /* -> ValueError                    */
+#define IALS_E_SINGULAR (-2)  /* -> SingularMatrixError(row,pivot) */
+#define IALS_E_CUDA (-3)      /* -> RuntimeError                  */
+#define IALS_E_NOMEM (-4)     /* workspace too small -> ValueError */
+
+/* One side of the interaction matrix (reference SideView, data.py:26-52).
+ * Rows are users (user pass) or items (item pass); entry e of row r lives in
+ * [ptr[r], ptr[r+1]).  pos[e] is the canonical (user-major) score-cache slot
+ * of the entry (data.py:156-162); NULL means identity (user view).  labels /
+ * weights NULL mean all ones. */
+typedef struct ials_side {
+  int32_t n_rows;          /* rows of the side being updated            */
+  int32_t n_fixed;         /* rows of the opposite (fixed) side         */
+  int64_t nnz;             /* entries                                   */
+  const int32_t* ptr;      /* [n_rows + 1]                              */
+  const int32_t* cols;     /* [nnz] fixed-side row of each entry        */
+  const float* labels;     /* [nnz] y, or NULL                          */
+  const float* weights;    /* [nnz] alpha, or NULL                      */
+  const int32_t* pos;      /* [nnz] cache slot, or NULL                 */
+  const float* lam;        /* [n_rows] effective_reg (model.py:144-150) */
+} ials_side;
+
+/* Work schedule of one side for one block width (built once per dataset by
+ * ials_schedule_* on the host mirror): light rows are solved by one fused
+ * kernel in descending-degree order; heavy rows are split into slices whose
+ * partial Hessians are reduced in a fixed order (deterministic). */
+typedef struct ials_sched {
+  int32_t n_light;
+  const int32_t* light_rows;    /* [n_light]                                  */
+  int32_t n_heavy;
+  const int32_t* heavy_rows;    /* [n_heavy]                                  */
+  const int32_t* heavy_slice0;  /* [n_heavy + 1] first slice of each heavy row */
+  int32_t n_slices;
+  const int32_t* slice_heavy;   /* [n_slices] heavy index of each slice        */
+  const int32_t* slice_begin;   /* [n_slices] absolute entry range             */
+  const int32_t* slice_end;     /* [n_slices]                                  */
+} ials_sched;
+
+typedef struct ials_session ials_session;
+
+int ials_version(void);
+int ials_session_create(int device, ials_session** out);
+int ials_session_destroy(ials_session* s);
+/* Copies the last error message (NUL-terminated) into buf. */
+int ials_last_error(ials_session* s, char* buf, size_t len);
+/* Clear the device error word (stream-ordered). */
+int ials_reset_singular(ials_session* s, void* stream);
+/* Synchronises `stream`; returns IALS_E_SINGULAR and fills row/pivot/side
+ * (0 user, 1 item) if a non-positive pivot was met since the last reset. */
+int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pivot,
+                        int32_t* side);
+
+/* Heavy-row threshold (entries) used by the schedule for block width b. */
+int64_t ials_heavy_threshold(int32_t b);
+/* Slice length (entries) of heavy rows for block width b. */
+int64_t ials_slice_len(int32_t b);
+
+/* Bytes of scratch ials_side_pass / ials_partial_gramian / ials_epoch need. */
+size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, int32_t b,
+                            int32_t n_slices_max, int32_t n_heavy_max);
+
+/* out[e] = <W[user of e], H[col e]> for the user-major CSR (ptr, cols). */
+int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
+                     const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                     float* out, void* stream);
+
+/* slab[t][j] = sum_r M[r][t] * M[r][b0 + j]  (d x b, row-major, ld = b). */
+int ials_partial_gramian(ials_session* s, const float* M, int32_t n, int32_t ldm, int32_t d,
+                         int32_t b0, int32_t b, float* slab, void* workspace, size_t ws_bytes,
+                         void* stream);
+
+/* One exact Newton step on columns [b0, b0+b) of every row of `side`
+ * (reference _newton_side_pass, solvers.py:152-186): reads `fixed`
+ * (n_fixed x d) and the slab (d x b, from ials_partial_gramian of `fixed`),
+ * updates own[:, b0:b0+b] and the score cache in place.  side_id (0 user,
+ * 1 item) only labels a singular-row report. */
+int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sched,
+                   const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                   int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
+                   int32_t side_id, void* workspace, size_t ws_bytes, void* stream);
+
+/* One full iALS++ epoch (ialspp_epoch, solvers.py:340-375) over contiguous
+ * blocks of width b (the last keeps the remainder): cache recompute, then
+ * per block slab(H) -> user pass -> slab(W) -> item pass. */
+int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+               const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
+               float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
+               void* workspace, size_t ws_bytes, void* stream);
+
+/* Workspace bytes for ials_loss_terms at embedding dimension d. */
+size_t ials_loss_workspace_bytes(int32_t d);
+
+/* Device loss pieces (compute_loss, model.py:168-188), all in fp64:
+ * out[0] = sum_e w_e (yhat_e - y_e)^2 over the user-major CSR,
+ * out[1] = <W^T W, H^T H>, out[2] = sum_u lam_u |w_u|^2, out[3] = sum_i lam_i |h_i|^2. */
+int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* items,
+                    const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                    double* out, void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IALS_B200_H */

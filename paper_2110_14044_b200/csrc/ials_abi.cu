@@ -1,0 +1,422 @@
+// ials_abi.cu -- C ABI of libials_b200.so (see include/ials_b200.h).
+//
+// Host-side launch logic for the iALS++ kernels.  Everything here is
+// stream-ordered and allocation-free (scratch comes from the caller's
+// workspace); the only device allocation is the session's error word.
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#include "../../include/ials_b200.h"
+#include "ials_common.cuh"
+#include "ials_dense.cuh"
+#include "ials_sweep.cuh"
+#include "ials_loss.cuh"
+
+using namespace ials;
+
+struct ials_session {
+  int device;
+  unsigned long long* err;  // device error word (ULLONG_MAX = clean)
+  char msg[512];
+};
+
+static thread_local char g_msg[512];
+
+static int fail(ials_session* s, int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  char* dst = s ? s->msg : g_msg;
+  vsnprintf(dst, 512, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(s, expr)                                                             \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return fail((s), IALS_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e),  \
+                  __FILE__, __LINE__);                                                \
+  } while (0)
+
+#define LAUNCH_CHECK(s)                                                               \
+  do {                                                                                \
+    cudaError_t _e = cudaGetLastError();                                              \
+    if (_e != cudaSuccess)                                                            \
+      return fail((s), IALS_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                \
+  } while (0)
+
+static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int block_tile(int b) {
+  if (b <= 8) return 8;
+  if (b <= 16) return 16;
+  if (b <= 32) return 32;
+  if (b <= 64) return 64;
+  if (b <= 128) return 128;
+  return 256;
+}
+
+static constexpr int kMaxSplits = 64;
+
+// Exported functions get C linkage from their declarations in ials_b200.h.
+
+int ials_version(void) { return 1; }
+
+int ials_session_create(int device, ials_session** out) {
+  if (!out) return fail(nullptr, IALS_E_INVALID, "out is NULL");
+  ials_session* s = new ials_session();
+  s->device = device;
+  s->msg[0] = 0;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&s->err, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(s->err, 0xFF, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    fail(nullptr, IALS_E_CUDA, "session create: %s", cudaGetErrorString(e));
+    delete s;
+    return IALS_E_CUDA;
+  }
+  *out = s;
+  return IALS_OK;
+}
+
+int ials_session_destroy(ials_session* s) {
+  if (!s) return IALS_OK;
+  cudaFree(s->err);
+  delete s;
+  return IALS_OK;
+}
+
+int ials_last_error(ials_session* s, char* buf, size_t len) {
+  if (!buf || len == 0) return IALS_E_INVALID;
+  const char* m = s ? s->msg : g_msg;
+  strncpy(buf, m, len - 1);
+  buf[len - 1] = 0;
+  return IALS_OK;
+}
+
+int ials_reset_singular(ials_session* s, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  CUDA_TRY(s, cudaMemsetAsync(s->err, 0xFF, sizeof(unsigned long long), S(stream)));
+  return IALS_OK;
+}
+
+int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pivot,
+                        int32_t* side) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  unsigned long long key = 0;
+  CUDA_TRY(s, cudaMemcpyAsync(&key, s->err, sizeof(key), cudaMemcpyDeviceToHost, S(stream)));
+  CUDA_TRY(s, cudaStreamSynchronize(S(stream)));
+  if (key == ~0ull) return IALS_OK;
+  const int sd = static_cast<int>(key >> 62);
+  const int64_t r = static_cast<int64_t>((key >> 24) & 0xFFFFFFFFull);
+  const int pv = static_cast<int>(key & 0xFFFFFF);
+  if (row) *row = r;
+  if (pivot) *pivot = pv;
+  if (side) *side = sd;
+  return fail(s, IALS_E_SINGULAR, "normal equations singular for %s row %lld (pivot %d)",
+              sd == 0 ? "user" : "item", (long long)r, pv);
+}
+
+int64_t ials_heavy_threshold(int32_t b) { return block_tile(b) <= 32 ? 2048 : 4096; }
+int64_t ials_slice_len(int32_t b) {
+  const int bt = block_tile(b);
+  return bt <= 32 ? 1024 : (bt == 256 ? 1024 : 2048);
+}
+
+static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
+  (void)n;
+  return al256(size_t(kMaxSplits) * d * b * sizeof(float));
+}
+
+static size_t pass_ws(int32_t n_rows, int32_t b, int32_t n_slices, int32_t n_heavy) {
+  const size_t bt = block_tile(b);
+  return al256(size_t(n_rows) * b * 4) + al256(size_t(n_slices) * bt * bt * 4) +
+         al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4);
+}
+
+size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, int32_t b,
+                            int32_t n_slices_max, int32_t n_heavy_max) {
+  // epoch layout: [slab d*b][gram partials][pass scratch]; loss needs at most
+  // 2 d x d gramians + partials, covered separately by ials_loss_workspace.
+  return al256(size_t(d) * b * 4) + gram_ws(std::max(n_rows_max, n_fixed_max), d, b) +
+         pass_ws(std::max(n_rows_max, n_fixed_max), b, n_slices_max, n_heavy_max);
+}
+
+// ------------------------------------------------------------------ predictions
+template <int LPN>
+static void launch_pred_lpn(int nv, dim3 g, dim3 t, cudaStream_t st, int n_rows, const int* ptr,
+                            const int* cols, const float* W, int ldw, const float* H, int ldh,
+                            int d, float* out) {
+  switch (nv) {
+    case 1: k_pred_vec<LPN, 1><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+    case 2: k_pred_vec<LPN, 2><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+    case 4: k_pred_vec<LPN, 4><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+    case 8: k_pred_vec<LPN, 8><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+    default: k_pred_vec<LPN, 16><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+  }
+}
+
+int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
+                     const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                     float* out, void* stream) {
+  if (n_rows < 0 || d < 1 || ldw < d || ldh < d)
+    return fail(s, IALS_E_INVALID, "predictions: bad shape (n_rows=%d d=%d)", n_rows, d);
+  if (n_rows == 0) return IALS_OK;
+  const int warps_needed = n_rows;
+  const int blocks = std::min((warps_needed + 7) / 8, kNumSMs * 16);
+  const bool vec = (d % 4 == 0) && (ldw % 4 == 0) && (ldh % 4 == 0) && d <= 2048 &&
+                   (reinterpret_cast<uintptr_t>(W) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(H) % 16 == 0);
+  if (vec) {
+    const int d4 = d / 4;
+    int lpn = 1;
+    while (lpn * 2 <= std::max(1, d4 / 4) && lpn < 32) lpn *= 2;
+    int nv = (d4 + lpn - 1) / lpn;
+    int nvp = 1;
+    while (nvp < nv) nvp *= 2;
+    if (nvp > 16) { lpn = 32; nvp = 16; }
+    dim3 g(blocks), t(256);
+    switch (lpn) {
+      case 1: launch_pred_lpn<1>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+      case 2: launch_pred_lpn<2>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+      case 4: launch_pred_lpn<4>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+      case 8: launch_pred_lpn<8>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+      case 16: launch_pred_lpn<16>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+      default: launch_pred_lpn<32>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+    }
+  } else {
+    k_pred_scalar<<<blocks, 256, 0, S(stream)>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out);
+  }
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+// ------------------------------------------------------------------ gramian
+static int gramian_impl(ials_session* s, const float* M, int32_t n, int32_t ldm, int32_t d,
+                        int32_t b0, int32_t b, float* slab, float* part, size_t part_bytes,
+                        cudaStream_t st) {
+  const int tiles = ((d + GT - 1) / GT) * ((b + GT - 1) / GT);
+  int nsplit = std::max(1, (2 * kNumSMs + tiles - 1) / tiles);
+  nsplit = std::min(nsplit, std::max(1, (n + 255) / 256));
+  nsplit = std::min(nsplit, kMaxSplits);
+  while (nsplit > 1 && size_t(nsplit) * d * b * 4 > part_bytes) --nsplit;
+  if (size_t(nsplit) * d * b * 4 > part_bytes)
+    return fail(s, IALS_E_NOMEM, "partial_gramian: workspace too small");
+  int rps = (n + nsplit - 1) / nsplit;
+  rps = ((rps + GK - 1) / GK) * GK;
+  if (n == 0) {
+    CUDA_TRY(s, cudaMemsetAsync(slab, 0, size_t(d) * b * 4, st));
+    return IALS_OK;
+  }
+  dim3 g((d + GT - 1) / GT, (b + GT - 1) / GT, nsplit);
+  k_slab_partial<<<g, 256, 0, st>>>(M, n, ldm, d, b0, b, rps, part);
+  LAUNCH_CHECK(s);
+  const size_t cnt = size_t(d) * b;
+  const int rb = (int)std::min<size_t>((cnt + 255) / 256, 4096);
+  k_reduce_splits<<<rb, 256, 0, st>>>(part, nsplit, cnt, slab);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+int ials_partial_gramian(ials_session* s, const float* M, int32_t n, int32_t ldm, int32_t d,
+                         int32_t b0, int32_t b, float* slab, void* workspace, size_t ws_bytes,
+                         void* stream) {
+  if (n < 0 || d < 1 || ldm < d || b < 1 || b0 < 0 || b0 + b > d)
+    return fail(s, IALS_E_INVALID, "partial_gramian: bad shape (n=%d d=%d b0=%d b=%d)", n, d,
+                b0, b);
+  return gramian_impl(s, M, n, ldm, d, b0, b, slab, static_cast<float*>(workspace), ws_bytes,
+                      S(stream));
+}
+
+// ------------------------------------------------------------------ side pass
+template <int BT>
+static int set_smem_attrs(ials_session* s) {
+  static bool done = false;
+  if (done) return IALS_OK;
+  const int bytes = Lay<BT>::CTA_BYTES;
+  CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_light<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_cache<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done = true;
+  return IALS_OK;
+}
+
+template <int BT>
+static int launch_sweep(ials_session* s, const SweepParams& p, cudaStream_t st) {
+  using L = Lay<BT>;
+  int rc = set_smem_attrs<BT>(s);
+  if (rc) return rc;
+  const int threads = L::NT * L::RPC;
+  if (p.n_light > 0) {
+    k_sweep_light<BT><<<(p.n_light + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  if (p.n_heavy > 0) {
+    k_heavy_partial<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    k_heavy_solve<BT><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    k_heavy_cache<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  return IALS_OK;
+}
+
+static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sched* sched,
+                          const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                          int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
+                          int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!side || !sched || !fixed || !own || !slab || !cache)
+    return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
+  if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
+    return fail(s, IALS_E_INVALID, "side_pass: bad block (d=%d b0=%d b=%d)", d, b0, b);
+  const int bt = block_tile(b);
+  const size_t need = pass_ws(side->n_rows, b, sched->n_slices, sched->n_heavy);
+  if (need > ws_bytes)
+    return fail(s, IALS_E_NOMEM, "side_pass: workspace %zu < %zu bytes", ws_bytes, need);
+  SweepParams p;
+  p.side = SideDev{side->n_rows, side->n_fixed, side->ptr, side->cols, side->labels,
+                   side->weights, side->pos, side->lam};
+  p.fixed = fixed;
+  p.ldf = ldf;
+  p.own = own;
+  p.ldo = ldo;
+  p.d = d;
+  p.b0 = b0;
+  p.b = b;
+  p.slab = slab;
+  p.alpha0 = alpha0;
+  p.cache = cache;
+  p.side_id = side_id;
+  p.err = s->err;
+  p.vec = (b % 4 == 0) && (b0 % 4 == 0) && (ldf % 4 == 0) &&
+          (reinterpret_cast<uintptr_t>(fixed) % 16 == 0);
+  p.light_rows = sched->light_rows;
+  p.n_light = sched->n_light;
+  p.heavy_rows = sched->heavy_rows;
+  p.heavy_slice0 = sched->heavy_slice0;
+  p.n_heavy = sched->n_heavy;
+  p.slice_heavy = sched->slice_heavy;
+  p.slice_begin = sched->slice_begin;
+  p.slice_end = sched->slice_end;
+  p.n_slices = sched->n_slices;
+  char* w = ws;
+  float* proj = reinterpret_cast<float*>(w);
+  w += al256(size_t(side->n_rows) * b * 4);
+  p.hpart = reinterpret_cast<float*>(w);
+  w += al256(size_t(sched->n_slices) * bt * bt * 4);
+  p.gpart = reinterpret_cast<double*>(w);
+  w += al256(size_t(sched->n_slices) * bt * 8);
+  p.hdelta = reinterpret_cast<float*>(w);
+  p.proj = proj;
+  if (side->n_rows > 0) {
+    dim3 g((side->n_rows + GT - 1) / GT, (b + GT - 1) / GT);
+    k_project<<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, b, alpha0, proj);
+    LAUNCH_CHECK(s);
+  }
+  switch (bt) {
+    case 8: return launch_sweep<8>(s, p, st);
+    case 16: return launch_sweep<16>(s, p, st);
+    case 32: return launch_sweep<32>(s, p, st);
+    case 64: return launch_sweep<64>(s, p, st);
+    case 128: return launch_sweep<128>(s, p, st);
+    default: return launch_sweep<256>(s, p, st);
+  }
+}
+
+int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sched,
+                   const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                   int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
+                   int32_t side_id, void* workspace, size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  return side_pass_impl(s, side, sched, fixed, ldf, own, ldo, d, b0, b, slab, alpha0, cache,
+                        side_id, static_cast<char*>(workspace), ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------ epoch
+int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+               const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
+               float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
+               void* workspace, size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (!users || !items || !user_sched || !item_sched)
+    return fail(s, IALS_E_INVALID, "epoch: NULL argument");
+  if (b < 1 || b > d || b > 256) return fail(s, IALS_E_INVALID, "epoch: bad block size %d", b);
+  cudaStream_t st = S(stream);
+  char* ws = static_cast<char*>(workspace);
+  const size_t slab_bytes = al256(size_t(d) * b * 4);
+  const size_t gbytes = gram_ws(0, d, b);
+  if (ws_bytes < slab_bytes + gbytes) return fail(s, IALS_E_NOMEM, "epoch: workspace too small");
+  float* slab = reinterpret_cast<float*>(ws);
+  float* part = reinterpret_cast<float*>(ws + slab_bytes);
+  char* pws = ws + slab_bytes + gbytes;
+  const size_t pbytes = ws_bytes - slab_bytes - gbytes;
+  int rc = ials_predictions(s, users->n_rows, users->ptr, users->cols, W, ldw, H, ldh, d, cache,
+                            stream);
+  if (rc) return rc;
+  for (int b0 = 0; b0 < d; b0 += b) {
+    const int bb = std::min(b, d - b0);
+    rc = gramian_impl(s, H, items->n_rows, ldh, d, b0, bb, slab, part, gbytes, st);
+    if (rc) return rc;
+    rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
+                        pws, pbytes, st);
+    if (rc) return rc;
+    rc = gramian_impl(s, W, users->n_rows, ldw, d, b0, bb, slab, part, gbytes, st);
+    if (rc) return rc;
+    rc = side_pass_impl(s, items, item_sched, W, ldw, H, ldh, d, b0, bb, slab, alpha0, cache, 1,
+                        pws, pbytes, st);
+    if (rc) return rc;
+  }
+  return IALS_OK;
+}
+
+// ------------------------------------------------------------------ loss
+size_t ials_loss_workspace_bytes(int32_t d) {
+  return 2 * al256(size_t(d) * d * 4) + gram_ws(0, d, d) +
+         al256(size_t(kLossBlocks) * 4 * sizeof(double));
+}
+
+int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* items,
+                    const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                    double* out, void* workspace, size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (!users || !items || !W || !H || !out) return fail(s, IALS_E_INVALID, "loss: NULL argument");
+  cudaStream_t st = S(stream);
+  // workspace: [gw d*d][gh d*d][gram partials][block partials (doubles)]
+  char* w = static_cast<char*>(workspace);
+  const size_t gsz = al256(size_t(d) * d * 4);
+  const size_t psz = gram_ws(0, d, d);
+  const size_t rsz = al256(size_t(kLossBlocks) * 4 * sizeof(double));
+  if (ws_bytes < 2 * gsz + psz + rsz) return fail(s, IALS_E_NOMEM, "loss: workspace too small");
+  float* gw = reinterpret_cast<float*>(w);
+  float* gh = reinterpret_cast<float*>(w + gsz);
+  float* part = reinterpret_cast<float*>(w + 2 * gsz);
+  double* red = reinterpret_cast<double*>(w + 2 * gsz + psz);
+  int rc = gramian_impl(s, W, users->n_rows, ldw, d, 0, d, gw, part, psz, st);
+  if (rc) return rc;
+  rc = gramian_impl(s, H, items->n_rows, ldh, d, 0, d, gh, part, psz, st);
+  if (rc) return rc;
+  k_loss_observed<<<kLossBlocks, 256, 0, st>>>(users->n_rows, users->ptr, users->cols,
+                                               users->labels, users->weights, W, ldw, H, ldh, d,
+                                               red);
+  LAUNCH_CHECK(s);
+  k_loss_dot<<<kLossBlocks, 256, 0, st>>>(gw, gh, size_t(d) * d, red + kLossBlocks);
+  LAUNCH_CHECK(s);
+  k_loss_rownorm<<<kLossBlocks, 256, 0, st>>>(W, users->n_rows, ldw, d, users->lam,
+                                              red + 2 * kLossBlocks);
+  LAUNCH_CHECK(s);
+  k_loss_rownorm<<<kLossBlocks, 256, 0, st>>>(H, items->n_rows, ldh, d, items->lam,
+                                              red + 3 * kLossBlocks);
+  LAUNCH_CHECK(s);
+  k_loss_final<<<1, 256, 0, st>>>(red, out);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+

@@ -1,0 +1,179 @@
+// ials_dense.cuh -- K-pred (score-cache recompute), K-slab (partial Gramian)
+// and K-proj (alpha0 * U @ slab), FP32 SIMT versions.
+#pragma once
+#include "ials_common.cuh"
+
+namespace ials {
+
+// ---------------------------------------------------------------- K-pred
+// compute_predictions (model.py:153-165): out[e] = <W[row], H[cols[e]]> over
+// the user-major CSR.  One warp per row (grid-stride); a group of LPN lanes
+// per entry, each lane holding NV float4 of the row of W in registers.
+template <int LPN, int NV>
+__global__ void __launch_bounds__(256)
+    k_pred_vec(int n_rows, const int* __restrict__ ptr, const int* __restrict__ cols,
+               const float* __restrict__ W, int ldw, const float* __restrict__ H, int ldh,
+               int d, float* __restrict__ out) {
+  constexpr int GPW = 32 / LPN;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int sub = lane / LPN, gl = lane % LPN;
+  const int d4 = d >> 2;
+  for (int row = gw; row < n_rows; row += nw) {
+    float4 w[NV];
+    const float4* wr = reinterpret_cast<const float4*>(W + (size_t)row * ldw);
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      const int v = gl + m * LPN;
+      w[m] = v < d4 ? __ldg(wr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int e0 = __ldg(ptr + row), e1 = __ldg(ptr + row + 1);
+    for (int eb = e0; eb < e1; eb += GPW) {
+      const int e = eb + sub;
+      float s = 0.f;
+      if (e < e1) {
+        const float4* hr = reinterpret_cast<const float4*>(H + (size_t)__ldg(cols + e) * ldh);
+#pragma unroll
+        for (int m = 0; m < NV; ++m) {
+          const int v = gl + m * LPN;
+          if (v < d4) {
+            const float4 h = __ldg(hr + v);
+            s = fmaf(w[m].x, h.x, s);
+            s = fmaf(w[m].y, h.y, s);
+            s = fmaf(w[m].z, h.z, s);
+            s = fmaf(w[m].w, h.w, s);
+          }
+        }
+      }
+      s = group_sum<LPN>(s);
+      if (e < e1 && gl == 0) out[e] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_pred_scalar(int n_rows, const int* __restrict__ ptr, const int* __restrict__ cols,
+                  const float* __restrict__ W, int ldw, const float* __restrict__ H, int ldh,
+                  int d, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int row = gw; row < n_rows; row += nw) {
+    const float* wr = W + (size_t)row * ldw;
+    const int e0 = ptr[row], e1 = ptr[row + 1];
+    for (int e = e0; e < e1; ++e) {
+      const float* hr = H + (size_t)cols[e] * ldh;
+      float s = 0.f;
+      for (int t = lane; t < d; t += 32) s = fmaf(wr[t], hr[t], s);
+      s = warp_sum(s);
+      if (lane == 0) out[e] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K-slab
+// partial_gramian (linalg.py:39-45): slab[t][j] = sum_r M[r][t] M[r][b0+j].
+// Split-K over rows; each CTA writes a 64x64 partial tile, a second kernel
+// sums the splits in a fixed order (deterministic).
+constexpr int GT = 64, GK = 16;
+
+__global__ void __launch_bounds__(256)
+    k_slab_partial(const float* __restrict__ M, int n, int ldm, int d, int b0, int b,
+                   int rows_per_split, float* __restrict__ part) {
+  __shared__ __align__(16) float As[GK][GT + 4];
+  __shared__ __align__(16) float Bs[GK][GT + 4];
+  const int t0 = blockIdx.x * GT, j0 = blockIdx.y * GT, split = blockIdx.z;
+  const int r_beg = split * rows_per_split;
+  const int r_end = min(n, r_beg + rows_per_split);
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  float acc[4][4] = {};
+  for (int r0 = r_beg; r0 < r_end; r0 += GK) {
+    for (int i = tid; i < GK * GT; i += 256) {
+      const int rr = i / GT, cc = i % GT;
+      const int r = r0 + rr;
+      const bool rok = r < r_end;
+      As[rr][cc] = (rok && t0 + cc < d) ? M[(size_t)r * ldm + t0 + cc] : 0.f;
+      Bs[rr][cc] = (rok && j0 + cc < b) ? M[(size_t)r * ldm + b0 + j0 + cc] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < GK; ++rr) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[rr][ty * 4]);
+      const float4 c = *reinterpret_cast<const float4*>(&Bs[rr][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], cv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* out = part + (size_t)split * d * b;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + ty * 4 + i;
+    if (t >= d) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int jj = j0 + tx * 4 + j;
+      if (jj < b) out[(size_t)t * b + jj] = acc[i][j];
+    }
+  }
+}
+
+__global__ void k_reduce_splits(const float* __restrict__ part, int nsplit, size_t count,
+                                float* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < nsplit; ++k) s += part[(size_t)k * count + i];
+    out[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------- K-proj
+// proj[r][j] = alpha0 * sum_t own[r][t] slab[t][j]  (the alpha0 * w_r G[:, pi]
+// gradient term of solvers.py:175), 64x64 output tiles, K = d.
+__global__ void __launch_bounds__(256)
+    k_project(const float* __restrict__ own, int n_rows, int ldo, int d,
+              const float* __restrict__ slab, int b, float alpha0, float* __restrict__ proj) {
+  __shared__ __align__(16) float As[GK][GT + 4];  // As[k][r]
+  __shared__ __align__(16) float Bs[GK][GT + 4];  // Bs[k][j]
+  const int r0 = blockIdx.x * GT, j0 = blockIdx.y * GT;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < d; k0 += GK) {
+    for (int i = tid; i < GK * GT; i += 256) {
+      const int rr = i / GK, kk = i % GK;  // own tile: 64 rows x 16 k (k fastest)
+      const int r = r0 + rr, k = k0 + kk;
+      As[kk][rr] = (r < n_rows && k < d) ? own[(size_t)r * ldo + k] : 0.f;
+      const int kb = i / GT, jj = i % GT;
+      Bs[kb][jj] = (k0 + kb < d && j0 + jj < b) ? slab[(size_t)(k0 + kb) * b + j0 + jj] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 c = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], cv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty * 4 + i;
+    if (r >= n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int jj = j0 + tx * 4 + j;
+      if (jj < b) proj[(size_t)r * b + jj] = alpha0 * acc[i][j];
+    }
+  }
+}
+
+}  // namespace ials

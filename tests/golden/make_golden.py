@@ -112,7 +112,7 @@ SMALL_CASES = [
     (6, 30, 30, 200, 5, 2, 0.1, 0.01, 1.0, "real", [[1, 3], [0, 2, 4]]),  # permuted partition
     (7, 45, 35, 450, 16, 16, 0.1, 0.001, 1.0, "unit", None),
     (8, 33, 29, 250, 32, 8, 0.1, 0.001, 1.0, "real", None),
-    (9, 20, 64, 700, 64, 32, 0.1, 0.001, 1.0, "unit", None),
+    (9, 80, 64, 900, 64, 32, 0.1, 0.001, 1.0, "unit", None),
     (10, 40, 40, 400, 48, 48, 0.1, 0.002, 1.0, "unit", None),
 ]
 

@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through libials_b200.so) against the golden
+vectors of the unmodified reference and against the CPU oracle.
+
+Tolerances (north_star: FP32 build vs float64 reference):
+  embeddings  ||X_gpu - X_ref||_F / ||X_ref||_F <= 1e-3  and  max|dX| / max|X_ref| <= 1e-3
+  loss        |L_gpu - L_ref| / L_ref <= 1e-3
+  CSR / index arrays: bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import relf, relmax, small_case
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def ials():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2110_14044_b200 as m
+    from paper_2110_14044_b200 import _lib
+    _lib.load()
+    return m
+
+
+def _tiny(ials, g):
+    data = ials.InteractionDataset(int(g["num_users"]), int(g["num_items"]), g["coo_users"],
+                                   g["coo_items"])
+    cfg = ials.SolverConfig(dim=32, block_size=8, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, init_stddev=0.1, epochs=10, seed=0)
+    model = ials.FactorModel(g["w0"].astype(np.float64), g["h0"].astype(np.float64))
+    return data, cfg, model
+
+
+def test_predictions_and_slab(ials, tiny_golden):
+    g = tiny_golden
+    data, cfg, model = _tiny(ials, g)
+    pred = ials.compute_predictions(model, data)
+    assert relmax(pred.scores, g["pred0"]) < 1e-5
+    slab = ials.partial_gramian(model.item_factors, np.arange(8))
+    assert relmax(slab, g["slab_h_b0"]) < 1e-5
+    # non-contiguous block
+    blk = np.array([1, 5, 9, 30])
+    want = g["h0"].astype(np.float64).T @ g["h0"].astype(np.float64)[:, blk]
+    assert relmax(ials.partial_gramian(model.item_factors, blk), want) < 1e-5
+
+
+def test_block_update_user_then_item(ials, tiny_golden):
+    g = tiny_golden
+    data, cfg, model = _tiny(ials, g)
+    cache = ials.compute_predictions(model, data)
+    ials.block_update(model, data, cache, cfg, np.arange(8), side="user")
+    assert relf(model.user_factors, g["w_user_b0"]) < TOL
+    assert relmax(model.user_factors, g["w_user_b0"]) < TOL
+    assert relmax(cache.scores, g["cache_user_b0"]) < TOL
+    ials.block_update(model, data, cache, cfg, np.arange(8), side="item")
+    assert relf(model.item_factors, g["h_item_b0"]) < TOL
+    assert relmax(model.item_factors, g["h_item_b0"]) < TOL
+    assert relmax(cache.scores, g["cache_item_b0"]) < TOL
+
+
+def test_tiny_one_and_ten_epochs(ials, tiny_golden):
+    g = tiny_golden
+    data, cfg, model = _tiny(ials, g)
+    cache = ials.PredictionCache.zeros(data.n_interactions)
+    ials.ialspp_epoch(model, data, cache, cfg)
+    for got, want in ((model.user_factors, g["w1"]), (model.item_factors, g["h1"])):
+        assert relf(got, want) < TOL and relmax(got, want) < TOL
+    assert abs(ials.compute_loss(model, data, cfg) - float(g["loss1"])) / float(g["loss1"]) < TOL
+    data, cfg, model = _tiny(ials, g)
+    _, reports = ials.train(model, data, cfg, log_loss=True)
+    for got, want in ((model.user_factors, g["w10"]), (model.item_factors, g["h10"])):
+        assert relf(got, want) < TOL and relmax(got, want) < TOL
+    losses = np.array([r.loss for r in reports])
+    assert np.all(np.abs(losses - g["losses"]) / g["losses"] < TOL)
+    assert np.all(np.diff(losses) <= 1e-6 * losses[:-1])     # monotone descent
+
+
+@pytest.mark.parametrize("seed", list(range(1, 11)))
+def test_small_instances(ials, small_golden, seed):
+    c = small_case(small_golden, seed)
+    data = ials.InteractionDataset(c["U"], c["I"], c["users"], c["items"], c["labels"],
+                                   c["weights"])
+    cfg = ials.SolverConfig(dim=c["d"], block_size=c["b"], unobserved_weight=c["alpha0"],
+                            reg=c["reg"], reg_exponent=c["nu"], epochs=3, seed=seed)
+    part = None
+    if "blocks" in c:
+        part = ials.BlockPartition(tuple(c["blocks"]), c["d"])
+    model = ials.FactorModel(c["w0"].copy(), c["h0"].copy())
+    cache = ials.PredictionCache.zeros(c["nnz"])
+    for e in range(3):
+        ials.ialspp_epoch(model, data, cache, cfg, part, e)
+        if e == 0:
+            assert relf(model.user_factors, c["w1"]) < TOL
+            assert relf(model.item_factors, c["h1"]) < TOL
+    for got, want in ((model.user_factors, c["w3"]), (model.item_factors, c["h3"])):
+        assert relf(got, want) < TOL and relmax(got, want) < TOL
+    assert abs(ials.compute_loss(model, data, cfg) - float(c["loss3"])) / float(c["loss3"]) < TOL
+    # single item-side block update of the last block
+    model = ials.FactorModel(c["w0"].copy(), c["h0"].copy())
+    cache = ials.compute_predictions(model, data)
+    ials.block_update(model, data, cache, cfg, c["bu_block"], side="item")
+    assert relf(model.item_factors, c["bu_h"]) < TOL
+    assert relmax(cache.scores, c["bu_cache"]) < TOL
+
+
+def test_singular_row_is_named(ials):
+    # reference tests/test_solvers.py:82-91 (empty row, nu=1, alpha0=0)
+    data = ials.InteractionDataset(2, 2, [0], [0])
+    cfg = ials.SolverConfig(dim=2, unobserved_weight=0.0, reg=0.1, reg_exponent=1.0)
+    model = ials.init_model(cfg, 2, 2)
+    cache = ials.compute_predictions(model, data)
+    with pytest.raises(ials.SingularMatrixError) as err:
+        ials.block_update(model, data, cache, cfg, np.arange(2), side="user")
+    assert err.value.row == 1 and err.value.pivot == 0
+
+
+def test_deterministic(ials, tiny_golden):
+    g = tiny_golden
+    runs = []
+    for _ in range(2):
+        data, cfg, model = _tiny(ials, g)
+        ials.train(model, data, cfg.with_(epochs=2))
+        runs.append(model.user_factors.copy())
+    assert np.array_equal(runs[0], runs[1])
+
+
+def _heavy_instance(U, I, per_user, s, seed):
+    rng = np.random.default_rng(seed)
+    w = np.arange(1, I + 1, dtype=np.float64) ** -s
+    w /= w.sum()
+    users, items = [], []
+    for u in range(U):
+        k = int(rng.integers(1, per_user + 1))
+        its = rng.choice(I, size=min(k, I), replace=False, p=w)
+        users.append(np.full(its.size, u))
+        items.append(its)
+    return U, I, np.concatenate(users), np.concatenate(items)
+
+
+@pytest.mark.parametrize("d,b,I", [(16, 8, 600), (32, 32, 600), (64, 64, 600), (128, 128, 600),
+                                   (96, 48, 600), (256, 256, 600),
+                                   # d > I: item Hessians with kappa ~ 4e3 in the first epoch
+                                   (64, 64, 60), (128, 128, 60)])
+def test_heavy_rows_vs_oracle(ials, d, b, I):
+    """Items above the heavy threshold go through split-K slices."""
+    from oracle import ialspp_oracle as orc
+    U, I, users, items = _heavy_instance(9000, I, 12, 1.2, 3)
+    data = ials.InteractionDataset(U, I, users, items)
+    assert data.item_counts.max() > 4096
+    cfg = ials.SolverConfig(dim=d, block_size=b, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=1, seed=1)
+    model = ials.init_model(cfg, U, I)
+    model.user_factors[:] = model.user_factors.astype(np.float32)
+    model.item_factors[:] = model.item_factors.astype(np.float32)
+    w, h = model.user_factors.copy(), model.item_factors.copy()
+    ials.train(model, data, cfg)
+    csr = orc.build_csr(U, I, users, items)
+    orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 1)
+    assert relf(model.user_factors, w) < TOL and relf(model.item_factors, h) < TOL
+    assert relmax(model.user_factors, w) < TOL and relmax(model.item_factors, h) < TOL
