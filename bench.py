@@ -1,0 +1,470 @@
+#!/usr/bin/env python
+"""iALS++ epoch benchmark (BASELINE.json metric: epoch seconds & nnz*d updates/s,
+% of roofline) on B200.
+
+A "step" is one full iALS++ epoch (cache recompute + B blocks x {slab(H), user
+pass, slab(W), item pass}) over a seeded synthetic interaction set with the
+named shape.  Default workload: configs[3], the ML20M-shaped set
+(136,677 x 20,108, 10.0M pairs) at d=1024, b=128 -- the configuration the
+metric (b=128) and the >=50%-of-roofline target are quoted on.
+
+    python bench.py [--config L1] [--gpus 1] [--steps 5] [--warmup 3]
+    python bench.py --impl reference ...     # the CPU oracle arm
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # key: (shape, d, b, description)
+    "tiny": ("tiny", 32, 8, "configs[0] tiny 2,000x1,000 ~50k, d=32 b=8"),
+    "mid": ("mid", 128, 32, "configs[1] ML20M-shaped 136,677x20,108 10.0M, d=128 b=32"),
+    "sw-b1": ("mid", 256, 1, "configs[2] d=256 b=1 (iCD case)"),
+    "sw-b16": ("mid", 256, 16, "configs[2] d=256 b=16"),
+    "sw-b64": ("mid", 256, 64, "configs[2] d=256 b=64"),
+    "sw-b128": ("mid", 256, 128, "configs[2] d=256 b=128"),
+    "sw-b256": ("mid", 256, 256, "configs[2] d=256 b=d (iALS case)"),
+    "L1": ("mid", 1024, 128, "configs[3] ML20M-shaped 136,677x20,108 10.0M, d=1024 b=128"),
+    "L2": ("mid", 2048, 128, "configs[3] ML20M-shaped, d=2048 b=128"),
+    "msd": ("msd", 2048, 128, "configs[4] MSD-shaped 571,355x41,140 33.6M, d=2048 b=128"),
+}
+ALPHA0, REG, NU, SIGMA = 0.1, 1e-3, 1.0, 0.1
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# FP32 FFMA peak: tools/microbench.cu on this pool's B200 (MEASURED_PEAKS.json has no FP32 figure)
+FP32_PEAK_TFLOPS = 64.5
+FP32_NOMINAL_TFLOPS = 74.4   # 148 SM x 128 lanes x 2 x 1.965 GHz
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------- data
+def dataset(shape, seed=0):
+    """(U, I, CSR dict) of the synthetic set; cached on disk (inputs only)."""
+    from paper_2110_14044_b200 import synthetic
+    cache_dir = os.path.expanduser("~/.cache/ials_b200")
+    path = os.path.join(cache_dir, f"{shape}_s{seed}.npz")
+    if os.path.exists(path):
+        with np.load(path) as z:
+            return {k: z[k] for k in z.files}
+    U, I, users, items = synthetic.generate(shape, seed)
+    from paper_2110_14044_b200.data import InteractionDataset
+    data = InteractionDataset(U, I, users, items)
+    iv = data.item_view()
+    out = {"U": np.array(U), "I": np.array(I), "user_ptr": data.user_ptr,
+           "user_cols": data.items.astype(np.int32), "item_ptr": data.item_ptr,
+           "item_cols": iv.cols.astype(np.int32), "item_pos": iv.cache_pos.astype(np.int32),
+           "users": data.users.astype(np.int32), "digest": np.array(synthetic.digest(users, items))}
+    try:
+        os.makedirs(cache_dir, exist_ok=True)
+        np.savez(path + ".tmp.npz", **out)
+        os.replace(path + ".tmp.npz", path)
+    except OSError:
+        pass
+    return out
+
+
+def roofline_model(U, I, S, d, b, p_fp32_tflops, bw_gbs):
+    """sweep FLOPs / gathered bytes per epoch, slab, predictions."""
+    B = -(-d // b)
+    f_sw = B * (2 * S * (b * (b + 1) + 4 * b) + (U + I) * (2 * d * b + b ** 3 / 3 + 2 * b * b))
+    q_sw = B * (2 * S * (4 * b + 4 + 8) + (U + I) * (4 * d + 4 * b + 8))
+    f_g = 2 * (U + I) * d * d
+    q_g = B * 4 * (U + I) * d
+    q_p = S * (4 * d + 8) + 4 * U * d
+    t_sw = max(f_sw / (p_fp32_tflops * 1e12), q_sw / (bw_gbs * 1e9))
+    t_g = max(f_g / (p_fp32_tflops * 1e12), q_g / (bw_gbs * 1e9))
+    t_p = q_p / (bw_gbs * 1e9)
+    bound = "fp32" if f_sw / (p_fp32_tflops * 1e12) >= q_sw / (bw_gbs * 1e9) else "hbm"
+    return {"F_sw": f_sw, "Q_sw": q_sw, "F_G": f_g, "Q_P": q_p, "t_sw": t_sw, "t_G": t_g,
+            "t_P": t_p, "t_epoch": t_sw + t_g + t_p, "sweep_bound": bound, "B": B}
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- distributed
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------- ours
+def run_ours(args, cfg_key):
+    import torch
+
+    from paper_2110_14044_b200 import _lib
+    from paper_2110_14044_b200.engine import DeviceProblem, Engine
+
+    shape, d, b, desc = CONFIGS[cfg_key]
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    ds = dataset(shape)
+    U, I = int(ds["U"]), int(ds["I"])
+    S = int(ds["user_ptr"][-1])
+    prob = DeviceProblem(dev, U, I, ds["user_ptr"], ds["user_cols"], ds["item_ptr"],
+                         ds["item_cols"], ds["item_pos"])
+    prob.set_regularizer(ALPHA0, REG, NU)
+    eng = Engine(prob)
+    # seeded init (model.py:123-134), fp32
+    from paper_2110_14044_b200.model import SolverConfig, init_model
+    cfg = SolverConfig(dim=d, block_size=b, unobserved_weight=ALPHA0, reg=REG,
+                       reg_exponent=NU, init_stddev=SIGMA, seed=0)
+    m = init_model(cfg, U, I)
+    W0 = torch.from_numpy(m.user_factors.astype(np.float32)).to(dev)
+    H0 = torch.from_numpy(m.item_factors.astype(np.float32)).to(dev)
+    del m
+    W, H = W0.clone(), H0.clone()
+    cache = torch.zeros(S, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    B = -(-d // b)
+    spans = [(b0, min(b, d - b0)) for b0 in range(0, d, b)]
+    slab = torch.empty(d * b, dtype=torch.float32, device=dev)
+    su, si = prob.users.schedule(b), prob.items.schedule(b)
+
+    def epoch_phased(ev):
+        """One epoch with CUDA events between phases (cache / slab / user / item)."""
+        ev[0].record(stream)
+        eng.predictions(W, H, cache)
+        k = 1
+        ev[k].record(stream); k += 1
+        for b0, bb in spans:
+            sl = slab[: d * bb].view(d, bb)
+            for side, fixed, own in (("user", H, W), ("item", W, H)):
+                eng.partial_gramian(fixed, b0, bb, sl)
+                ev[k].record(stream); k += 1
+                eng.side_pass(side, fixed, own, b0, bb, sl, ALPHA0, cache)
+                ev[k].record(stream); k += 1
+        return k
+
+    n_ev = 2 + 4 * len(spans)
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+              for _ in range(args.steps)]
+    for _ in range(args.warmup):
+        epoch_phased([torch.cuda.Event(enable_timing=True) for _ in range(n_ev)])
+    eng.sess.reset_singular()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clk = ClockSampler(local)
+    with clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for s in range(args.steps):
+            epoch_phased(events[s])
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    eng.sess.raise_if_singular()
+    total_ms = t_start.elapsed_time(t_end)
+    # per-phase sums
+    ph = {"cache": 0.0, "gramian": 0.0, "user": 0.0, "item": 0.0}
+    for s in range(args.steps):
+        e = events[s]
+        ph["cache"] += e[0].elapsed_time(e[1])
+        k = 1
+        for _ in spans:
+            for side in ("user", "item"):
+                ph["gramian"] += e[k].elapsed_time(e[k + 1])
+                ph[side] += e[k + 1].elapsed_time(e[k + 2])
+                k += 2
+    ms_step = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
+    updates = 2.0 * S * d
+    value = updates * world / (ms_step / 1e3)
+
+    hbm, hbm_src = load_peaks()
+    rl = roofline_model(U, I, S, d, b, FP32_PEAK_TFLOPS, hbm)
+    sweep_ms = (ph["user"] + ph["item"]) / args.steps
+    if rl["sweep_bound"] == "fp32":
+        achieved = rl["F_sw"] / (sweep_ms / 1e3) / 1e12
+        roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": FP32_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TFLOPS, 4)}
+    else:
+        achieved = rl["Q_sw"] / (sweep_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4)}
+    roof.update({
+        "traffic": None,
+        "kernel": "block sweep (K-proj + k_sweep_light + k_heavy_*), per side pass",
+        "per_launch_algorithmic": (rl["F_sw"] if roof["unit"] == "TFLOP/s" else rl["Q_sw"]) / (2 * rl["B"]),
+        "avg_launch_ms": round(sweep_ms / (2 * rl["B"]), 4),
+        "peak_source": "tools/microbench.cu FFMA (measured, this pool)" if roof["bound"] == "fp32" else hbm_src,
+        "sweep_share_of_step": round(sweep_ms / ms_step, 4),
+        "epoch_roofline_ms": round(rl["t_epoch"] * 1e3, 3),
+        "epoch_frac_of_roofline": round(rl["t_epoch"] * 1e3 / ms_step, 4),
+        "sweep_roofline_ms": round(rl["t_sw"] * 1e3, 3),
+    })
+    launches_per_epoch = 1 + len(spans) * 2 * 2  # pred + (slab partial + reduce) x 2
+    for sch in (su, si):
+        per_pass = 1 + (1 if sch.n_light else 0) + (3 if sch.n_heavy else 0)
+        launches_per_epoch += len(spans) * per_pass
+
+    # ---- e2e through the C-ABI epoch call with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        Wh = W0.cpu().pin_memory()
+        Hh = H0.cpu().pin_memory()
+        Ch = torch.empty(S, dtype=torch.float32).pin_memory()
+        Wo, Ho = torch.empty_like(Wh).pin_memory(), torch.empty_like(Hh).pin_memory()
+        def e2e_step():
+            W.copy_(Wh, non_blocking=True)
+            H.copy_(Hh, non_blocking=True)
+            eng.epoch(W, H, cache, b, ALPHA0)
+            Wo.copy_(W, non_blocking=True)
+            Ho.copy_(H, non_blocking=True)
+            Ch.copy_(cache, non_blocking=True)
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        z.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = a.elapsed_time(z) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": updates * world / (e2e_ms / 1e3), "unit": "nnz*d/s",
+               "ms_per_step": round(e2e_ms, 3),
+               "h2d_bytes_per_step": 4 * (U + I) * d,
+               "d2h_bytes_per_step": 4 * (U + I) * d + 4 * S,
+               "path": "ials_epoch C-ABI call, W/H from pinned host, W/H/cache back"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(ds, d, b, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": "ialspp_epoch_nnz_d_updates_per_s",
+            "value": value, "unit": "nnz*d/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "epoch_seconds": round(ms_step / 1e3, 6),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded Zipf/lognormal stand-in for ML20M/MSD shapes)",
+            "config": {"workload": cfg_key, "desc": desc, "users": U, "items": I, "nnz": S,
+                       "d": d, "b": b, "alpha0": ALPHA0, "reg": REG, "reg_exponent": NU,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (W,H,cache,CSR > 126 MB)" if (U + I) * d * 4 + 12 * S > 126e6 else "inputs fit in L2 (launch-bound config)"},
+            "phases_ms": {k: round(v / args.steps, 4) for k, v in ph.items()},
+            "roofline": roof,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_epoch * args.steps,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
+    """Oracle port (oracle/ialspp_oracle.py, NumPy f64 + OpenBLAS, all host
+    threads) on a bounded systematic sample: predictions for a sample of user
+    rows, one block's two slabs in full, the user pass for every s_u-th user and
+    the item pass for every s_i-th item (degree-sorted), scaled by the stride;
+    epoch = t_pred + B * t_block ("extrapolated from 1 of B blocks")."""
+    from oracle import ialspp_oracle as orc
+    U, I = int(ds["U"]), int(ds["I"])
+    uptr, iptr = ds["user_ptr"].astype(np.int64), ds["item_ptr"].astype(np.int64)
+    S = int(uptr[-1])
+    rng = np.random.default_rng(0)
+    scale = SIGMA / np.sqrt(d)
+    w = rng.normal(0.0, scale, size=(U, d))
+    h = rng.normal(0.0, scale, size=(I, d))
+    users = ds["users"].astype(np.int64)
+    ucols = ds["user_cols"].astype(np.int64)
+    icols = ds["item_cols"].astype(np.int64)
+    ipos = ds["item_pos"].astype(np.int64)
+    lab = np.ones(S)
+    lu = orc.effective_reg(np.diff(uptr), I, REG, ALPHA0, NU)
+    li = orc.effective_reg(np.diff(iptr), U, REG, ALPHA0, NU)
+    B = -(-d // b)
+    blk = np.arange(min(b, d))
+    # size the strides from a quick calibration of the per-entry cost
+    work_u = (S * b * b + U * (d * b + b ** 3 / 3))
+    per_unit = 2.0e-10 * max(1.0, b / 32)    # rough s per (flop-ish unit) on the host
+    s_u = max(1, int(work_u * per_unit * B / (0.35 * budget_s)))
+    s_i = max(1, s_u // 8)
+    s_p = max(1, int(S * d * 2e-9 / (0.15 * budget_s)))
+    t0 = time.perf_counter()
+    prows = np.arange(0, U, s_p)
+    idx = np.concatenate([np.arange(uptr[r], uptr[r + 1]) for r in prows])
+    _ = orc.predictions(w, h, users[idx], ucols[idx])
+    t_pred = (time.perf_counter() - t0) * (S / max(idx.size, 1))
+    cache = np.zeros(S)
+    t0 = time.perf_counter()
+    slab_h = orc.partial_gramian(h, blk)
+    t_gh = time.perf_counter() - t0
+    def timed_pass(ptr, cols, pos, fixed, own, slab, lam, stride):
+        head, tail = orc.systematic_rows(np.diff(ptr), stride)
+        t = 0.0
+        for rows, weight in ((head, 1.0), (tail, float(stride))):
+            if rows.size:
+                t0 = time.perf_counter()
+                orc.side_pass(ptr, cols, lab, lab, pos, fixed, own, cache, blk, slab, ALPHA0,
+                              lam, rows=rows)
+                t += (time.perf_counter() - t0) * weight
+        return t
+
+    t_user = timed_pass(uptr, ucols, np.arange(S), h, w, slab_h, lu, s_u)
+    t0 = time.perf_counter()
+    slab_w = orc.partial_gramian(w, blk)
+    t_gw = time.perf_counter() - t0
+    t_item = timed_pass(iptr, icols, ipos, w, h, slab_w, li, s_i)
+    t_epoch = t_pred + B * (t_gh + t_user + t_gw + t_item)
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info()]
+        threads = max([t for _, t in blas if t] or [os.cpu_count()])
+    except Exception:
+        blas, threads = [], os.cpu_count()
+    return {"value": 2.0 * S * d / t_epoch, "unit": "nnz*d/s", "cores": int(threads),
+            "kind": "port", "epoch_seconds_est": round(t_epoch, 2),
+            "sample": (f"oracle/ialspp_oracle.py f64 on this host: predictions for every {s_p}th "
+                       f"user, block-0 slabs in full, user / item pass on the 64 heaviest rows "
+                       f"in full plus every {s_u}th / {s_i}th run of 64 degree-sorted rows "
+                       f"(scaled by the stride); epoch = t_pred + {B} x t_block "
+                       f"(extrapolated from 1 of {B} blocks)"),
+            "phase_seconds_est": {"pred": round(t_pred, 3), "gram": round(t_gh + t_gw, 3),
+                                  "user_per_block": round(t_user, 3),
+                                  "item_per_block": round(t_item, 3)},
+            "blas": str(blas)}
+
+
+def run_reference(args, cfg_key):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    shape, d, b, desc = CONFIGS[cfg_key]
+    ds = dataset(shape)
+    S = int(ds["user_ptr"][-1])
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(ds, d, b, budget_s=args.cpu_budget)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(ds, d, b, budget_s=args.cpu_budget))
+    value = statistics.median(v["value"] for v in vals)
+    last = vals[-1]
+    line = {"impl": "reference", "metric": "ialspp_epoch_nnz_d_updates_per_s", "value": value,
+            "unit": "nnz*d/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(2.0 * S * d / value * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Zipf/lognormal stand-in for ML20M/MSD shapes)",
+            "config": {"workload": cfg_key, "desc": desc, "nnz": S, "d": d, "b": b},
+            "cpu_baseline": {"value": value, "unit": "nnz*d/s", "cores": last["cores"],
+                             "kind": "port", "sample": last["sample"]},
+            "e2e": {"value": value, "unit": "nnz*d/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="L1")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args, args.config)
+    else:
+        run_ours(args, args.config)
+
+
+if __name__ == "__main__":
+    main()

@@ -14,8 +14,11 @@ CPU container and writes ``tests/golden/*.npz``).  Parity is therefore pinned
 to the reference itself, not only to this restatement.
 
 Each function cites the reference lines it restates.  The structure is my
-own: rows are batched by *exact* degree (no power-of-two padding buckets,
-``data.py:54-85``), and the block solve uses a batched Cholesky.
+own: rows are batched on a x1.25 geometric degree grid (finer than the
+reference's power-of-two buckets, ``data.py:54-85``) with zero-weight padding
+entries; like the reference, the batched solve is LAPACK gesv
+(``solvers.py:101-114``) and a failing batch is diagnosed row by row with a
+Cholesky to name the row and pivot.
 """
 
 from __future__ import annotations
@@ -31,6 +34,7 @@ __all__ = [
 ]
 
 _ROW_BATCH_ELEMS = 1 << 21     # gathered (rows x degree x block) elements per batch
+_GRID = 1.25                   # degree classes: widths on a geometric grid
 
 
 class SingularRow(np.linalg.LinAlgError):
@@ -118,8 +122,10 @@ def partition(dim, block_size):
     return [np.arange(s, min(s + block_size, dim)) for s in range(0, dim, block_size)]
 
 
-def predictions(w, h, users, items, chunk=1 << 20):
+def predictions(w, h, users, items, chunk=None):
     """yhat_k = <w[users_k], h[items_k]> in canonical order (model.py:153-165)."""
+    if chunk is None:     # bound the gathered temporaries to ~256 MB
+        chunk = max(1024, (1 << 25) // max(1, w.shape[1]))
     out = np.empty(users.size)
     for s in range(0, users.size, chunk):
         e = min(s + chunk, users.size)
@@ -169,22 +175,35 @@ def side_pass(ptr, cols, labels, weights, cache_pos, fixed, update, cache, block
     block = np.asarray(block)
     p = block.size
     slab_pp = slab[block, :]
+    # block columns of the fixed side plus one all-zero sentinel row that padded
+    # entries point at (weight 0, label 0, cache slot -> scratch)
+    fixed_blk = np.zeros((fixed.shape[0] + 1, p))
+    fixed_blk[:-1] = fixed[:, block]
+    sentinel = fixed.shape[0]
     counts = np.diff(ptr)
     if rows is None:
         rows = np.arange(counts.size)
     rows = np.asarray(rows, dtype=np.int64)
     deg = counts[rows]
+    # batch rows whose degree rounds up to the same width on a x1.25 geometric grid
+    width = np.where(deg > 0, np.ceil(_GRID ** np.ceil(np.log(np.maximum(deg, 1)) / np.log(_GRID))),
+                     0).astype(np.int64)
+    width = np.maximum(width, deg)
     eye = np.eye(p)
-    for n in np.unique(deg):
-        grp = rows[deg == n]
+    cache_ext = np.append(cache, 0.0)
+    scratch = cache.size
+    for n in np.unique(width):
+        grp = rows[width == n]
         step = max(1, _ROW_BATCH_ELEMS // max(1, int(n) * p))
         for s in range(0, grp.size, step):
             r = grp[s:s + step]
-            idx = ptr[r][:, None] + np.arange(n)[None, :]            # (m, n)
-            x = fixed[cols[idx]][:, :, block]                        # (m, n, p)
-            a = weights[idx]
-            pos = cache_pos[idx]
-            rho = a * (cache[pos] - labels[idx])
+            off = np.arange(n)[None, :]
+            valid = off < counts[r][:, None]                         # (m, n)
+            idx = np.where(valid, ptr[r][:, None] + off, 0)
+            x = fixed_blk[np.where(valid, cols[idx], sentinel)]      # (m, n, p)
+            a = np.where(valid, weights[idx], 0.0)
+            pos = np.where(valid, cache_pos[idx], scratch)
+            rho = a * (cache_ext[pos] - np.where(valid, labels[idx], 0.0))
             w_full = update[r]
             w_blk = w_full[:, block]
             lam = lam_rows[r]
@@ -193,7 +212,7 @@ def side_pass(ptr, cols, labels, weights, cache_pos, fixed, update, cache, block
             hs = np.matmul(np.swapaxes(x * a[:, :, None], 1, 2), x)
             hs += alpha0 * slab_pp + lam[:, None, None] * eye
             try:
-                chol = np.linalg.cholesky(hs)
+                delta = np.linalg.solve(hs, g[:, :, None])[:, :, 0]
             except np.linalg.LinAlgError:
                 for i in range(r.size):
                     try:
@@ -201,11 +220,10 @@ def side_pass(ptr, cols, labels, weights, cache_pos, fixed, update, cache, block
                     except np.linalg.LinAlgError:
                         raise SingularRow(r[i], _first_bad_pivot(hs[i])) from None
                 raise
-            # two batched triangular solves: L y = g, L^T delta = y
-            y = np.linalg.solve(chol, g[:, :, None])
-            delta = np.linalg.solve(np.swapaxes(chol, 1, 2), y)[:, :, 0]
             update[np.ix_(r, block)] = w_blk - delta
-            cache[pos] -= np.matmul(x, delta[:, :, None])[:, :, 0]
+            cache_ext[pos] -= np.matmul(x, delta[:, :, None])[:, :, 0]
+            cache_ext[scratch] = 0.0
+    cache[:] = cache_ext[:-1]
 
 
 def side_regs(csr, alpha0, reg, exponent):
@@ -270,8 +288,18 @@ def cache_drift(cache, w, h, csr):
     return float(np.max(np.abs(cache - fresh) / (1.0 + np.abs(fresh)), initial=0.0))
 
 
-def systematic_rows(counts, stride):
-    """Every ``stride``-th row of the degree-sorted row list (a low-variance
-    sample for bounded CPU timing; each sampled row stands for ``stride``)."""
+def systematic_rows(counts, stride, run=64):
+    """A low-variance row sample for bounded CPU timing of a side pass.
+
+    Returns ``(head, tail)``: ``head`` = the ``run`` highest-degree rows (timed
+    in full, weight 1 -- they dominate heavy-tailed item sides), ``tail`` =
+    every ``stride``-th run of ``run`` consecutive rows of the remaining
+    degree-sorted list (weight ``stride``; rows of equal degree still batch as
+    in a full pass)."""
     order = np.argsort(-np.asarray(counts), kind="stable")
-    return np.sort(order[::stride])
+    if stride <= 1:
+        return np.sort(order), np.empty(0, dtype=np.int64)
+    head, rest = order[:run], order[run:]
+    starts = np.arange(0, rest.size, stride * run)
+    tail = np.concatenate([rest[s:s + run] for s in starts]) if starts.size else rest[:0]
+    return np.sort(head), np.sort(tail)

@@ -255,7 +255,15 @@ static int launch_sweep(ials_session* s, const SweepParams& p, cudaStream_t st) 
   if (rc) return rc;
   const int threads = L::NT * L::RPC;
   if (p.n_light > 0) {
-    k_sweep_light<BT><<<(p.n_light + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_light<BT>,
+                                                               threads, L::CTA_BYTES));
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int need = (p.n_light + L::RPC - 1) / L::RPC;
+    const int grid = std::min(need, per_sm * kNumSMs);
+    k_sweep_light<BT><<<grid, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
   }
   if (p.n_heavy > 0) {

@@ -88,8 +88,11 @@ struct Lay {
   static constexpr int OFF_RH = OFF_AW + 2 * KC;
   static constexpr int OFF_PS = OFF_RH + 2 * KC;
   static constexpr int OFF_L = OFF_PS + 2 * KC;
-  static constexpr int OFF_CB = OFF_L + ((LP + 3) / 4) * 4;
-  static constexpr int OFF_Y = OFF_CB + 2 * BT;
+  static constexpr int PLD = BT + 4;  // row stride of the transposed panel buffers
+  static constexpr int OFF_PB = OFF_L + ((LP + 3) / 4) * 4;  // raw panel, [8][PLD]
+  static constexpr int OFF_LB = OFF_PB + 8 * PLD;            // L panel,   [8][PLD]
+  static constexpr int OFF_PY = OFF_LB + 8 * PLD;            // y of the panel [8]
+  static constexpr int OFF_Y = OFF_PY + 8;
   static constexpr int OFF_YF = OFF_Y + BT;
   static constexpr int OFF_ID = OFF_YF + BT;
   static constexpr int OFF_D = OFF_ID + BT;
@@ -267,7 +270,21 @@ IALS_DEVI int accumulate_range(const SweepParams& p, Tiles<BT>& T, double& gacc,
 }
 
 // Steps 3-5: add the alpha0 slab / lambda terms, factor, solve; leaves the
-// step d in sm[OFF_D .. +b).  Returns false (after reporting) on a bad pivot.
+// step d in sm[OFF_D .. +b).  A non-positive pivot is reported to the error
+// word (the solve continues with pivot 1 so every value stays finite).
+//
+// Factorisation: right-looking blocked Cholesky with panels of 8 columns.
+// The lower triangle lives in the same register tiles the Hessian was
+// accumulated in.  Per panel:
+//   A1  warp 0 factors the 8x8 diagonal block (every lane redundantly, in
+//       registers) and forward-solves its part of the right-hand side;
+//   A2  every row below the panel is triangular-solved against it (one thread
+//       per row) and its RHS entry is updated;
+//   B   the trailing matrix takes a rank-8 update in the register tiles
+//       (vectorised panel loads, no masking: elements above the trailing block
+//       are final or unused), then the owners publish the next raw panel.
+// The backward solve L^T d = y runs on warp 0 panel by panel from the packed
+// L kept in shared memory.
 template <int BT>
 IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gacc, float* sm,
                                   int row, int tid, int team) {
@@ -275,12 +292,18 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
   const int warp = tid >> 5, lane = tid & 31;
   const int b = p.b;
   float* Lp = sm + L::OFF_L;
-  float* cb = sm + L::OFF_CB;
+  float* PB = sm + L::OFF_PB;
+  float* LB = sm + L::OFF_LB;
+  float* PY = sm + L::OFF_PY;
   float* ys = sm + L::OFF_Y;
   float* yf = sm + L::OFF_YF;
   float* invd = sm + L::OFF_ID;
   float* ds = sm + L::OFF_D;
   const float lam = p.side.lam[row];
+  if (tid < BT && tid >= b) {  // padded rows: zero L panel rows keep them identity
+#pragma unroll
+    for (int q = 0; q < 8; ++q) LB[q * L::PLD + tid] = 0.f;
+  }
   if (tid < BT) {
     double g = 0.0;
     if (tid < b)
@@ -308,94 +331,165 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
         T.acc[t][i][j] = v;
       }
     }
-    // publish column 0
-    if (T.coff[t] == 0) {
+  }
+  // 8-wide panels need SC >= 8 for the owner layout; BT = 8 / 16 tiles have
+  // SC = 2 / 4, so their panels are assembled from 4 / 2 owner lanes.
+  constexpr int PW = 8;
+  const int np = (b + PW - 1) / PW;
+  // publish panel 0 (raw)
 #pragma unroll
-      for (int i = 0; i < L::SR; ++i) cb[T.roff[t] + i] = T.acc[t][i][0];
+  for (int t = 0; t < L::TPW; ++t) {
+    if (!T.valid[t] || T.coff[t] >= PW) continue;
+#pragma unroll
+    for (int m = 0; m < L::SC; ++m) {
+      float* dst = PB + (T.coff[t] + m) * L::PLD + T.roff[t];
+#pragma unroll
+      for (int i = 0; i < L::SR; ++i) dst[i] = T.acc[t][i][m];
     }
   }
   team_sync<L::NW>(team);
-  // Right-looking Cholesky, one column per step; forward solve fused.
-  for (int j = 0; j < b; ++j) {
-    const float* cj = cb + (j & 1) * BT;
-    float piv = cj[j];
-    if (!(piv > 0.f) || !(piv < 3.0e38f)) {
-      if (tid == 0) report_singular(p.err, p.side_id, row, j);
-      piv = 1.f;
-    }
-    const float rp = 1.0f / sqrtf(piv);
-    const float yj = ys[j] * rp;
-    if (tid < b) {
-      if (tid > j) {
-        const float l = cj[tid] * rp;
-        Lp[tid * (tid + 1) / 2 + j] = l;
-        ys[tid] -= l * yj;
-      } else if (tid == j) {
-        Lp[j * (j + 1) / 2 + j] = piv * rp;
-        invd[j] = rp;
-        yf[j] = yj;
+  for (int pp = 0; pp < np; ++pp) {
+    const int c0 = pp * PW;
+    // ---- A1: 8x8 diagonal block (warp 0, redundantly per lane)
+    if (warp == 0) {
+      float a[PW][PW];
+#pragma unroll
+      for (int q = 0; q < PW; ++q)
+#pragma unroll
+        for (int m = 0; m <= q; ++m) a[q][m] = PB[m * L::PLD + c0 + q];
+      float rinv[PW];
+      int bad = -1;
+#pragma unroll
+      for (int k = 0; k < PW; ++k) {
+        float dk = a[k][k];
+        if (!(dk > 0.f) || !(dk < 3.0e38f)) {
+          if (bad < 0) bad = k;
+          dk = 1.f;
+        }
+        const float r = rsqrtf(dk);
+        rinv[k] = r;
+        a[k][k] = dk * r;
+#pragma unroll
+        for (int i = k + 1; i < PW; ++i) a[i][k] *= r;
+#pragma unroll
+        for (int i = k + 1; i < PW; ++i)
+#pragma unroll
+          for (int j = k + 1; j <= i; ++j) a[i][j] = fmaf(-a[i][k], a[j][k], a[i][j]);
+      }
+      if (bad >= 0 && c0 + bad < b && lane == 0) report_singular(p.err, p.side_id, row, c0 + bad);
+      float y[PW];
+#pragma unroll
+      for (int q = 0; q < PW; ++q) {
+        float v = ys[c0 + q];
+#pragma unroll
+        for (int m = 0; m < q; ++m) v = fmaf(-a[q][m], y[m], v);
+        y[q] = v * rinv[q];
+      }
+      if (lane < PW) {
+        const int q = lane;
+        float yq = 0.f, rq = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < PW; ++qq)
+          if (qq == q) { yq = y[qq]; rq = rinv[qq]; }
+        const int gq = c0 + q;
+        invd[gq] = rq;
+        yf[gq] = yq;
+        PY[q] = yq;
+        float* lrow = Lp + gq * (gq + 1) / 2 + c0;
+#pragma unroll
+        for (int qq = 0; qq < PW; ++qq) {
+          if (qq != q) continue;
+#pragma unroll
+          for (int m = 0; m < PW; ++m) {
+            const float v = (m <= qq) ? a[qq][m] : 0.f;
+            LB[m * L::PLD + gq] = v;
+            if (m <= qq) lrow[m] = v;
+          }
+        }
       }
     }
-    float* cn = cb + ((j + 1) & 1) * BT;
+    team_sync<L::NW>(team);
+    // ---- A2: rows below the panel (one thread per row)
+    for (int t = c0 + PW + tid; t < b; t += L::NT) {
+      float l[PW];
+      float yv = ys[t];
+      float* lrow = Lp + t * (t + 1) / 2 + c0;
 #pragma unroll
-    for (int t = 0; t < L::TPW; ++t) {
-      if (!T.valid[t]) continue;
-      if (T.roff[t] - (lane >> 2) * L::SR + L::ST <= j + 1) continue;  // super-tile done
-      float li[L::SR], lk[L::SC];
+      for (int q = 0; q < PW; ++q) {
+        float v = PB[q * L::PLD + t];
 #pragma unroll
-      for (int i = 0; i < L::SR; ++i) {
-        const int gi = T.roff[t] + i;
-        li[i] = (gi > j) ? cj[gi] * rp : 0.f;
+        for (int m = 0; m < q; ++m) v = fmaf(-l[m], LB[m * L::PLD + c0 + q], v);
+        l[q] = v * invd[c0 + q];
+        LB[q * L::PLD + t] = l[q];
+        lrow[q] = l[q];
+        yv = fmaf(-l[q], PY[q], yv);
       }
+      ys[t] = yv;
+    }
+    team_sync<L::NW>(team);
+    // ---- B: rank-8 trailing update + publish the next raw panel
+    const int cn = c0 + PW;
+    if (cn < b) {
 #pragma unroll
-      for (int k = 0; k < L::SC; ++k) {
-        const int gk = T.coff[t] + k;
-        lk[k] = (gk > j) ? cj[gk] * rp : 0.f;
-      }
+      for (int t = 0; t < L::TPW; ++t) {
+        if (!T.valid[t]) continue;
+        const int colend = T.coff[t] - (lane & 3) * L::SC + L::ST;  // super-tile column end
+        if (colend <= cn) continue;                                 // no trailing columns
 #pragma unroll
-      for (int i = 0; i < L::SR; ++i)
+        for (int q = 0; q < PW; ++q) {
+          float lr[L::SR], lc[L::SC];
+          lds_vec<L::SR>(lr, LB + q * L::PLD + T.roff[t]);
+          lds_vec<L::SC>(lc, LB + q * L::PLD + T.coff[t]);
 #pragma unroll
-        for (int k = 0; k < L::SC; ++k) T.acc[t][i][k] = fmaf(-li[i], lk[k], T.acc[t][i][k]);
-      // publish column j + 1 (owner lanes)
-      const int jn = j + 1 - T.coff[t];
-      if (jn >= 0 && jn < L::SC) {
+          for (int i = 0; i < L::SR; ++i)
 #pragma unroll
-        for (int i = 0; i < L::SR; ++i) {
+            for (int j = 0; j < L::SC; ++j) T.acc[t][i][j] = fmaf(-lr[i], lc[j], T.acc[t][i][j]);
+        }
+        if (T.coff[t] >= cn && T.coff[t] < cn + PW) {
 #pragma unroll
-          for (int k = 0; k < L::SC; ++k)
-            if (k == jn) cn[T.roff[t] + i] = T.acc[t][i][k];
+          for (int m = 0; m < L::SC; ++m) {
+            float* dst = PB + (T.coff[t] - cn + m) * L::PLD + T.roff[t];
+#pragma unroll
+            for (int i = 0; i < L::SR; ++i) dst[i] = T.acc[t][i][m];
+          }
         }
       }
     }
     team_sync<L::NW>(team);
   }
-  // Backward solve L^T d = y by warp 0 of the team.
+  // ---- backward solve L^T d = y (warp 0, panel by panel)
   if (warp == 0) {
-    float yv[L::MB];
+    for (int pp = np - 1; pp >= 0; --pp) {
+      const int c0 = pp * PW;
+      float z[PW], dlt[PW];
 #pragma unroll
-    for (int m = 0; m < L::MB; ++m) {
-      const int i = lane + 32 * m;
-      yv[m] = (i < b) ? yf[i] : 0.f;
-    }
+      for (int q = 0; q < PW; ++q) z[q] = yf[c0 + q];
 #pragma unroll
-    for (int mo = L::MB - 1; mo >= 0; --mo) {
-      const int jtop = min(31, b - 1 - 32 * mo);
-      for (int jj = jtop; jj >= 0; --jj) {
-        const int j = mo * 32 + jj;
-        const float dj = __shfl_sync(0xffffffffu, yv[mo], jj) * invd[j];
-        if (lane == jj) yv[mo] = dj;
-        const float* Lrow = Lp + j * (j + 1) / 2;
+      for (int q = PW - 1; q >= 0; --q) {
+        float v = z[q];
+        const int gq = c0 + q;
 #pragma unroll
-        for (int mm = 0; mm <= mo; ++mm) {
-          const int i = lane + 32 * mm;
-          if (i < j) yv[mm] = fmaf(-Lrow[i], dj, yv[mm]);
+        for (int m = q + 1; m < PW; ++m) {
+          const int gm = c0 + m;
+          v = fmaf(-Lp[gm * (gm + 1) / 2 + gq], dlt[m], v);
         }
+        dlt[q] = v * invd[gq];
       }
-    }
+      if (lane < PW) {
 #pragma unroll
-    for (int m = 0; m < L::MB; ++m) {
-      const int i = lane + 32 * m;
-      if (i < b) ds[i] = yv[m];
+        for (int q = 0; q < PW; ++q)
+          if (q == lane && c0 + q < b) ds[c0 + q] = dlt[q];
+      }
+      for (int i = lane; i < c0; i += 32) {
+        float v = yf[i];
+#pragma unroll
+        for (int q = 0; q < PW; ++q) {
+          const int gq = c0 + q;
+          v = fmaf(-Lp[gq * (gq + 1) / 2 + i], dlt[q], v);
+        }
+        yf[i] = v;
+      }
+      __syncwarp();
     }
   }
   team_sync<L::NW>(team);
@@ -463,21 +557,23 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   extern __shared__ __align__(16) float smem_all[];
   const int team = threadIdx.x / L::NT;
   const int tid = threadIdx.x - team * L::NT;
-  const int task = blockIdx.x * L::RPC + team;
-  if (task >= p.n_light) return;
   float* sm = smem_all + team * L::FLOATS;
-  const int row = p.light_rows[task];
-  const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
   zero_stage<BT>(sm, tid);
   team_sync<L::NW>(team);
-  Tiles<BT> T;
-  T.init(tid >> 5, tid & 31);
-  double gacc = 0.0;
-  const int nch = accumulate_range<BT>(p, T, gacc, sm, ebeg, eend, tid, team);
-  finalize_and_solve<BT>(p, T, gacc, sm, row, tid, team);
-  const float* ds = sm + L::OFF_D;
-  if (tid < p.b) p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
-  cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);
+  // persistent: rows are in descending-degree order, strided over the grid
+  for (int task = blockIdx.x * L::RPC + team; task < p.n_light; task += gridDim.x * L::RPC) {
+    const int row = p.light_rows[task];
+    const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
+    Tiles<BT> T;
+    T.init(tid >> 5, tid & 31);
+    double gacc = 0.0;
+    const int nch = accumulate_range<BT>(p, T, gacc, sm, ebeg, eend, tid, team);
+    finalize_and_solve<BT>(p, T, gacc, sm, row, tid, team);
+    const float* ds = sm + L::OFF_D;
+    if (tid < p.b) p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
+    cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);
+    team_sync<L::NW>(team);
+  }
 }
 
 template <int BT>
