@@ -91,6 +91,11 @@ int ials_reset_singular(ials_session* s, void* stream);
 int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pivot,
                         int32_t* side);
 
+/* Route block widths 33..128 through the tcgen05 (tensor-core, 3xTF32)
+ * sweep (1) or the FP32 SIMT sweep (0, default until the tensor-core path
+ * is faster).  Returns the previous setting.  IALS_TC=1 sets the default. */
+int ials_set_tensor_cores(int enable);
+
 /* Heavy-row threshold (entries) used by the schedule for block width b. */
 int64_t ials_heavy_threshold(int32_t b);
 /* Slice length (entries) of heavy rows for block width b. */

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <cstdarg>
 #include <algorithm>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/ials_b200.h"
@@ -14,6 +15,7 @@
 #include "ials_dense.cuh"
 #include "ials_sweep.cuh"
 #include "ials_loss.cuh"
+#include "ials_sweep_tc.cuh"
 
 using namespace ials;
 
@@ -248,9 +250,64 @@ static int set_smem_attrs(ials_session* s) {
   return IALS_OK;
 }
 
+static int g_tc = -1;  // -1: not yet read from IALS_TC
+static bool tc_enabled() {
+  if (g_tc < 0) {
+    const char* e = getenv("IALS_TC");
+    g_tc = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_tc == 1;
+}
+
+int ials_set_tensor_cores(int enable) {
+  const int prev = tc_enabled() ? 1 : 0;
+  g_tc = enable ? 1 : 0;
+  return prev;
+}
+
+// BT = 128 on the tensor core: light rows fused (k_sweep_tc128), heavy-row
+// partial Hessians on the tensor core, their solve / cache update on SIMT.
+static int launch_sweep_tc128(ials_session* s, const SweepParams& p, cudaStream_t st) {
+  using L = Lay<128>;
+  int rc = set_smem_attrs<128>(s);
+  if (rc) return rc;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     TcLay::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc128,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc128, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     100));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc128,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_tc128, 128,
+                                                             TcLay::BYTES));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 4) per_sm = 4;  // TMEM: 128 columns per CTA, 512 per SM
+  }
+  if (p.n_light > 0) {
+    const int grid = std::min(p.n_light, per_sm * kNumSMs);
+    k_sweep_tc128<<<grid, 128, TcLay::BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  if (p.n_heavy > 0) {
+    const int grid = std::min(p.n_slices, per_sm * kNumSMs);
+    k_heavy_partial_tc128<<<grid, 128, TcLay::BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    const int threads = L::NT * L::RPC;
+    k_heavy_solve<128><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    k_heavy_cache<128><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  return IALS_OK;
+}
+
 template <int BT>
 static int launch_sweep(ials_session* s, const SweepParams& p, cudaStream_t st) {
   using L = Lay<BT>;
+  if (BT == 128 && p.b > 32 && tc_enabled()) return launch_sweep_tc128(s, p, st);
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
   const int threads = L::NT * L::RPC;

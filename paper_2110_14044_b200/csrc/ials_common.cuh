@@ -9,6 +9,7 @@ namespace ials {
 
 constexpr int kNumSMs = 148;
 
+#define IALS_SMEM_U32_DEFINED
 IALS_DEVI uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

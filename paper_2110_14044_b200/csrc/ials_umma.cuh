@@ -1,0 +1,132 @@
+// ials_umma.cuh -- thin inline-PTX wrappers for the 5th-gen tensor core
+// (tcgen05.*), TMEM and mbarriers on sm_100a, plus the shared-memory operand
+// layouts the iALS++ kernels use.  Descriptor bit layouts follow the PTX ISA
+// (shared-memory matrix descriptor, instruction descriptor for kind::tf32).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef IALS_DEVI
+#define IALS_DEVI __device__ __forceinline__
+#endif
+
+namespace ials {
+
+#ifndef IALS_SMEM_U32_DEFINED
+#define IALS_SMEM_U32_DEFINED
+IALS_DEVI uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+#endif
+
+constexpr uint32_t kSwizzleNone = 0;   // layout_type field values
+constexpr uint32_t kSwizzle128B = 2;
+
+// ---------------------------------------------------------------- layouts
+// MN-major, 128-byte swizzle (tf32): atoms of 8 K-rows x 32 MN-elements
+// (1 KB, 1024-byte aligned); inside an atom the 16-byte chunk c of K-row r
+// sits at chunk c ^ r.  lbo / sbo are the float strides between MN-atoms /
+// K-atoms.  Returns the float index of element (m, k).
+IALS_DEVI int sw128_mn_index(int m, int k, int lbo, int sbo) {
+  const int r = k & 7, e = m & 31;
+  return (k >> 3) * sbo + (m >> 5) * lbo + r * 32 + (((e >> 2) ^ r) << 2) + (e & 3);
+}
+
+// K-major, no swizzle ("interleave"): core matrices of 8 MN-rows x 4 K-elements
+// (128 bytes); sbo / lbo are the float strides between 8-row groups / 4-element
+// K chunks.
+IALS_DEVI int kmaj_none_index(int m, int q, int sbo, int lbo) {
+  return (m >> 3) * sbo + (q >> 2) * lbo + (m & 7) * 4 + (q & 3);
+}
+
+// Shared-memory matrix descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version 1 [46,48), base offset 0, layout type [61,64).
+IALS_DEVI uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                              uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7) << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::tf32, fp32 accumulate: c_format [4,6)=1,
+// a_format [7,10)=2, b_format [10,13)=2, a_negate 13, a_major 15, b_major 16
+// (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
+IALS_DEVI uint32_t make_idesc_tf32(int M, int N, int a_mn, int b_mn, int a_neg) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_neg << 13) | ((uint32_t)a_mn << 15) |
+         ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ---------------------------------------------------------------- tcgen05
+IALS_DEVI void umma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                         int accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+IALS_DEVI void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+IALS_DEVI void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+IALS_DEVI void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+IALS_DEVI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// one full warp; writes the TMEM base address to *dst (shared)
+IALS_DEVI void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+IALS_DEVI void tmem_free(uint32_t base, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "r"(ncols));
+}
+
+IALS_DEVI void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+IALS_DEVI void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
+}
+IALS_DEVI void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+IALS_DEVI void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- mbarrier
+IALS_DEVI void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+IALS_DEVI void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// tf32 split: the tensor core uses the upper 19 bits of an fp32 operand, so
+// hi = x as stored and lo = x - trunc_tf32(x) (exact in fp32).
+IALS_DEVI float tf32_lo(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+}  // namespace ials

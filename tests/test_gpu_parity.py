@@ -164,3 +164,36 @@ def test_heavy_rows_vs_oracle(ials, d, b, I):
     orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 1)
     assert relf(model.user_factors, w) < TOL and relf(model.item_factors, h) < TOL
     assert relmax(model.user_factors, w) < TOL and relmax(model.item_factors, h) < TOL
+
+
+@pytest.mark.parametrize("d,b", [(128, 128), (200, 100), (96, 72), (128, 40)])
+def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
+    """b in (32, 128] runs the tcgen05 3xTF32 sweep; compare with the oracle
+    and with the FP32 SIMT sweep on the same input (2 epochs)."""
+    from oracle import ialspp_oracle as orc
+    from paper_2110_14044_b200 import _lib
+    lib = _lib.load()
+    U, I, users, items = _heavy_instance(3000, 900, 60, 1.0, 5)
+    data = ials.InteractionDataset(U, I, users, items)
+    cfg = ials.SolverConfig(dim=d, block_size=b, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=2, seed=2)
+    init = ials.init_model(cfg, U, I)
+    init.user_factors[:] = init.user_factors.astype(np.float32)
+    init.item_factors[:] = init.item_factors.astype(np.float32)
+    got = {}
+    try:
+        for tc in (1, 0):
+            lib.ials_set_tensor_cores(tc)
+            m = init.copy()
+            ials.train(m, data, cfg)
+            got[tc] = m
+    finally:
+        lib.ials_set_tensor_cores(0)
+    w, h = init.user_factors.copy(), init.item_factors.copy()
+    csr = orc.build_csr(U, I, users, items)
+    orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
+    for tc in (1, 0):
+        m = got[tc]
+        assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL, tc
+        assert relmax(m.user_factors, w) < TOL and relmax(m.item_factors, h) < TOL, tc
+    assert relf(got[1].user_factors, got[0].user_factors) < 1e-4
