@@ -110,6 +110,14 @@ int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const 
                      const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                      float* out, void* stream);
 
+/* Sharded path (dual-cache delta scheme): over a local CSR,
+ * out[e] += <A[row][b0 .. b0+b), D[cols[e]][0 .. b)> -- the score change
+ * that the other side's last half-epoch (delta D of its column block) caused.
+ * No reference counterpart (the reference is single-process). b <= 256. */
+int ials_cache_correct(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
+                       const float* A, int32_t lda, int32_t b0, const float* D, int32_t ldd,
+                       int32_t b, float* out, void* stream);
+
 /* slab[t][j] = sum_r M[r][t] * M[r][b0 + j]  (d x b, row-major, ld = b). */
 int ials_partial_gramian(ials_session* s, const float* M, int32_t n, int32_t ldm, int32_t d,
                          int32_t b0, int32_t b, float* slab, void* workspace, size_t ws_bytes,

@@ -199,6 +199,19 @@ int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const 
   return IALS_OK;
 }
 
+// ------------------------------------------------------------------ correction
+int ials_cache_correct(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
+                       const float* A, int32_t lda, int32_t b0, const float* D, int32_t ldd,
+                       int32_t b, float* out, void* stream) {
+  if (n_rows < 0 || b < 1 || b > 256 || b0 < 0 || lda < b0 + b || ldd < b)
+    return fail(s, IALS_E_INVALID, "cache_correct: bad shape (b0=%d b=%d)", b0, b);
+  if (n_rows == 0) return IALS_OK;
+  const int blocks = std::min((n_rows + 7) / 8, kNumSMs * 16);
+  k_cache_correct<<<blocks, 256, 0, S(stream)>>>(n_rows, ptr, cols, A, lda, b0, D, ldd, b, out);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
 // ------------------------------------------------------------------ gramian
 static int gramian_impl(ials_session* s, const float* M, int32_t n, int32_t ldm, int32_t d,
                         int32_t b0, int32_t b, float* slab, float* part, size_t part_bytes,

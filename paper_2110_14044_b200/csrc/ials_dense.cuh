@@ -72,6 +72,39 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------- K-corr
+// Dual-cache delta correction of the sharded path:
+// out[e] += <A[row, b0:b0+b], D[cols[e], 0:b]> over a (local) CSR, where D is
+// the change of the other side's column block in the previous half-epoch.
+__global__ void __launch_bounds__(256)
+    k_cache_correct(int n_rows, const int* __restrict__ ptr, const int* __restrict__ cols,
+                    const float* __restrict__ A, int lda, int b0, const float* __restrict__ D,
+                    int ldd, int b, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int row = gw; row < n_rows; row += nw) {
+    const float* ar = A + (size_t)row * lda + b0;
+    float areg[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int j = lane + 32 * m;
+      areg[m] = j < b ? ar[j] : 0.f;
+    }
+    for (int e = ptr[row]; e < ptr[row + 1]; ++e) {
+      const float* dr = D + (size_t)cols[e] * ldd;
+      float s = 0.f;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int j = lane + 32 * m;
+        if (j < b) s = fmaf(areg[m], __ldg(dr + j), s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) out[e] += s;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K-slab
 // partial_gramian (linalg.py:39-45): slab[t][j] = sum_r M[r][t] M[r][b0+j].
 // Split-K over rows; each CTA writes a 64x64 partial tile, a second kernel

@@ -1,0 +1,261 @@
+"""Multi-GPU iALS++ epoch: row shards, replicated tables, NCCL collectives.
+
+SURVEY.md §8e.  One process per GPU (``torch.distributed``).  Users and items
+are split into contiguous, nnz-balanced shards; W and H are replicated on every
+rank.  Per block pi:
+
+  1. slab(H)[:, pi]: partial over the local item rows -> all-reduce (d x b)
+  2. user sweep on the local user rows
+  3. all-gather of the updated column block W[:, pi] (U_r x b per rank)
+  4. slab(W)[:, pi]: partial over the local user rows -> all-reduce
+  5. item sweep on the local item rows
+  6. all-gather of H[:, pi]
+
+Score caches are never moved (dual-cache delta scheme): each rank keeps C_u
+(its users' entries, user-major) and C_i (its items' entries, item-major),
+both recomputed at epoch start.  The reference's single cache is updated by
+every pass for every entry; here, before a pass, the local cache is corrected
+for the other side's last half-epoch:
+
+  user pass of block pi : C_u[k] += <W[u, pi-1], dH[i, pi-1]>
+  item pass of block pi : C_i[k] += <H[i, pi],   dW[u, pi]>
+
+with dX = X_new - X_old of the column block that was just all-gathered.  In
+exact arithmetic this equals the reference's cache maintenance
+(``solvers.py:186``), so the iterates are the reference's (up to rounding).
+
+The compute steps go through an ``ops`` object: ``GpuOps`` (the product: the
+libials_b200 kernels, fp32) or, in tests only, a float64 CPU implementation
+wrapping the oracle, which lets the sharding / collective / correction logic
+be verified with the ``gloo`` backend on CPU (tests/test_distributed.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+__all__ = ["shard_bounds", "LocalSide", "ShardedTrainer", "GpuOps"]
+
+
+def shard_bounds(ptr, world, row_weight=0.0):
+    """Contiguous row ranges [lo_r, hi_r) balancing nnz (+ row_weight per row)."""
+    ptr = np.asarray(ptr, dtype=np.int64)
+    n = ptr.size - 1
+    cost = ptr.astype(np.float64) + row_weight * np.arange(n + 1)
+    targets = cost[-1] * np.arange(world + 1) / world
+    cuts = np.searchsorted(cost, targets, side="left")
+    cuts[0], cuts[-1] = 0, n
+    cuts = np.maximum.accumulate(np.clip(cuts, 0, n))
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+@dataclass
+class LocalSide:
+    """Rows [lo, hi) of one side: a rebased CSR whose entries index the local
+    cache (identity positions), cols = global ids of the other side."""
+
+    lo: int
+    hi: int
+    ptr: np.ndarray       # (hi - lo + 1,) int64, ptr[0] == 0
+    cols: np.ndarray      # global ids of the fixed side
+    labels: np.ndarray | None
+    weights: np.ndarray | None
+    lam: np.ndarray       # effective regularizer of the local rows
+    base: int             # offset of the first local entry in the full side view
+    n_fixed: int
+
+    @property
+    def n_rows(self):
+        return self.hi - self.lo
+
+    @property
+    def nnz(self):
+        return int(self.ptr[-1])
+
+
+def make_local_side(ptr, cols, labels, weights, lam, lo, hi, n_fixed):
+    ptr = np.asarray(ptr, dtype=np.int64)
+    s, e = int(ptr[lo]), int(ptr[hi])
+    return LocalSide(lo, hi, ptr[lo:hi + 1] - s, np.asarray(cols[s:e]),
+                     None if labels is None else np.asarray(labels[s:e]),
+                     None if weights is None else np.asarray(weights[s:e]),
+                     np.asarray(lam[lo:hi]), s, n_fixed)
+
+
+class GpuOps:
+    """The product compute path: libials_b200 kernels on this rank's GPU."""
+
+    def __init__(self, device):
+        from .engine import Session
+        self.device = torch.device(device)
+        self.sess = Session(self.device.index or 0)
+        self.dtype = torch.float32
+        self._sides = {}
+        self._ws = None
+
+    def _dev(self, side: LocalSide):
+        key = id(side)
+        if key not in self._sides:
+            from .engine import DeviceSide
+            ds = DeviceSide(self.device, side.ptr, side.cols, side.labels, side.weights, None,
+                            side.lam, side.n_fixed)
+            self._sides[key] = ds
+        return self._sides[key]
+
+    def _workspace(self, nbytes):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _stream(self):
+        from .engine import current_stream_handle
+        return current_stream_handle(self.device)
+
+    def predictions(self, side, A_rows, B, out):
+        from .engine import _ptr
+        ds = self._dev(side)
+        rc = self.sess.lib.ials_predictions(self.sess.handle, ds.n_rows, _ptr(ds.ptr), _ptr(ds.cols),
+                                            _ptr(A_rows), A_rows.stride(0), _ptr(B), B.stride(0),
+                                            A_rows.shape[1], _ptr(out), self._stream())
+        self.sess.check(rc, "predictions")
+
+    def correct(self, side, A_rows, b0, D, out):
+        from .engine import _ptr
+        ds = self._dev(side)
+        rc = self.sess.lib.ials_cache_correct(self.sess.handle, ds.n_rows, _ptr(ds.ptr),
+                                              _ptr(ds.cols), _ptr(A_rows), A_rows.stride(0), b0,
+                                              _ptr(D), D.stride(0), D.shape[1], _ptr(out),
+                                              self._stream())
+        self.sess.check(rc, "cache_correct")
+
+    def gram(self, M_rows, b0, b):
+        from .engine import _ptr
+        d = M_rows.shape[1]
+        out = torch.empty((d, b), dtype=self.dtype, device=self.device)
+        if M_rows.shape[0] == 0:
+            return out.zero_()
+        ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(1, M_rows.shape[0], d, b, 0, 0)))
+        rc = self.sess.lib.ials_partial_gramian(self.sess.handle, _ptr(M_rows), M_rows.shape[0],
+                                                M_rows.stride(0), d, b0, b, _ptr(out), _ptr(ws),
+                                                ws.numel(), self._stream())
+        self.sess.check(rc, "partial_gramian")
+        return out
+
+    def sweep(self, side, fixed, own_rows, b0, b, slab, alpha0, cache, side_id):
+        from .engine import _ptr
+        import ctypes
+        ds = self._dev(side)
+        sch = ds.schedule(b)
+        d = own_rows.shape[1]
+        ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(
+            max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)))
+        rc = self.sess.lib.ials_side_pass(self.sess.handle, ctypes.byref(ds.struct),
+                                          ctypes.byref(sch.struct), _ptr(fixed), fixed.stride(0),
+                                          _ptr(own_rows), own_rows.stride(0), d, b0, b,
+                                          _ptr(slab), float(alpha0), _ptr(cache), side_id,
+                                          _ptr(ws), ws.numel(), self._stream())
+        self.sess.check(rc, "side_pass")
+
+    def check(self):
+        self.sess.raise_if_singular()
+
+
+class ShardedTrainer:
+    """One rank's share of a sharded iALS++ run (call collectively on all ranks)."""
+
+    def __init__(self, data, W, H, alpha0, reg, exponent, ops, group=None):
+        self.ops = ops
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.alpha0 = float(alpha0)
+        U, I = int(data["num_users"]), int(data["num_items"])
+        self.U, self.I = U, I
+        up, ip = np.asarray(data["user_ptr"]), np.asarray(data["item_ptr"])
+        lam_u = reg * (np.diff(up) + alpha0 * I) ** exponent
+        lam_i = reg * (np.diff(ip) + alpha0 * U) ** exponent
+        self.user_bounds = shard_bounds(up, self.world)
+        self.item_bounds = shard_bounds(ip, self.world, row_weight=1.0)
+        ulo, uhi = self.user_bounds[self.rank]
+        ilo, ihi = self.item_bounds[self.rank]
+        self.us = make_local_side(up, data["user_cols"], data.get("labels"), data.get("weights"),
+                                  lam_u, ulo, uhi, I)
+        order = np.asarray(data["item_order"])
+        lab_i = None if data.get("labels") is None else np.asarray(data["labels"])[order]
+        wt_i = None if data.get("weights") is None else np.asarray(data["weights"])[order]
+        self.is_ = make_local_side(ip, data["item_cols"], lab_i, wt_i, lam_i, ilo, ihi, U)
+        self.W, self.H = W, H          # replicated full tables (this rank's device)
+        dev, dt = W.device, W.dtype
+        self.Cu = torch.zeros(self.us.nnz, dtype=dt, device=dev)
+        self.Ci = torch.zeros(self.is_.nnz, dtype=dt, device=dev)
+        self._umax = max(h - l for l, h in self.user_bounds)
+        self._imax = max(h - l for l, h in self.item_bounds)
+
+    # ---------------------------------------------------------------- comms
+    def _allreduce(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def _allgather_block(self, X, bounds, nmax, b0, b):
+        """All-gather rows [lo_r, hi_r) of the column block X[:, b0:b0+b]."""
+        lo, hi = bounds[self.rank]
+        if self.world == 1:
+            return
+        send = torch.zeros((nmax, b), dtype=X.dtype, device=X.device)
+        send[: hi - lo] = X[lo:hi, b0:b0 + b]
+        recv = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(recv, send, group=self.group)
+        for r, (l, h) in enumerate(bounds):
+            if r != self.rank and h > l:
+                X[l:h, b0:b0 + b] = recv[r][: h - l]
+
+    # ---------------------------------------------------------------- epoch
+    def epoch(self, block_size):
+        W, H, ops = self.W, self.H, self.ops
+        d = W.shape[1]
+        ulo, uhi = self.user_bounds[self.rank]
+        ilo, ihi = self.item_bounds[self.rank]
+        Wl, Hl = W[ulo:uhi], H[ilo:ihi]
+        ops.predictions(self.us, Wl, H, self.Cu)
+        ops.predictions(self.is_, Hl, W, self.Ci)
+        prev = None        # (b0, b, dH) of the last item pass
+        for b0 in range(0, d, block_size):
+            b = min(block_size, d - b0)
+            # ---- user pass
+            if prev is not None:
+                ops.correct(self.us, Wl, prev[0], prev[2], self.Cu)
+            slab = self._allreduce(ops.gram(Hl, b0, b))
+            w_old = W[:, b0:b0 + b].clone()
+            ops.sweep(self.us, H, Wl, b0, b, slab, self.alpha0, self.Cu, 0)
+            self._allgather_block(W, self.user_bounds, self._umax, b0, b)
+            dW = W[:, b0:b0 + b] - w_old
+            # ---- item pass
+            ops.correct(self.is_, Hl, b0, dW, self.Ci)
+            slab = self._allreduce(ops.gram(Wl, b0, b))
+            h_old = H[:, b0:b0 + b].clone()
+            ops.sweep(self.is_, W, Hl, b0, b, slab, self.alpha0, self.Ci, 1)
+            self._allgather_block(H, self.item_bounds, self._imax, b0, b)
+            prev = (b0, b, H[:, b0:b0 + b] - h_old)
+        # bring C_u up to date with the last item pass
+        if prev is not None:
+            ops.correct(self.us, Wl, prev[0], prev[2], self.Cu)
+
+    def gather_cache(self):
+        """The canonical (user-major) cache, assembled on every rank."""
+        if self.world == 1:
+            return self.Cu.clone()
+        nmax = max(int(self.us.nnz), 1)
+        sizes = torch.tensor([self.us.nnz], device=self.Cu.device)
+        all_sizes = [torch.zeros_like(sizes) for _ in range(self.world)]
+        dist.all_gather(all_sizes, sizes, group=self.group)
+        nmax = int(max(s.item() for s in all_sizes))
+        send = torch.zeros(max(nmax, 1), dtype=self.Cu.dtype, device=self.Cu.device)
+        send[: self.us.nnz] = self.Cu
+        recv = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(recv, send, group=self.group)
+        return torch.cat([recv[r][: int(all_sizes[r].item())] for r in range(self.world)])

@@ -197,3 +197,29 @@ def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
         assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL, tc
         assert relmax(m.user_factors, w) < TOL and relmax(m.item_factors, h) < TOL, tc
     assert relf(got[1].user_factors, got[0].user_factors) < 1e-4
+
+
+def test_sharded_path_gpu_ops_single_rank(ials):
+    """The multi-GPU orchestration with the real kernels (GpuOps, fp32) at
+    world size 1: local sides, the item-major cache C_i and the delta
+    corrections (k_cache_correct) against the oracle."""
+    import torch
+    from oracle import ialspp_oracle as orc
+    from paper_2110_14044_b200.distributed import GpuOps, ShardedTrainer
+    U, I, users, items = _heavy_instance(2500, 700, 40, 1.0, 9)
+    csr = orc.build_csr(U, I, users, items)
+    data = {"num_users": U, "num_items": I, "user_ptr": csr["user_ptr"], "user_cols": csr["items"],
+            "item_ptr": csr["item_ptr"], "item_cols": csr["users"][csr["item_order"]],
+            "item_order": csr["item_order"], "labels": None, "weights": None}
+    d, b = 48, 16
+    w, h = orc.init_factors(U, I, d, 0.1, 4)
+    w, h = w.astype(np.float32).astype(np.float64), h.astype(np.float32).astype(np.float64)
+    W = torch.from_numpy(w.astype(np.float32)).cuda()
+    H = torch.from_numpy(h.astype(np.float32)).cuda()
+    tr = ShardedTrainer(data, W, H, 0.1, 1e-3, 1.0, GpuOps("cuda:0"))
+    for _ in range(2):
+        tr.epoch(b)
+    cache = tr.gather_cache().double().cpu().numpy()
+    ref_cache = orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
+    assert relf(W.double().cpu().numpy(), w) < TOL and relf(H.double().cpu().numpy(), h) < TOL
+    assert relmax(cache, ref_cache) < TOL
