@@ -110,11 +110,21 @@ int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const 
                      const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                      float* out, void* stream);
 
-/* Sharded path (dual-cache delta scheme): over a local CSR,
- * out[e] += <A[row][b0 .. b0+b), D[cols[e]][0 .. b)> -- the score change
- * that the other side's last half-epoch (delta D of its column block) caused.
- * No reference counterpart (the reference is single-process). b <= 256. */
-int ials_cache_correct(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
+/* Same as ials_predictions over a list of row segments: segment t covers
+ * entries [seg_beg[t], seg_end[t]) of row seg_row[t] (long rows spread over
+ * many warps; used for the item-major cache of the sharded path). */
+int ials_predictions_segments(ials_session* s, int32_t n_seg, const int32_t* seg_row,
+                              const int32_t* seg_beg, const int32_t* seg_end, const int32_t* cols,
+                              const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                              float* out, void* stream);
+
+/* Sharded path (dual-cache delta scheme): over row segments
+ * of a local CSR, out[e] += <A[row][b0 .. b0+b), D[cols[e]][0 .. b)> -- the
+ * score change the other side's last half-epoch (delta D of its column
+ * block) caused.  No reference counterpart (the reference is single-process).
+ * b <= 256. */
+int ials_cache_correct(ials_session* s, int32_t n_seg, const int32_t* seg_row,
+                       const int32_t* seg_beg, const int32_t* seg_end, const int32_t* cols,
                        const float* A, int32_t lda, int32_t b0, const float* D, int32_t ldd,
                        int32_t b, float* out, void* stream);
 

@@ -50,8 +50,10 @@ SIGNATURES = {
     "ials_slice_len": (c_i64, [c_i32]),
     "ials_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
     "ials_predictions": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_i32, c_p, c_i32, c_i32, c_p, c_p]),
-    "ials_cache_correct": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_i32, c_i32, c_p, c_i32, c_i32,
-                                   c_p, c_p]),
+    "ials_predictions_segments": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_i32, c_p, c_i32,
+                                          c_i32, c_p, c_p]),
+    "ials_cache_correct": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_i32, c_i32, c_p, c_i32,
+                                   c_i32, c_p, c_p]),
     "ials_partial_gramian": (c_i32, [c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_p, c_p,
                                      c_sz, c_p]),
     "ials_side_pass": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p,

@@ -152,23 +152,45 @@ size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, 
 
 // ------------------------------------------------------------------ predictions
 template <int LPN>
-static void launch_pred_lpn(int nv, dim3 g, dim3 t, cudaStream_t st, int n_rows, const int* ptr,
+static void launch_pred_lpn(int nv, dim3 g, dim3 t, cudaStream_t st, int n_items, Items it,
                             const int* cols, const float* W, int ldw, const float* H, int ldh,
                             int d, float* out) {
   switch (nv) {
-    case 1: k_pred_vec<LPN, 1><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-    case 2: k_pred_vec<LPN, 2><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-    case 4: k_pred_vec<LPN, 4><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-    case 8: k_pred_vec<LPN, 8><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-    default: k_pred_vec<LPN, 16><<<g, t, 0, st>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+    case 1: k_pred_vec<LPN, 1><<<g, t, 0, st>>>(n_items, it, cols, W, ldw, H, ldh, d, out); break;
+    case 2: k_pred_vec<LPN, 2><<<g, t, 0, st>>>(n_items, it, cols, W, ldw, H, ldh, d, out); break;
+    case 4: k_pred_vec<LPN, 4><<<g, t, 0, st>>>(n_items, it, cols, W, ldw, H, ldh, d, out); break;
+    case 8: k_pred_vec<LPN, 8><<<g, t, 0, st>>>(n_items, it, cols, W, ldw, H, ldh, d, out); break;
+    default: k_pred_vec<LPN, 16><<<g, t, 0, st>>>(n_items, it, cols, W, ldw, H, ldh, d, out); break;
   }
 }
+
+static int predictions_impl(ials_session* s, int32_t n_items, Items it, const int32_t* cols,
+                            const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                            float* out, void* stream);
 
 int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
                      const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                      float* out, void* stream) {
-  if (n_rows < 0 || d < 1 || ldw < d || ldh < d)
-    return fail(s, IALS_E_INVALID, "predictions: bad shape (n_rows=%d d=%d)", n_rows, d);
+  if (n_rows < 0) return fail(s, IALS_E_INVALID, "predictions: n_rows < 0");
+  return predictions_impl(s, n_rows, Items{ptr, nullptr, nullptr, nullptr}, cols, W, ldw, H, ldh,
+                          d, out, stream);
+}
+
+int ials_predictions_segments(ials_session* s, int32_t n_seg, const int32_t* seg_row,
+                              const int32_t* seg_beg, const int32_t* seg_end, const int32_t* cols,
+                              const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                              float* out, void* stream) {
+  if (n_seg < 0 || (n_seg > 0 && (!seg_row || !seg_beg || !seg_end)))
+    return fail(s, IALS_E_INVALID, "predictions_segments: bad segment list");
+  return predictions_impl(s, n_seg, Items{nullptr, seg_row, seg_beg, seg_end}, cols, W, ldw, H,
+                          ldh, d, out, stream);
+}
+
+static int predictions_impl(ials_session* s, int32_t n_rows, Items it, const int32_t* cols,
+                            const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
+                            float* out, void* stream) {
+  if (d < 1 || ldw < d || ldh < d)
+    return fail(s, IALS_E_INVALID, "predictions: bad shape (d=%d)", d);
   if (n_rows == 0) return IALS_OK;
   const int warps_needed = n_rows;
   const int blocks = std::min((warps_needed + 7) / 8, kNumSMs * 16);
@@ -185,29 +207,31 @@ int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const 
     if (nvp > 16) { lpn = 32; nvp = 16; }
     dim3 g(blocks), t(256);
     switch (lpn) {
-      case 1: launch_pred_lpn<1>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-      case 2: launch_pred_lpn<2>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-      case 4: launch_pred_lpn<4>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-      case 8: launch_pred_lpn<8>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-      case 16: launch_pred_lpn<16>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
-      default: launch_pred_lpn<32>(nvp, g, t, S(stream), n_rows, ptr, cols, W, ldw, H, ldh, d, out); break;
+      case 1: launch_pred_lpn<1>(nvp, g, t, S(stream), n_rows, it, cols, W, ldw, H, ldh, d, out); break;
+      case 2: launch_pred_lpn<2>(nvp, g, t, S(stream), n_rows, it, cols, W, ldw, H, ldh, d, out); break;
+      case 4: launch_pred_lpn<4>(nvp, g, t, S(stream), n_rows, it, cols, W, ldw, H, ldh, d, out); break;
+      case 8: launch_pred_lpn<8>(nvp, g, t, S(stream), n_rows, it, cols, W, ldw, H, ldh, d, out); break;
+      case 16: launch_pred_lpn<16>(nvp, g, t, S(stream), n_rows, it, cols, W, ldw, H, ldh, d, out); break;
+      default: launch_pred_lpn<32>(nvp, g, t, S(stream), n_rows, it, cols, W, ldw, H, ldh, d, out); break;
     }
   } else {
-    k_pred_scalar<<<blocks, 256, 0, S(stream)>>>(n_rows, ptr, cols, W, ldw, H, ldh, d, out);
+    k_pred_scalar<<<blocks, 256, 0, S(stream)>>>(n_rows, it, cols, W, ldw, H, ldh, d, out);
   }
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
 
 // ------------------------------------------------------------------ correction
-int ials_cache_correct(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
+int ials_cache_correct(ials_session* s, int32_t n_seg, const int32_t* seg_row,
+                       const int32_t* seg_beg, const int32_t* seg_end, const int32_t* cols,
                        const float* A, int32_t lda, int32_t b0, const float* D, int32_t ldd,
                        int32_t b, float* out, void* stream) {
-  if (n_rows < 0 || b < 1 || b > 256 || b0 < 0 || lda < b0 + b || ldd < b)
+  if (n_seg < 0 || b < 1 || b > 256 || b0 < 0 || lda < b0 + b || ldd < b)
     return fail(s, IALS_E_INVALID, "cache_correct: bad shape (b0=%d b=%d)", b0, b);
-  if (n_rows == 0) return IALS_OK;
-  const int blocks = std::min((n_rows + 7) / 8, kNumSMs * 16);
-  k_cache_correct<<<blocks, 256, 0, S(stream)>>>(n_rows, ptr, cols, A, lda, b0, D, ldd, b, out);
+  if (n_seg == 0) return IALS_OK;
+  const int blocks = std::min((n_seg + 7) / 8, kNumSMs * 16);
+  k_cache_correct<<<blocks, 256, 0, S(stream)>>>(n_seg, Items{nullptr, seg_row, seg_beg, seg_end},
+                                                 cols, A, lda, b0, D, ldd, b, out);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }

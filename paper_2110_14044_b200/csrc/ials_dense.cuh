@@ -9,9 +9,26 @@ namespace ials {
 // compute_predictions (model.py:153-165): out[e] = <W[row], H[cols[e]]> over
 // the user-major CSR.  One warp per row (grid-stride); a group of LPN lanes
 // per entry, each lane holding NV float4 of the row of W in registers.
+// Work items are rows (seg_row == nullptr: item t = row t, entries ptr[t..t+1))
+// or row segments (row seg_row[t], entries [seg_beg[t], seg_end[t])) so that a
+// long row is spread over many warps.
+struct Items {
+  const int* ptr;
+  const int* seg_row;
+  const int* seg_beg;
+  const int* seg_end;
+  IALS_DEVI void get(int t, int& row, int& e0, int& e1) const {
+    if (seg_row) {
+      row = __ldg(seg_row + t); e0 = __ldg(seg_beg + t); e1 = __ldg(seg_end + t);
+    } else {
+      row = t; e0 = __ldg(ptr + t); e1 = __ldg(ptr + t + 1);
+    }
+  }
+};
+
 template <int LPN, int NV>
 __global__ void __launch_bounds__(256)
-    k_pred_vec(int n_rows, const int* __restrict__ ptr, const int* __restrict__ cols,
+    k_pred_vec(int n_items, Items it, const int* __restrict__ cols,
                const float* __restrict__ W, int ldw, const float* __restrict__ H, int ldh,
                int d, float* __restrict__ out) {
   constexpr int GPW = 32 / LPN;
@@ -20,7 +37,9 @@ __global__ void __launch_bounds__(256)
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int sub = lane / LPN, gl = lane % LPN;
   const int d4 = d >> 2;
-  for (int row = gw; row < n_rows; row += nw) {
+  for (int t = gw; t < n_items; t += nw) {
+    int row, e0, e1;
+    it.get(t, row, e0, e1);
     float4 w[NV];
     const float4* wr = reinterpret_cast<const float4*>(W + (size_t)row * ldw);
 #pragma unroll
@@ -28,7 +47,6 @@ __global__ void __launch_bounds__(256)
       const int v = gl + m * LPN;
       w[m] = v < d4 ? __ldg(wr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int e0 = __ldg(ptr + row), e1 = __ldg(ptr + row + 1);
     for (int eb = e0; eb < e1; eb += GPW) {
       const int e = eb + sub;
       float s = 0.f;
@@ -53,15 +71,16 @@ __global__ void __launch_bounds__(256)
 }
 
 __global__ void __launch_bounds__(256)
-    k_pred_scalar(int n_rows, const int* __restrict__ ptr, const int* __restrict__ cols,
+    k_pred_scalar(int n_items, Items it, const int* __restrict__ cols,
                   const float* __restrict__ W, int ldw, const float* __restrict__ H, int ldh,
                   int d, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int row = gw; row < n_rows; row += nw) {
+  for (int t = gw; t < n_items; t += nw) {
+    int row, e0, e1;
+    it.get(t, row, e0, e1);
     const float* wr = W + (size_t)row * ldw;
-    const int e0 = ptr[row], e1 = ptr[row + 1];
     for (int e = e0; e < e1; ++e) {
       const float* hr = H + (size_t)cols[e] * ldh;
       float s = 0.f;
@@ -77,13 +96,15 @@ __global__ void __launch_bounds__(256)
 // out[e] += <A[row, b0:b0+b], D[cols[e], 0:b]> over a (local) CSR, where D is
 // the change of the other side's column block in the previous half-epoch.
 __global__ void __launch_bounds__(256)
-    k_cache_correct(int n_rows, const int* __restrict__ ptr, const int* __restrict__ cols,
+    k_cache_correct(int n_items, Items it, const int* __restrict__ cols,
                     const float* __restrict__ A, int lda, int b0, const float* __restrict__ D,
                     int ldd, int b, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int row = gw; row < n_rows; row += nw) {
+  for (int t = gw; t < n_items; t += nw) {
+    int row, e0, e1;
+    it.get(t, row, e0, e1);
     const float* ar = A + (size_t)row * lda + b0;
     float areg[8];
 #pragma unroll
@@ -91,7 +112,7 @@ __global__ void __launch_bounds__(256)
       const int j = lane + 32 * m;
       areg[m] = j < b ? ar[j] : 0.f;
     }
-    for (int e = ptr[row]; e < ptr[row + 1]; ++e) {
+    for (int e = e0; e < e1; ++e) {
       const float* dr = D + (size_t)cols[e] * ldd;
       float s = 0.f;
 #pragma unroll

@@ -97,12 +97,22 @@ class GpuOps:
         self._sides = {}
         self._ws = None
 
+    SEG = 256   # entries per row segment of the gather-dot kernels
+
     def _dev(self, side: LocalSide):
         key = id(side)
         if key not in self._sides:
             from .engine import DeviceSide
             ds = DeviceSide(self.device, side.ptr, side.cols, side.labels, side.weights, None,
                             side.lam, side.n_fixed)
+            counts = np.diff(side.ptr)
+            nseg = (counts + self.SEG - 1) // self.SEG
+            row = np.repeat(np.arange(side.n_rows), nseg)
+            first = np.concatenate([[0], np.cumsum(nseg)[:-1]])
+            beg = side.ptr[:-1][row] + (np.arange(row.size) - first[row]) * self.SEG
+            end = np.minimum(beg + self.SEG, side.ptr[1:][row])
+            to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(self.device)
+            ds.segs = (int(row.size), to(row), to(beg), to(end))
             self._sides[key] = ds
         return self._sides[key]
 
@@ -118,15 +128,17 @@ class GpuOps:
     def predictions(self, side, A_rows, B, out):
         from .engine import _ptr
         ds = self._dev(side)
-        rc = self.sess.lib.ials_predictions(self.sess.handle, ds.n_rows, _ptr(ds.ptr), _ptr(ds.cols),
-                                            _ptr(A_rows), A_rows.stride(0), _ptr(B), B.stride(0),
-                                            A_rows.shape[1], _ptr(out), self._stream())
+        n, r, bg, en = ds.segs
+        rc = self.sess.lib.ials_predictions_segments(
+            self.sess.handle, n, _ptr(r), _ptr(bg), _ptr(en), _ptr(ds.cols), _ptr(A_rows),
+            A_rows.stride(0), _ptr(B), B.stride(0), A_rows.shape[1], _ptr(out), self._stream())
         self.sess.check(rc, "predictions")
 
     def correct(self, side, A_rows, b0, D, out):
         from .engine import _ptr
         ds = self._dev(side)
-        rc = self.sess.lib.ials_cache_correct(self.sess.handle, ds.n_rows, _ptr(ds.ptr),
+        n, r, bg, en = ds.segs
+        rc = self.sess.lib.ials_cache_correct(self.sess.handle, n, _ptr(r), _ptr(bg), _ptr(en),
                                               _ptr(ds.cols), _ptr(A_rows), A_rows.stride(0), b0,
                                               _ptr(D), D.stride(0), D.shape[1], _ptr(out),
                                               self._stream())
