@@ -30,10 +30,15 @@ class IalsSide(ctypes.Structure):
 
 
 class IalsSched(ctypes.Structure):
-    """``ials_sched`` (light / heavy row schedule of one side)."""
+    """``ials_sched`` (light / heavy row schedule of one side + tensor-core plan)."""
     _fields_ = [("n_light", c_i32), ("light_rows", c_p), ("n_heavy", c_i32),
                 ("heavy_rows", c_p), ("heavy_slice0", c_p), ("n_slices", c_i32),
-                ("slice_heavy", c_p), ("slice_begin", c_p), ("slice_end", c_p)]
+                ("slice_heavy", c_p), ("slice_begin", c_p), ("slice_end", c_p),
+                ("tc_n_rows", c_i32), ("tc_rows", c_p), ("tc_row_slice0", c_p),
+                ("tc_n_slices", c_i32), ("tc_slice_row", c_p), ("tc_slice_begin", c_p),
+                ("tc_slice_end", c_p), ("tc_n_waves", c_i32), ("tc_wave_row0", c_p),
+                ("tc_wave_slice0", c_p), ("tc_max_wave_rows", c_i32),
+                ("tc_max_wave_slices", c_i32)]
 
 
 #: every symbol include/ials_b200.h declares, with its ctypes signature
@@ -49,6 +54,8 @@ SIGNATURES = {
     "ials_heavy_threshold": (c_i64, [c_i32]),
     "ials_slice_len": (c_i64, [c_i32]),
     "ials_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
+    "ials_tc_workspace_bytes": (c_sz, [c_i32, c_i32]),
+    "ials_tc_wave_slices": (c_i32, []),
     "ials_predictions": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_i32, c_p, c_i32, c_i32, c_p, c_p]),
     "ials_predictions_segments": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_i32, c_p, c_i32,
                                           c_i32, c_p, c_p]),

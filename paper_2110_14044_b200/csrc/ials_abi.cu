@@ -16,6 +16,7 @@
 #include "ials_sweep.cuh"
 #include "ials_loss.cuh"
 #include "ials_sweep_tc.cuh"
+#include "ials_sweep_tc2.cuh"
 
 using namespace ials;
 
@@ -135,6 +136,13 @@ static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
   (void)n;
   return al256(size_t(kMaxSplits) * d * b * sizeof(float));
 }
+
+size_t ials_tc_workspace_bytes(int32_t max_wave_rows, int32_t max_wave_slices) {
+  return al256(size_t(max_wave_slices) * kTcPKS * 4) + al256(size_t(max_wave_slices) * 128 * 8) +
+         al256(size_t(max_wave_rows) * 128 * 4);
+}
+
+int32_t ials_tc_wave_slices(void) { return 2560; }
 
 static size_t pass_ws(int32_t n_rows, int32_t b, int32_t n_slices, int32_t n_heavy) {
   const size_t bt = block_tile(b);
@@ -318,10 +326,18 @@ static int launch_sweep_tc128(ials_session* s, const SweepParams& p, cudaStream_
                                      100));
     CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc128,
                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_tc128, 128,
-                                                             TcLay::BYTES));
-    if (per_sm < 1) per_sm = 1;
-    if (per_sm > 4) per_sm = 4;  // TMEM: 128 columns per CTA, 512 per SM
+    // residency from the kernel's real resources (the occupancy API has been
+    // seen to under-report here): shared memory, registers, TMEM columns
+    cudaFuncAttributes fa;
+    CUDA_TRY(s, cudaFuncGetAttributes(&fa, k_sweep_tc128));
+    int dev = 0;
+    CUDA_TRY(s, cudaGetDevice(&dev));
+    int smem_sm = 0, regs_sm = 0;
+    CUDA_TRY(s, cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    CUDA_TRY(s, cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+    const int by_smem = smem_sm / (TcLay::BYTES + 1024);
+    const int by_regs = regs_sm / (((fa.numRegs + 7) / 8) * 8 * 128);
+    per_sm = std::max(1, std::min(std::min(by_smem, by_regs), 4));
   }
   if (p.n_light > 0) {
     const int grid = std::min(p.n_light, per_sm * kNumSMs);
@@ -337,6 +353,55 @@ static int launch_sweep_tc128(ials_session* s, const SweepParams& p, cudaStream_
     LAUNCH_CHECK(s);
     k_heavy_cache<128><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
+  }
+  return IALS_OK;
+}
+
+// residency of a 128-thread tensor-core kernel from its real resources
+template <typename K>
+static int tc_per_sm(ials_session* s, K kernel, int bytes, int* out) {
+  CUDA_TRY(s, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(s, cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  cudaFuncAttributes fa;
+  CUDA_TRY(s, cudaFuncGetAttributes(&fa, kernel));
+  int dev = 0, smem_sm = 0, regs_sm = 0;
+  CUDA_TRY(s, cudaGetDevice(&dev));
+  CUDA_TRY(s, cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  CUDA_TRY(s, cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+  const int by_smem = smem_sm / (bytes + 1024);
+  const int by_regs = regs_sm / (((fa.numRegs + 7) / 8) * 8 * 128);
+  *out = std::max(1, std::min(std::min(by_smem, by_regs), 32));
+  return IALS_OK;
+}
+
+static int launch_tc_waves(ials_session* s, SweepParams p, const ials_sched* sched,
+                           cudaStream_t st) {
+  static int h_sm = 0, f_sm = 0, c_sm = 0;
+  if (h_sm == 0) {
+    int rc = tc_per_sm(s, k_tc_hess, TcLayH::BYTES, &h_sm);
+    if (!rc) rc = tc_per_sm(s, k_tc_factor, TcLayF::BYTES, &f_sm);
+    if (!rc) rc = tc_per_sm(s, k_tc_cache, TcLayC::BYTES, &c_sm);
+    if (rc) return rc;
+    h_sm = std::min(h_sm, 4);  // TMEM: 128 columns per CTA
+    f_sm = std::min(f_sm, 4);
+  }
+  for (int w = 0; w < sched->tc_n_waves; ++w) {
+    p.w_r0 = sched->tc_wave_row0[w];
+    p.w_r1 = sched->tc_wave_row0[w + 1];
+    p.w_s0 = sched->tc_wave_slice0[w];
+    p.w_s1 = sched->tc_wave_slice0[w + 1];
+    const int ns = p.w_s1 - p.w_s0, nr = p.w_r1 - p.w_r0;
+    if (nr <= 0) continue;
+    if (ns > 0) {
+      k_tc_hess<<<std::min(ns, h_sm * kNumSMs), 128, TcLayH::BYTES, st>>>(p);
+      LAUNCH_CHECK(s);
+    }
+    k_tc_factor<<<std::min(nr, f_sm * kNumSMs), 128, TcLayF::BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    if (ns > 0) {
+      k_tc_cache<<<std::min(ns, c_sm * kNumSMs), 128, TcLayC::BYTES, st>>>(p);
+      LAUNCH_CHECK(s);
+    }
   }
   return IALS_OK;
 }
@@ -380,7 +445,11 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
     return fail(s, IALS_E_INVALID, "side_pass: bad block (d=%d b0=%d b=%d)", d, b0, b);
   const int bt = block_tile(b);
-  const size_t need = pass_ws(side->n_rows, b, sched->n_slices, sched->n_heavy);
+  const bool use_tc = bt == 128 && b > 32 && tc_enabled() && sched->tc_n_rows > 0;
+  const size_t need_simt = pass_ws(side->n_rows, b, sched->n_slices, sched->n_heavy);
+  const size_t need_tc = al256(size_t(side->n_rows) * b * 4) +
+                         ials_tc_workspace_bytes(sched->tc_max_wave_rows, sched->tc_max_wave_slices);
+  const size_t need = use_tc ? need_tc : need_simt;
   if (need > ws_bytes)
     return fail(s, IALS_E_NOMEM, "side_pass: workspace %zu < %zu bytes", ws_bytes, need);
   SweepParams p;
@@ -418,11 +487,30 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   w += al256(size_t(sched->n_slices) * bt * 8);
   p.hdelta = reinterpret_cast<float*>(w);
   p.proj = proj;
+  p.tc_rows = sched->tc_rows;
+  p.tc_row_slice0 = sched->tc_row_slice0;
+  p.tc_slice_row = sched->tc_slice_row;
+  p.tc_slice_beg = sched->tc_slice_begin;
+  p.tc_slice_end = sched->tc_slice_end;
+  p.w_r0 = p.w_r1 = p.w_s0 = p.w_s1 = 0;
+  if (use_tc) {  // tensor-core scratch follows proj
+    char* t = ws + al256(size_t(side->n_rows) * b * 4);
+    p.hbuf = reinterpret_cast<float*>(t);
+    t += al256(size_t(sched->tc_max_wave_slices) * kTcPKS * 4);
+    p.gbuf = reinterpret_cast<double*>(t);
+    t += al256(size_t(sched->tc_max_wave_slices) * 128 * 8);
+    p.dbuf = reinterpret_cast<float*>(t);
+  } else {
+    p.hbuf = nullptr;
+    p.gbuf = nullptr;
+    p.dbuf = nullptr;
+  }
   if (side->n_rows > 0) {
     dim3 g((side->n_rows + GT - 1) / GT, (b + GT - 1) / GT);
     k_project<<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, b, alpha0, proj);
     LAUNCH_CHECK(s);
   }
+  if (use_tc) return launch_tc_waves(s, p, sched, st);
   switch (bt) {
     case 8: return launch_sweep<8>(s, p, st);
     case 16: return launch_sweep<16>(s, p, st);

@@ -59,6 +59,17 @@ struct SweepParams {
   float* hpart;   // [n_slices][BT*BT]
   double* gpart;  // [n_slices][BT] (fp64: the gradient sum cancels strongly)
   float* hdelta;  // [n_heavy][BT]
+  // tensor-core wave plan (BT = 128): every row cut into slices, rows in
+  // descending degree; a wave is rows [w_r0, w_r1) = slices [w_s0, w_s1)
+  const int* tc_rows;
+  const int* tc_row_slice0;
+  const int* tc_slice_row;
+  const int* tc_slice_beg;
+  const int* tc_slice_end;
+  int w_r0, w_r1, w_s0, w_s1;
+  float* hbuf;    // [wave slices][8448] packed lower rows (4-aligned)
+  double* gbuf;   // [wave slices][128]
+  float* dbuf;    // [wave rows][128]
 };
 
 template <int BT>
@@ -463,7 +474,9 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
       const int c0 = pp * PW;
       float z[PW], dlt[PW];
 #pragma unroll
-      for (int q = 0; q < PW; ++q) z[q] = yf[c0 + q];
+      for (int q = 0; q < PW; ++q) z[q] = (c0 + q < b) ? yf[c0 + q] : 0.f;
+      // rows >= b are padding: their packed L entries outside the diagonal
+      // block were never written, so they must not be read (NaN * 0 = NaN)
 #pragma unroll
       for (int q = PW - 1; q >= 0; --q) {
         float v = z[q];
@@ -471,9 +484,9 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
 #pragma unroll
         for (int m = q + 1; m < PW; ++m) {
           const int gm = c0 + m;
-          v = fmaf(-Lp[gm * (gm + 1) / 2 + gq], dlt[m], v);
+          if (gm < b) v = fmaf(-Lp[gm * (gm + 1) / 2 + gq], dlt[m], v);
         }
-        dlt[q] = v * invd[gq];
+        dlt[q] = (gq < b) ? v * invd[gq] : 0.f;
       }
       if (lane < PW) {
 #pragma unroll
@@ -485,7 +498,7 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
 #pragma unroll
         for (int q = 0; q < PW; ++q) {
           const int gq = c0 + q;
-          v = fmaf(-Lp[gq * (gq + 1) / 2 + i], dlt[q], v);
+          if (gq < b) v = fmaf(-Lp[gq * (gq + 1) / 2 + i], dlt[q], v);
         }
         yf[i] = v;
       }

@@ -37,7 +37,9 @@ struct TcLay {
   static constexpr int LP = BT * (BT + 1) / 2;
   static constexpr int OFF_DG = OFF_L + ((LP * 4 + 15) / 16) * 16;  // 8x8 diagonal block
   static constexpr int OFF_PY = OFF_DG + 64 * 4;
-  static constexpr int OFF_Y = OFF_PY + 8 * 4;
+  static constexpr int OFF_RV = OFF_PY + 8 * 4;     // 1/diag of the panel
+  static constexpr int OFF_YP = OFF_RV + 8 * 4;     // forward-solved y of the panel
+  static constexpr int OFF_Y = OFF_YP + 8 * 4;
   static constexpr int OFF_YF = OFF_Y + BT * 4;
   static constexpr int OFF_ID = OFF_YF + BT * 4;
   static constexpr int OFF_D = OFF_ID + BT * 4;
@@ -121,9 +123,9 @@ IALS_DEVI void tc_flush(const TcState& st, float (&sum)[128], int tid) {
 // fp32 register row sum `sum` (thread i holds row i): a two-level sum, so the
 // tensor core's accumulation rounding only ever applies to one chunk's sum.
 // Returns the number of chunks.
+template <class L = TcLay>
 IALS_DEVI int tc_accumulate(const SweepParams& p, char* smem, TcState& st, double& gacc,
                             float (&sum)[128], int ebeg, int eend, int tid) {
-  using L = TcLay;
   float* XN = reinterpret_cast<float*>(smem + L::OFF_X);
   float* AW = reinterpret_cast<float*>(smem + L::OFF_AW);
   float* RH = reinterpret_cast<float*>(smem + L::OFF_RH);
@@ -272,8 +274,8 @@ IALS_DEVI void tc_store_rowsum(const TcState& st, const float (&sum)[128], int t
 
 // Cholesky of the TMEM matrix + forward solve; leaves L (packed) in smem,
 // y in OFF_YF, 1/diag in OFF_ID.  ys (OFF_Y) holds the gradient on entry.
+template <class L = TcLay>
 IALS_DEVI void tc_factor(const SweepParams& p, char* smem, TcState& st, int row, int tid) {
-  using L = TcLay;
   float* Lp = reinterpret_cast<float*>(smem + L::OFF_L);
   float* DG = reinterpret_cast<float*>(smem + L::OFF_DG);
   float* PY = reinterpret_cast<float*>(smem + L::OFF_PY);
@@ -300,39 +302,63 @@ IALS_DEVI void tc_factor(const SweepParams& p, char* smem, TcState& st, int row,
       PY[i - c0] = yi;
     }
     tc_cta_sync();
-    // redundant 8x8 factorisation of the diagonal block
-    float a[8][8];
+    // the warp holding the diagonal rows factors the 8x8 block once
+    float* RV = reinterpret_cast<float*>(smem + L::OFF_RV);
+    float* YP = reinterpret_cast<float*>(smem + L::OFF_YP);
+    if ((tid >> 5) == (c0 >> 5)) {
+      float a[8][8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < 8; ++q)
 #pragma unroll
-      for (int m = 0; m <= q; ++m) a[q][m] = DG[q * 8 + m];
-    float rinv[8];
-    int bad = -1;
+        for (int m = 0; m <= q; ++m) a[q][m] = DG[q * 8 + m];
+      float rinv[8];
+      int bad = -1;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float dk = a[k][k];
-      if (!(dk > 0.f) || !(dk < 3.0e38f)) {
-        if (bad < 0) bad = k;
-        dk = 1.f;
+      for (int k = 0; k < 8; ++k) {
+        float dk = a[k][k];
+        if (!(dk > 0.f) || !(dk < 3.0e38f)) {
+          if (bad < 0) bad = k;
+          dk = 1.f;
+        }
+        const float r = rsqrtf(dk);
+        rinv[k] = r;
+        a[k][k] = dk * r;
+#pragma unroll
+        for (int q = k + 1; q < 8; ++q) a[q][k] *= r;
+#pragma unroll
+        for (int q = k + 1; q < 8; ++q)
+#pragma unroll
+          for (int m = k + 1; m <= q; ++m) a[q][m] = fmaf(-a[q][k], a[m][k], a[q][m]);
       }
-      const float r = rsqrtf(dk);
-      rinv[k] = r;
-      a[k][k] = dk * r;
+      if (bad >= 0 && c0 + bad < b && (tid & 31) == 0)
+        report_singular(p.err, p.side_id, row, c0 + bad);
+      float yp[8];
 #pragma unroll
-      for (int q = k + 1; q < 8; ++q) a[q][k] *= r;
+      for (int q = 0; q < 8; ++q) {
+        float t = PY[q];
 #pragma unroll
-      for (int q = k + 1; q < 8; ++q)
+        for (int m = 0; m < q; ++m) t = fmaf(-a[q][m], yp[m], t);
+        yp[q] = t * rinv[q];
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) {
 #pragma unroll
-        for (int m = k + 1; m <= q; ++m) a[q][m] = fmaf(-a[q][k], a[m][k], a[q][m]);
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+          for (int m = 0; m < 8; ++m) DG[q * 8 + m] = (m <= q) ? a[q][m] : 0.f;
+          RV[q] = rinv[q];
+          YP[q] = yp[q];
+        }
+      }
     }
-    if (bad >= 0 && c0 + bad < b && tid == 0) report_singular(p.err, p.side_id, row, c0 + bad);
-    float yp[8];
+    tc_cta_sync();
+    float a[8][8], rinv[8], yp[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float t = PY[q];
 #pragma unroll
-      for (int m = 0; m < q; ++m) t = fmaf(-a[q][m], yp[m], t);
-      yp[q] = t * rinv[q];
+      for (int m = 0; m <= q; ++m) a[q][m] = DG[q * 8 + m];
+      rinv[q] = RV[q];
+      yp[q] = YP[q];
     }
     // this row's panel entries
     float l[8];
@@ -394,8 +420,8 @@ IALS_DEVI void tc_factor(const SweepParams& p, char* smem, TcState& st, int row,
 }
 
 // Backward solve L^T d = y (warp 0), identical to the SIMT kernel's.
+template <class L = TcLay>
 IALS_DEVI void tc_backward(const SweepParams& p, char* smem, int tid) {
-  using L = TcLay;
   const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L);
   float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
   const float* invd = reinterpret_cast<const float*>(smem + L::OFF_ID);
@@ -439,9 +465,9 @@ IALS_DEVI void tc_backward(const SweepParams& p, char* smem, int tid) {
   tc_cta_sync();
 }
 
+template <class L = TcLay>
 IALS_DEVI void tc_cache_update(const SweepParams& p, char* smem, int ebeg, int eend, int nch,
                                int tid) {
-  using L = TcLay;
   float* XN = reinterpret_cast<float*>(smem + L::OFF_X);
   float* AW = reinterpret_cast<float*>(smem + L::OFF_AW);
   float* RH = reinterpret_cast<float*>(smem + L::OFF_RH);

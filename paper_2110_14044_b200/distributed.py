@@ -164,7 +164,8 @@ class GpuOps:
         sch = ds.schedule(b)
         d = own_rows.shape[1]
         ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(
-            max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)))
+            max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)) +
+            int(self.sess.lib.ials_tc_workspace_bytes(sch.tc_max_wave_rows, sch.tc_max_wave_slices)))
         rc = self.sess.lib.ials_side_pass(self.sess.handle, ctypes.byref(ds.struct),
                                           ctypes.byref(sch.struct), _ptr(fixed), fixed.stride(0),
                                           _ptr(own_rows), own_rows.stride(0), d, b0, b,

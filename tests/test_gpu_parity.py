@@ -166,7 +166,8 @@ def test_heavy_rows_vs_oracle(ials, d, b, I):
     assert relmax(model.user_factors, w) < TOL and relmax(model.item_factors, h) < TOL
 
 
-@pytest.mark.parametrize("d,b", [(128, 128), (200, 100), (96, 72), (128, 40)])
+@pytest.mark.parametrize("d,b", [(128, 128), (200, 100), (96, 72), (128, 40), (120, 60),
+                                 (100, 98)])
 def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
     """b in (32, 128] runs the tcgen05 3xTF32 sweep; compare with the oracle
     and with the FP32 SIMT sweep on the same input (2 epochs)."""
