@@ -12,8 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libials_b200.so")
 SOURCES = ["ials_abi.cu"]
-DEPS = ["ials_abi.cu", "ials_common.cuh", "ials_dense.cuh", "ials_sweep.cuh", "ials_loss.cuh",
-        "ials_sweep_tc.cuh", "ials_umma.cuh"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

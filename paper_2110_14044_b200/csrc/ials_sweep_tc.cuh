@@ -109,12 +109,12 @@ IALS_DEVI void tc_cta_sync() { __syncthreads(); }
 IALS_DEVI void tc_flush(const TcState& st, float (&sum)[128], int tid) {
   const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
 #pragma unroll
-  for (int c0 = 0; c0 < 128; c0 += 8) {
-    float v[8];
-    tmem_ld8(row_addr + c0, v);
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    float v[32];
+    tmem_ld32(row_addr + c0, v);
     tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) sum[c0 + j] += v[j];
+    for (int j = 0; j < 32; ++j) sum[c0 + j] += v[j];
   }
 }
 
@@ -153,10 +153,17 @@ IALS_DEVI int tc_accumulate(const SweepParams& p, char* smem, TcState& st, doubl
     const float* aw = AW + buf * L::KC;
     const float* rh = RH + buf * L::KC;
     // fp64 gradient (thread j <-> column j)
-    {
-      double g = gacc;
-      for (int k = 0; k < nk; ++k) g = fma((double)rh[k], (double)X[k * L::XLD + tid], g);
-      gacc = g;
+    {  // four independent fp64 chains (DFMA latency), combined in a fixed order
+      double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+      int k = 0;
+      for (; k + 3 < nk; k += 4) {
+        g0 = fma((double)rh[k], (double)X[k * L::XLD + tid], g0);
+        g1 = fma((double)rh[k + 1], (double)X[(k + 1) * L::XLD + tid], g1);
+        g2 = fma((double)rh[k + 2], (double)X[(k + 2) * L::XLD + tid], g2);
+        g3 = fma((double)rh[k + 3], (double)X[(k + 3) * L::XLD + tid], g3);
+      }
+      for (; k < nk; ++k) g0 = fma((double)rh[k], (double)X[k * L::XLD + tid], g0);
+      gacc += (g0 + g1) + (g2 + g3);
     }
     // operands of the previous chunk must be consumed before overwriting;
     // its sum is then folded into the row sum

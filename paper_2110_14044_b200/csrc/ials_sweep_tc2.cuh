@@ -133,35 +133,63 @@ __global__ void __launch_bounds__(128) k_tc_factor(SweepParams p) {
     const int row = p.tc_rows[r];
     const int s_beg = p.tc_row_slice0[r], s_end = p.tc_row_slice0[r + 1];
     const float lam = p.side.lam[row];
-    const float* srow = p.slab + (size_t)(p.b0 + i) * b;
-    // Hessian row i (lower part) into TMEM, 8 columns at a time
+    // Hessian row i (lower part) = sum of the row's slice partials +
+    // alpha0 * slab + lam I; 32 columns per batch of loads
 #pragma unroll 1
-    for (int c8 = 0; c8 < 16; ++c8) {
-      float v[8];
+    for (int q = 0; q < 4; ++q) {
+      float v[32];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = 0.f;
-      if (8 * c8 <= i) {
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      if (32 * q <= i) {
         for (int s = s_beg; s < s_end; ++s) {
-          const float* hp = p.hbuf + (size_t)(s - p.w_s0) * kTcPKS + pk_off(i) + 8 * c8;
-          const float4 x0 = *reinterpret_cast<const float4*>(hp);
-          v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
-          if (8 * c8 + 4 <= i) {
-            const float4 x1 = *reinterpret_cast<const float4*>(hp + 4);
-            v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
+          const float* hp = p.hbuf + (size_t)(s - p.w_s0) * kTcPKS + pk_off(i) + 32 * q;
+          float4 x[8];
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            x[c4] = (32 * q + 4 * c4 <= i) ? *reinterpret_cast<const float4*>(hp + 4 * c4)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            v[4 * c4] += x[c4].x;
+            v[4 * c4 + 1] += x[c4].y;
+            v[4 * c4 + 2] += x[c4].z;
+            v[4 * c4 + 3] += x[c4].w;
           }
         }
       }
+      // + alpha0 * slab[pi, pi] + lam I on the b x b block, identity on padding
+      const float* srow = p.slab + (size_t)(p.b0 + i) * b + 32 * q;
+      if (i < b && (b & 3) == 0) {
+        float4 y[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int c = 8 * c8 + j;
+        for (int c4 = 0; c4 < 8; ++c4)
+          y[c4] = (32 * q + 4 * c4 < b) ? __ldg(reinterpret_cast<const float4*>(srow) + c4)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          v[4 * c4] = fmaf(a0, y[c4].x, v[4 * c4]);
+          v[4 * c4 + 1] = fmaf(a0, y[c4].y, v[4 * c4 + 1]);
+          v[4 * c4 + 2] = fmaf(a0, y[c4].z, v[4 * c4 + 2]);
+          v[4 * c4 + 3] = fmaf(a0, y[c4].w, v[4 * c4 + 3]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = 32 * q + j;
         if (i < b && c < b) {
-          v[j] += a0 * __ldg(srow + c);
+          if ((b & 3) != 0) v[j] = fmaf(a0, __ldg(srow + j), v[j]);
           if (c == i) v[j] += lam;
         } else {
           v[j] = (c == i) ? 1.f : 0.f;
         }
       }
-      tmem_st8(row_addr + 8 * c8, v);
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        float w8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w8[j] = v[8 * c8 + j];
+        tmem_st8(row_addr + 32 * q + 8 * c8, w8);
+      }
     }
     tmem_wait_st();
     {
