@@ -112,6 +112,10 @@ int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pi
  * is faster).  Returns the previous setting.  IALS_TC=1 sets the default. */
 int ials_set_tensor_cores(int enable);
 
+/* Profiling only: a device buffer (>= 8 * 1024 int64) that kernels fill with
+ * per-CTA phase timestamps (clock64), or NULL to disable. */
+int ials_debug_timestamps(void* dev_buf);
+
 /* Heavy-row threshold (entries) used by the schedule for block width b. */
 int64_t ials_heavy_threshold(int32_t b);
 /* Slice length (entries) of heavy rows for block width b. */

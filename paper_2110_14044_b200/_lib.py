@@ -51,6 +51,7 @@ SIGNATURES = {
     "ials_check_singular": (c_i32, [c_p, c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_i32),
                                     ctypes.POINTER(c_i32)]),
     "ials_set_tensor_cores": (c_i32, [c_i32]),
+    "ials_debug_timestamps": (c_i32, [c_p]),
     "ials_heavy_threshold": (c_i64, [c_i32]),
     "ials_slice_len": (c_i64, [c_i32]),
     "ials_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),

@@ -139,10 +139,11 @@ static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
 
 size_t ials_tc_workspace_bytes(int32_t max_wave_rows, int32_t max_wave_slices) {
   return al256(size_t(max_wave_slices) * kTcPKS * 4) + al256(size_t(max_wave_slices) * 128 * 8) +
-         al256(size_t(max_wave_rows) * 128 * 4);
+         al256(size_t(max_wave_rows) * 128 * 4) + al256(size_t(kTcPKS) * 4);
 }
 
-int32_t ials_tc_wave_slices(void) { return 2560; }
+// 1024 partial Hessians (35 MB) stay L2-resident between k_tc_hess and k_tc_factor
+int32_t ials_tc_wave_slices(void) { return 1024; }
 
 static size_t pass_ws(int32_t n_rows, int32_t b, int32_t n_slices, int32_t n_heavy) {
   const size_t bt = block_tile(b);
@@ -295,6 +296,12 @@ static int set_smem_attrs(ials_session* s) {
   return IALS_OK;
 }
 
+static long long* g_dbg = nullptr;  // profiling: per-CTA phase timestamps
+int ials_debug_timestamps(void* dev_buf) {
+  g_dbg = static_cast<long long*>(dev_buf);
+  return IALS_OK;
+}
+
 static int g_tc = -1;  // -1: not yet read from IALS_TC
 static bool tc_enabled() {
   if (g_tc < 0) {
@@ -384,7 +391,11 @@ static int launch_tc_waves(ials_session* s, SweepParams p, const ials_sched* sch
     if (rc) return rc;
     h_sm = std::min(h_sm, 4);  // TMEM: 128 columns per CTA
     f_sm = std::min(f_sm, 4);
+    if (const char* e = getenv("IALS_TC_FSM")) f_sm = std::max(1, std::min(f_sm, atoi(e)));
+    if (const char* e = getenv("IALS_TC_HSM")) h_sm = std::max(1, std::min(h_sm, atoi(e)));
   }
+  k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
+  LAUNCH_CHECK(s);
   for (int w = 0; w < sched->tc_n_waves; ++w) {
     p.w_r0 = sched->tc_wave_row0[w];
     p.w_r1 = sched->tc_wave_row0[w + 1];
@@ -493,6 +504,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.tc_slice_beg = sched->tc_slice_begin;
   p.tc_slice_end = sched->tc_slice_end;
   p.w_r0 = p.w_r1 = p.w_s0 = p.w_s1 = 0;
+  p.dbg = g_dbg;
   if (use_tc) {  // tensor-core scratch follows proj
     char* t = ws + al256(size_t(side->n_rows) * b * 4);
     p.hbuf = reinterpret_cast<float*>(t);
@@ -500,7 +512,10 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.gbuf = reinterpret_cast<double*>(t);
     t += al256(size_t(sched->tc_max_wave_slices) * 128 * 8);
     p.dbuf = reinterpret_cast<float*>(t);
+    t += al256(size_t(sched->tc_max_wave_rows) * 128 * 4);
+    p.tpl = reinterpret_cast<const float*>(t);
   } else {
+    p.tpl = nullptr;
     p.hbuf = nullptr;
     p.gbuf = nullptr;
     p.dbuf = nullptr;

@@ -70,6 +70,8 @@ struct SweepParams {
   float* hbuf;    // [wave slices][8448] packed lower rows (4-aligned)
   double* gbuf;   // [wave slices][128]
   float* dbuf;    // [wave rows][128]
+  long long* dbg; // optional per-CTA phase timestamps (profiling builds only)
+  const float* tpl;  // [8448] packed alpha0 * slab[pi, pi] (tensor-core plan)
 };
 
 template <int BT>

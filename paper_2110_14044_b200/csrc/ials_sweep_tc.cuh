@@ -427,49 +427,44 @@ IALS_DEVI void tc_factor(const SweepParams& p, char* smem, TcState& st, int row,
 }
 
 // Backward solve L^T d = y (warp 0), identical to the SIMT kernel's.
+// Backward solve L^T d = y, panel by panel from the last: every thread
+// back-substitutes the panel's 8 unknowns redundantly (from the packed L),
+// then thread r < c0 folds them into its own y_r; one barrier per panel.
 template <class L = TcLay>
 IALS_DEVI void tc_backward(const SweepParams& p, char* smem, int tid) {
   const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L);
   float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
   const float* invd = reinterpret_cast<const float*>(smem + L::OFF_ID);
   float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
-  const int b = p.b, lane = tid & 31;
-  if (tid < 32) {
-    const int np = (b + 7) >> 3;
-    for (int pp = np - 1; pp >= 0; --pp) {
-      const int c0 = pp * 8;
-      float z[8], dlt[8];
+  const int b = p.b;
+  const int np = (b + 7) >> 3;
+  float yr = (tid < b) ? yf[tid] : 0.f;   // this thread's running y_r
+  for (int pp = np - 1; pp >= 0; --pp) {
+    const int c0 = pp * 8;
+    float dlt[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) z[q] = (c0 + q < b) ? yf[c0 + q] : 0.f;
+    for (int q = 7; q >= 0; --q) {
+      const int gq = c0 + q;
+      float v = (gq < b) ? yf[gq] : 0.f;
 #pragma unroll
-      for (int q = 7; q >= 0; --q) {
-        const int gq = c0 + q;
-        float v = z[q];
-#pragma unroll
-        for (int m = q + 1; m < 8; ++m) {
-          const int gm = c0 + m;
-          if (gm < b) v = fmaf(-Lp[gm * (gm + 1) / 2 + gq], dlt[m], v);
-        }
-        dlt[q] = (gq < b) ? v * invd[gq] : 0.f;
+      for (int m = q + 1; m < 8; ++m) {
+        const int gm = c0 + m;
+        if (gm < b) v = fmaf(-Lp[gm * (gm + 1) / 2 + gq], dlt[m], v);
       }
-      if (lane < 8) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q == lane && c0 + q < b) ds[c0 + q] = dlt[q];
-      }
-      for (int r = lane; r < c0; r += 32) {
-        float v = yf[r];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int gq = c0 + q;
-          if (gq < b) v = fmaf(-Lp[gq * (gq + 1) / 2 + r], dlt[q], v);
-        }
-        yf[r] = v;
-      }
-      __syncwarp();
+      dlt[q] = (gq < b) ? v * invd[gq] : 0.f;
     }
+    if (tid >= c0 && tid < c0 + 8 && tid < b) ds[tid] = dlt[tid - c0];
+    if (tid < c0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int gq = c0 + q;
+        if (gq < b) yr = fmaf(-Lp[gq * (gq + 1) / 2 + tid], dlt[q], yr);
+      }
+    }
+    __syncthreads();
+    if (tid < c0 && tid >= c0 - 8) yf[tid] = yr;   // the next panel's entries
+    __syncthreads();
   }
-  tc_cta_sync();
 }
 
 template <class L = TcLay>

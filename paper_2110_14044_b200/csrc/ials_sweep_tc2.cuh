@@ -85,6 +85,20 @@ IALS_DEVI void tc_teardown(const TcState& st, int tid) {
   if (tid < 32) tmem_free(st.tmem, 128);
 }
 
+// alpha0 * slab[pi, pi] (identity on the padding) as packed lower rows: the
+// same 33 KB for every row of the pass, so k_tc_factor reads it from L1.
+__global__ void k_tc_template(SweepParams p, float* tpl) {
+  const int i = blockIdx.x, b = p.b;
+  for (int c = threadIdx.x; c < 4 * ((i >> 2) + 1); c += blockDim.x) {
+    float v;
+    if (i < b && c < b)
+      v = p.alpha0 * p.slab[(size_t)(p.b0 + i) * b + c];
+    else
+      v = (c == i) ? 1.f : 0.f;
+    tpl[pk_off(i) + c] = v;
+  }
+}
+
 __global__ void __launch_bounds__(128) k_tc_hess(SweepParams p) {
   using L = TcLayH;
   extern __shared__ __align__(1024) char smem_raw[];
@@ -97,12 +111,17 @@ __global__ void __launch_bounds__(128) k_tc_hess(SweepParams p) {
   TcState st;
   tc_setup(smem, st, L::OFF_BAR, tid);
   const int nq = (tid >> 2) + 1;  // float4s of packed row tid
+  int ndone = 0;
   for (int s = p.w_s0 + blockIdx.x; s < p.w_s1; s += gridDim.x) {
+    const bool rec = p.dbg && ndone == 1 && tid == 0;
+    long long t0 = 0, t1 = 0;
+    if (rec) t0 = clock64();
     float sum[128];
 #pragma unroll
     for (int c = 0; c < 128; ++c) sum[c] = 0.f;
     double gacc = 0.0;
     tc_accumulate<L>(p, smem, st, gacc, sum, p.tc_slice_beg[s], p.tc_slice_end[s], tid);
+    if (rec) t1 = clock64();
     float* hp = p.hbuf + (size_t)(s - p.w_s0) * kTcPKS + pk_off(tid);
 #pragma unroll
     for (int c4 = 0; c4 < 32; ++c4)
@@ -113,6 +132,12 @@ __global__ void __launch_bounds__(128) k_tc_hess(SweepParams p) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (rec) {
+      const long long t2 = clock64();
+      long long* o = p.dbg + 8 * 1024 + blockIdx.x * 4;
+      o[0] = t1 - t0; o[1] = t2 - t1; o[2] = p.tc_slice_end[s] - p.tc_slice_beg[s];
+    }
+    ++ndone;
   }
   tc_teardown(st, tid);
 }
@@ -129,69 +154,56 @@ __global__ void __launch_bounds__(128) k_tc_factor(SweepParams p) {
   const int b = p.b, i = tid;
   const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
   const float a0 = p.alpha0;
+  int nrow_done = 0;
+  long long tphase[8];
   for (int r = p.w_r0 + blockIdx.x; r < p.w_r1; r += gridDim.x) {
+    const bool rec = p.dbg && nrow_done == 1 && tid == 0;
+    if (rec) tphase[0] = clock64();
     const int row = p.tc_rows[r];
     const int s_beg = p.tc_row_slice0[r], s_end = p.tc_row_slice0[r + 1];
     const float lam = p.side.lam[row];
-    // Hessian row i (lower part) = sum of the row's slice partials +
-    // alpha0 * slab + lam I; 32 columns per batch of loads
+    // Hessian row i (lower part) = template (alpha0 * slab, L1-resident) +
+    // sum of the row's slice partials (+ lam on the diagonal); 64 columns per
+    // batch of loads, all in flight
+    const float* tp = p.tpl + pk_off(i);
 #pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      float v[32];
+    for (int q = 0; q < 2; ++q) {
+      if (rec) tphase[5 + q] = clock64();
+      if (64 * q > i) {
+        float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = 0.f;
-      if (32 * q <= i) {
-        for (int s = s_beg; s < s_end; ++s) {
-          const float* hp = p.hbuf + (size_t)(s - p.w_s0) * kTcPKS + pk_off(i) + 32 * q;
-          float4 x[8];
-#pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4)
-            x[c4] = (32 * q + 4 * c4 <= i) ? *reinterpret_cast<const float4*>(hp + 4 * c4)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            v[4 * c4] += x[c4].x;
-            v[4 * c4 + 1] += x[c4].y;
-            v[4 * c4 + 2] += x[c4].z;
-            v[4 * c4 + 3] += x[c4].w;
-          }
-        }
+        for (int c8 = 0; c8 < 8; ++c8) tmem_st8(row_addr + 64 * q + 8 * c8, z);
+        continue;
       }
-      // + alpha0 * slab[pi, pi] + lam I on the b x b block, identity on padding
-      const float* srow = p.slab + (size_t)(p.b0 + i) * b + 32 * q;
-      if (i < b && (b & 3) == 0) {
-        float4 y[8];
+      float4 x[16];
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4)
-          y[c4] = (32 * q + 4 * c4 < b) ? __ldg(reinterpret_cast<const float4*>(srow) + c4)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c4 = 0; c4 < 16; ++c4)
+        x[c4] = (64 * q + 4 * c4 <= i) ? __ldg(reinterpret_cast<const float4*>(tp + 64 * q) + c4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = s_beg; s < s_end; ++s) {
+        const float* hp = p.hbuf + (size_t)(s - p.w_s0) * kTcPKS + pk_off(i) + 64 * q;
+        float4 y[16];
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          v[4 * c4] = fmaf(a0, y[c4].x, v[4 * c4]);
-          v[4 * c4 + 1] = fmaf(a0, y[c4].y, v[4 * c4 + 1]);
-          v[4 * c4 + 2] = fmaf(a0, y[c4].z, v[4 * c4 + 2]);
-          v[4 * c4 + 3] = fmaf(a0, y[c4].w, v[4 * c4 + 3]);
+        for (int c4 = 0; c4 < 16; ++c4)
+          y[c4] = (64 * q + 4 * c4 <= i) ? __ldcg(reinterpret_cast<const float4*>(hp) + c4)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int c4 = 0; c4 < 16; ++c4) {
+          x[c4].x += y[c4].x; x[c4].y += y[c4].y; x[c4].z += y[c4].z; x[c4].w += y[c4].w;
         }
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int c = 32 * q + j;
-        if (i < b && c < b) {
-          if ((b & 3) != 0) v[j] = fmaf(a0, __ldg(srow + j), v[j]);
-          if (c == i) v[j] += lam;
-        } else {
-          v[j] = (c == i) ? 1.f : 0.f;
-        }
-      }
+      for (int c8 = 0; c8 < 8; ++c8) {
+        float w8[8] = {x[2 * c8].x, x[2 * c8].y, x[2 * c8].z, x[2 * c8].w,
+                       x[2 * c8 + 1].x, x[2 * c8 + 1].y, x[2 * c8 + 1].z, x[2 * c8 + 1].w};
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
-        float w8[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) w8[j] = v[8 * c8 + j];
-        tmem_st8(row_addr + 32 * q + 8 * c8, w8);
+        for (int j = 0; j < 8; ++j)
+          if (64 * q + 8 * c8 + j == i && i < b) w8[j] += lam;
+        tmem_st8(row_addr + 64 * q + 8 * c8, w8);
       }
     }
     tmem_wait_st();
+    if (rec) tphase[7] = clock64();
     {
       double g = 0.0;
       for (int s = s_beg; s < s_end; ++s) g += p.gbuf[(size_t)(s - p.w_s0) * 128 + tid];
@@ -204,8 +216,11 @@ __global__ void __launch_bounds__(128) k_tc_factor(SweepParams p) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (rec) tphase[1] = clock64();
     tc_factor<L>(p, smem, st, row, tid);
+    if (rec) tphase[2] = clock64();
     tc_backward<L>(p, smem, tid);
+    if (rec) tphase[3] = clock64();
     if (tid < b) {
       p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
       p.dbuf[(size_t)(r - p.w_r0) * 128 + tid] = ds[tid];
@@ -213,6 +228,11 @@ __global__ void __launch_bounds__(128) k_tc_factor(SweepParams p) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (rec) {
+      tphase[4] = clock64();
+      for (int k = 0; k < 8; ++k) p.dbg[blockIdx.x * 8 + k] = tphase[k];
+    }
+    ++nrow_done;
   }
   tc_teardown(st, tid);
 }
