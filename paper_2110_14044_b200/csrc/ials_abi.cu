@@ -17,6 +17,7 @@
 #include "ials_loss.cuh"
 #include "ials_sweep_tc.cuh"
 #include "ials_sweep_tc2.cuh"
+#include "ials_sweep_b1.cuh"
 
 using namespace ials;
 
@@ -262,8 +263,21 @@ static int gramian_impl(ials_session* s, const float* M, int32_t n, int32_t ldm,
     CUDA_TRY(s, cudaMemsetAsync(slab, 0, size_t(d) * b * 4, st));
     return IALS_OK;
   }
-  dim3 g((d + GT - 1) / GT, (b + GT - 1) / GT, nsplit);
-  k_slab_partial<<<g, 256, 0, st>>>(M, n, ldm, d, b0, b, rps, part);
+  if (b <= 16) {  // narrow 128 x 16 tiles: no wasted 64-wide tile columns
+    const int ct = (d + 127) / 128;
+    int ns = std::max(1, std::min(2 * kNumSMs / ct, (n + 255) / 256));
+    ns = std::min(ns, kMaxSplits);
+    while (ns > 1 && size_t(ns) * d * b * 4 > part_bytes) --ns;
+    nsplit = ns;
+    rps = (n + nsplit - 1) / nsplit;
+    rps = ((rps + 31) / 32) * 32;
+    nsplit = (n + rps - 1) / rps;
+    dim3 g(ct, nsplit);
+    k_slab_narrow<<<g, 256, 0, st>>>(M, n, ldm, d, b0, b, rps, part);
+  } else {
+    dim3 g((d + GT - 1) / GT, (b + GT - 1) / GT, nsplit);
+    k_slab_partial<<<g, 256, 0, st>>>(M, n, ldm, d, b0, b, rps, part);
+  }
   LAUNCH_CHECK(s);
   const size_t cnt = size_t(d) * b;
   const int rb = (int)std::min<size_t>((cnt + 255) / 256, 4096);
@@ -521,11 +535,32 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.dbuf = nullptr;
   }
   if (side->n_rows > 0) {
-    dim3 g((side->n_rows + GT - 1) / GT, (b + GT - 1) / GT);
-    k_project<<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, b, alpha0, proj);
+    if (b <= 16) {
+      k_project_narrow<<<(side->n_rows + 127) / 128, 256, 0, st>>>(own, side->n_rows, ldo, d, slab,
+                                                                    b, alpha0, proj);
+    } else {
+      dim3 g((side->n_rows + GT - 1) / GT, (b + GT - 1) / GT);
+      k_project<<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, b, alpha0, proj);
+    }
     LAUNCH_CHECK(s);
   }
   if (use_tc) return launch_tc_waves(s, p, sched, st);
+  if (b == 1) {  // scalar blocks: the iCD special case
+    if (p.n_light > 0) {
+      k_sweep_b1<<<std::min((p.n_light + 7) / 8, kNumSMs * 16), 256, 0, st>>>(p);
+      LAUNCH_CHECK(s);
+    }
+    if (p.n_heavy > 0) {
+      const int g = std::min((p.n_slices + 7) / 8, kNumSMs * 16);
+      k_b1_partial<<<g, 256, 0, st>>>(p);
+      LAUNCH_CHECK(s);
+      k_b1_solve<<<(p.n_heavy + 127) / 128, 128, 0, st>>>(p);
+      LAUNCH_CHECK(s);
+      k_b1_cache<<<g, 256, 0, st>>>(p);
+      LAUNCH_CHECK(s);
+    }
+    return IALS_OK;
+  }
   switch (bt) {
     case 8: return launch_sweep<8>(s, p, st);
     case 16: return launch_sweep<16>(s, p, st);

@@ -176,6 +176,107 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Narrow block widths (b <= 16): 128 (t) x 16 (j) tiles, 32 rows per
+// k-step staged in shared memory; each thread owns 4 (t) x 2 (j) outputs.
+__global__ void __launch_bounds__(256)
+    k_slab_narrow(const float* __restrict__ M, int n, int ldm, int d, int b0, int b,
+                  int rows_per_split, float* __restrict__ part) {
+  __shared__ __align__(16) float As[32][128 + 4];
+  __shared__ __align__(16) float Bs[32][16];
+  const int t0 = blockIdx.x * 128, split = blockIdx.y;
+  const int r_beg = split * rows_per_split;
+  const int r_end = min(n, r_beg + rows_per_split);
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;   // t = 4tx.., j = 2ty..
+  float acc[4][2] = {};
+  for (int r0 = r_beg; r0 < r_end; r0 += 32) {
+    for (int i = tid; i < 32 * 32; i += 256) {           // 32 rows x 32 float4
+      const int rr = i >> 5, c4 = i & 31, r = r0 + rr, t = t0 + 4 * c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < r_end) {
+        const float* src = M + (size_t)r * ldm + t;
+        if (t + 3 < d && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          if (t < d) v.x = src[0];
+          if (t + 1 < d) v.y = src[1];
+          if (t + 2 < d) v.z = src[2];
+          if (t + 3 < d) v.w = src[3];
+        }
+      }
+      *reinterpret_cast<float4*>(&As[rr][4 * c4]) = v;
+    }
+    for (int i = tid; i < 32 * 16; i += 256) {
+      const int rr = i >> 4, j = i & 15, r = r0 + rr;
+      Bs[rr][j] = (r < r_end && j < b) ? M[(size_t)r * ldm + b0 + j] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[rr][4 * tx]);
+      const float2 c = *reinterpret_cast<const float2*>(&Bs[rr][2 * ty]);
+      acc[0][0] = fmaf(a.x, c.x, acc[0][0]); acc[0][1] = fmaf(a.x, c.y, acc[0][1]);
+      acc[1][0] = fmaf(a.y, c.x, acc[1][0]); acc[1][1] = fmaf(a.y, c.y, acc[1][1]);
+      acc[2][0] = fmaf(a.z, c.x, acc[2][0]); acc[2][1] = fmaf(a.z, c.y, acc[2][1]);
+      acc[3][0] = fmaf(a.w, c.x, acc[3][0]); acc[3][1] = fmaf(a.w, c.y, acc[3][1]);
+    }
+    __syncthreads();
+  }
+  float* out = part + (size_t)split * d * b;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + 4 * tx + i;
+    if (t >= d) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int jj = 2 * ty + j;
+      if (jj < b) out[(size_t)t * b + jj] = acc[i][j];
+    }
+  }
+}
+
+// Narrow block widths: proj = alpha0 * own @ slab with 128 (rows) x 16 (j)
+// output tiles; K = d in steps of 32 staged in shared memory.
+__global__ void __launch_bounds__(256)
+    k_project_narrow(const float* __restrict__ own, int n_rows, int ldo, int d,
+                     const float* __restrict__ slab, int b, float alpha0, float* __restrict__ proj) {
+  __shared__ __align__(16) float As[32][128 + 4];   // As[k][r]
+  __shared__ __align__(16) float Bs[32][16];        // Bs[k][j]
+  const int r0 = blockIdx.x * 128;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  float acc[4][2] = {};
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    for (int i = tid; i < 128 * 32; i += 256) {
+      const int rr = i >> 5, kk = i & 31, r = r0 + rr, k = k0 + kk;
+      As[kk][rr] = (r < n_rows && k < d) ? own[(size_t)r * ldo + k] : 0.f;
+    }
+    for (int i = tid; i < 32 * 16; i += 256) {
+      const int kk = i >> 4, j = i & 15, k = k0 + kk;
+      Bs[kk][j] = (k < d && j < b) ? slab[(size_t)k * b + j] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][4 * tx]);
+      const float2 c = *reinterpret_cast<const float2*>(&Bs[kk][2 * ty]);
+      acc[0][0] = fmaf(a.x, c.x, acc[0][0]); acc[0][1] = fmaf(a.x, c.y, acc[0][1]);
+      acc[1][0] = fmaf(a.y, c.x, acc[1][0]); acc[1][1] = fmaf(a.y, c.y, acc[1][1]);
+      acc[2][0] = fmaf(a.z, c.x, acc[2][0]); acc[2][1] = fmaf(a.z, c.y, acc[2][1]);
+      acc[3][0] = fmaf(a.w, c.x, acc[3][0]); acc[3][1] = fmaf(a.w, c.y, acc[3][1]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + 4 * tx + i;
+    if (r >= n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int jj = 2 * ty + j;
+      if (jj < b) proj[(size_t)r * b + jj] = alpha0 * acc[i][j];
+    }
+  }
+}
+
 __global__ void k_reduce_splits(const float* __restrict__ part, int nsplit, size_t count,
                                 float* __restrict__ out) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;

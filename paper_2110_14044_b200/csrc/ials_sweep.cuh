@@ -165,10 +165,16 @@ IALS_DEVI void stage_chunk(const SweepParams& p, float* sm, int buf, int ebeg, i
   using L = Lay<BT>;
   float* X = sm + L::OFF_X + buf * L::KC * L::XLD;
   if (p.vec) {
+    // BT/4 float4 slots per entry (a power of two: shifts, no division);
+    // slots beyond b/4 are skipped
+    constexpr int SL = BT / 4 >= 1 ? BT / 4 : 1;
+    constexpr int LG = SL == 1 ? 0 : SL == 2 ? 1 : SL == 4 ? 2 : SL == 8 ? 3 : SL == 16 ? 4
+                       : SL == 32 ? 5 : 6;
     const int bv = p.b >> 2;
-    for (int i = tid; i < nk * bv; i += L::NT) {
-      int k = i / bv, v = i - k * bv;
-      int col = __ldg(p.side.cols + ebeg + k);
+    for (int i = tid; i < nk * SL; i += L::NT) {
+      const int k = i >> LG, v = i & (SL - 1);
+      if (v >= bv) continue;
+      const int col = __ldg(p.side.cols + ebeg + k);
       cp_async16(X + k * L::XLD + 4 * v, p.fixed + (size_t)col * p.ldf + p.b0 + 4 * v);
     }
   } else {
@@ -250,10 +256,18 @@ IALS_DEVI void accumulate_chunk(Tiles<BT>& T, double& gacc, const float* sm, int
   }
   if (tid < BT) {
     // fp64: g = sum rho_k h_k + alpha0 w G + lam w cancels by orders of magnitude
-    // on long rows, so the sum is formed in double and rounded once.
-    double g = gacc;
-    for (int k = 0; k < nk; ++k) g = fma((double)rh[k], (double)X[k * L::XLD + tid], g);
-    gacc = g;
+    // on long rows, so the sum is formed in double and rounded once (four
+    // independent chains hide the DFMA latency; fixed combination order).
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+    int k = 0;
+    for (; k + 3 < nk; k += 4) {
+      g0 = fma((double)rh[k], (double)X[k * L::XLD + tid], g0);
+      g1 = fma((double)rh[k + 1], (double)X[(k + 1) * L::XLD + tid], g1);
+      g2 = fma((double)rh[k + 2], (double)X[(k + 2) * L::XLD + tid], g2);
+      g3 = fma((double)rh[k + 3], (double)X[(k + 3) * L::XLD + tid], g3);
+    }
+    for (; k < nk; ++k) g0 = fma((double)rh[k], (double)X[k * L::XLD + tid], g0);
+    gacc += (g0 + g1) + (g2 + g3);
   }
 }
 
@@ -510,25 +524,44 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
   team_sync<L::NW>(team);
 }
 
-// Step 7 on one staged chunk: yhat[pos_k] -= x_k . d
+// Step 7 on one staged chunk: yhat[pos_k] -= x_k . d.  GL = BT/16 lanes
+// cooperate on one entry, each covering 16 consecutive floats (4 LDS.128), so
+// a team works on NW*32/GL entries at once.
 template <int BT>
 IALS_DEVI void cache_chunk(const SweepParams& p, const float* sm, int buf, int nk, int tid) {
   using L = Lay<BT>;
-  constexpr int GL = BT < 32 ? BT : 32;
+  constexpr int GL = BT >= 32 ? BT / 16 : 1;
   constexpr int EPW = 32 / GL;
+  constexpr int SEG = BT >= 16 ? 16 : BT;
   const float* X = sm + L::OFF_X + buf * L::KC * L::XLD;
   const int* ps = reinterpret_cast<const int*>(sm + L::OFF_PS) + buf * L::KC;
   const float* ds = sm + L::OFF_D;
   const int warp = tid >> 5, lane = tid & 31;
   const int sub = lane / GL, gl = lane % GL;
+  const int j0 = gl * SEG;
   for (int kb = 0; kb < nk; kb += L::NW * EPW) {
     const int k = kb + warp * EPW + sub;
-    float s = 0.f;
-    if (k < nk) {
-      for (int j = gl; j < p.b; j += GL) s = fmaf(X[k * L::XLD + j], ds[j], s);
+    float s0 = 0.f, s1 = 0.f;
+    if (k < nk && j0 < p.b) {
+      const float* xr = X + k * L::XLD + j0;
+      if (p.b - j0 >= SEG) {
+#pragma unroll
+        for (int j = 0; j < SEG; j += 4) {
+          float xv[4], dv[4];
+          lds_vec<4>(xv, xr + j);
+          lds_vec<4>(dv, ds + j0 + j);
+          s0 = fmaf(xv[0], dv[0], s0);
+          s1 = fmaf(xv[1], dv[1], s1);
+          s0 = fmaf(xv[2], dv[2], s0);
+          s1 = fmaf(xv[3], dv[3], s1);
+        }
+      } else {
+        for (int j = 0; j < p.b - j0; ++j) s0 = fmaf(xr[j], ds[j0 + j], s0);
+      }
     }
-    s = group_sum<GL>(s);
-    if (k < nk && gl == 0) p.cache[ps[k]] -= s;
+    float sum = s0 + s1;
+    if constexpr (GL > 1) sum = group_sum<GL>(sum);
+    if (k < nk && gl == 0) p.cache[ps[k]] -= sum;
   }
 }
 
