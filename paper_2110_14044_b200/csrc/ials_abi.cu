@@ -127,10 +127,16 @@ int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pi
               sd == 0 ? "user" : "item", (long long)r, pv);
 }
 
-int64_t ials_heavy_threshold(int32_t b) { return block_tile(b) <= 32 ? 2048 : 4096; }
+// Rows longer than the threshold are split into slices (partial Hessians
+// reduced in a fixed order): a one-warp row team at small block widths is
+// latency-bound on long rows, so it splits them early.
+int64_t ials_heavy_threshold(int32_t b) {
+  const int bt = block_tile(b);
+  return bt <= 16 ? 512 : bt == 32 ? 1024 : 4096;
+}
 int64_t ials_slice_len(int32_t b) {
   const int bt = block_tile(b);
-  return bt <= 32 ? 1024 : (bt == 256 ? 1024 : 2048);
+  return bt <= 16 ? 256 : bt == 32 ? 512 : (bt == 256 ? 1024 : 2048);
 }
 
 static size_t gram_ws(int32_t n, int32_t d, int32_t b) {

@@ -207,7 +207,7 @@ IALS_DEVI void stage_chunk(const SweepParams& p, float* sm, int buf, int ebeg, i
 // Hessian + gradient accumulation over one staged chunk.
 template <int BT>
 IALS_DEVI void accumulate_chunk(Tiles<BT>& T, double& gacc, const float* sm, int buf, int nk,
-                                int tid) {
+                                int tid, bool unit) {
   using L = Lay<BT>;
   const float* X = sm + L::OFF_X + buf * L::KC * L::XLD;
   const float* aw = sm + L::OFF_AW + buf * L::KC;
@@ -217,42 +217,44 @@ IALS_DEVI void accumulate_chunk(Tiles<BT>& T, double& gacc, const float* sm, int
   // tile that is then added to the running Hessian, as a blocked GEMM would;
   // a long row's sum is then ~sqrt(KC) times more accurate than one running
   // fp32 sum (matters for the ill-conditioned first epochs of heavy rows).
-  constexpr bool kBlocked = L::TPW == 1;
-  float loc[kBlocked ? L::SR : 1][kBlocked ? L::SC : 1];
-  if constexpr (kBlocked) {
+  // Tiles are visited outermost so one local tile suffices for any TPW.
+#pragma unroll
+  for (int t = 0; t < L::TPW; ++t) {
+    if (!T.valid[t]) continue;
+    float loc[L::SR][L::SC];
 #pragma unroll
     for (int i = 0; i < L::SR; ++i)
 #pragma unroll
       for (int j = 0; j < L::SC; ++j) loc[i][j] = 0.f;
-  }
+    const float* xr0 = X + T.roff[t];
+    const float* xc0 = X + T.coff[t];
+    // unit weights: no per-entry scale, so stop at nk (stale padded rows
+    // would otherwise contribute); weighted: padded entries carry a = 0
+    const int kend = unit ? nk : nk4;
 #pragma unroll 2
-  for (int k = 0; k < nk4; ++k) {
-    const float a = aw[k];
-    const float* xr = X + k * L::XLD;
-#pragma unroll
-    for (int t = 0; t < L::TPW; ++t) {
-      if (!T.valid[t]) continue;
+    for (int k = 0; k < kend; ++k) {
       float rv[L::SR], cv[L::SC];
-      lds_vec<L::SR>(rv, xr + T.roff[t]);
-      lds_vec<L::SC>(cv, xr + T.coff[t]);
+      lds_vec<L::SR>(rv, xr0 + k * L::XLD);
+      lds_vec<L::SC>(cv, xc0 + k * L::XLD);
+      if (unit) {
 #pragma unroll
-      for (int i = 0; i < L::SR; ++i) {
-        const float ra = rv[i] * a;
+        for (int i = 0; i < L::SR; ++i)
 #pragma unroll
-        for (int j = 0; j < L::SC; ++j) {
-          if constexpr (kBlocked)
-            loc[i][j] = fmaf(ra, cv[j], loc[i][j]);
-          else
-            T.acc[t][i][j] = fmaf(ra, cv[j], T.acc[t][i][j]);
+          for (int j = 0; j < L::SC; ++j) loc[i][j] = fmaf(rv[i], cv[j], loc[i][j]);
+      } else {
+        const float a = aw[k];
+#pragma unroll
+        for (int i = 0; i < L::SR; ++i) {
+          const float ra = rv[i] * a;
+#pragma unroll
+          for (int j = 0; j < L::SC; ++j) loc[i][j] = fmaf(ra, cv[j], loc[i][j]);
         }
       }
     }
-  }
-  if constexpr (kBlocked) {
 #pragma unroll
     for (int i = 0; i < L::SR; ++i)
 #pragma unroll
-      for (int j = 0; j < L::SC; ++j) T.acc[0][i][j] += loc[i][j];
+      for (int j = 0; j < L::SC; ++j) T.acc[t][i][j] += loc[i][j];
   }
   if (tid < BT) {
     // fp64: g = sum rho_k h_k + alpha0 w G + lam w cancels by orders of magnitude
@@ -290,7 +292,8 @@ IALS_DEVI int accumulate_range(const SweepParams& p, Tiles<BT>& T, double& gacc,
     }
     team_sync<L::NW>(team);
     int s = ebeg + c * L::KC;
-    accumulate_chunk<BT>(T, gacc, sm, c & 1, min(L::KC, eend - s), tid);
+    accumulate_chunk<BT>(T, gacc, sm, c & 1, min(L::KC, eend - s), tid,
+                         p.side.weights == nullptr);
     team_sync<L::NW>(team);
   }
   return nch;

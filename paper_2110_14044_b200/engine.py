@@ -334,6 +334,22 @@ class Engine:
                                  ws.numel(), self.stream())
         self.sess.check(rc, "epoch")
 
+    def epoch_graph(self, W, H, cache, b, alpha0):
+        """The same epoch captured once as a CUDA graph and replayed (one
+        launch per epoch instead of ~10 per block; matters for small configs).
+        The graph is keyed on the buffers, so W / H / cache must stay the same
+        tensors between calls."""
+        key = (W.data_ptr(), H.data_ptr(), cache.data_ptr(), int(b), float(alpha0))
+        g = getattr(self, "_graphs", {}).get(key)
+        if g is None:
+            self.epoch(W, H, cache, b, alpha0)          # attributes / workspace set up
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.epoch(W, H, cache, b, alpha0)
+            self.__dict__.setdefault("_graphs", {})[key] = g
+        g.replay()
+
     def loss_terms(self, W, H):
         """Device fp64 loss pieces; returns a (4,) float64 CUDA tensor."""
         d = W.shape[1]
