@@ -107,10 +107,21 @@ int ials_reset_singular(ials_session* s, void* stream);
 int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pivot,
                         int32_t* side);
 
-/* Route block widths 33..128 through the tcgen05 (tensor-core, 3xTF32)
- * sweep (1) or the FP32 SIMT sweep (0, default until the tensor-core path
- * is faster).  Returns the previous setting.  IALS_TC=1 sets the default. */
+/* Sweep engine for block widths 33..128: 0 = FP32 SIMT sweep, 1 = tcgen05
+ * (3xTF32) wave kernels for b in 33..128, 2 = fused tcgen05 sweep for b in
+ * 65..128 (4 rows in flight per SM; rows whose Cholesky pivots cancel more
+ * than IALS_TC_COND (default 256) x are re-solved by the SIMT sweep).
+ * Returns the previous setting.  The IALS_TC environment variable sets the
+ * initial mode (default 2). */
 int ials_set_tensor_cores(int enable);
+
+/* Number of rows the fused tensor-core sweep handed to the SIMT sweep since
+ * the session was created (or last reset); synchronises `stream`. */
+int ials_tc_redo_rows(ials_session* s, void* stream, int64_t* total, int32_t reset);
+
+/* The fused tensor-core sweep's cancellation limit (> 1); returns the
+ * previous value.  IALS_TC_COND sets the initial value. */
+float ials_set_tc_cond_max(float v);
 
 /* Profiling only: a device buffer (>= 8 * 1024 int64) that kernels fill with
  * per-CTA phase timestamps (clock64), or NULL to disable. */

@@ -51,6 +51,8 @@ SIGNATURES = {
     "ials_check_singular": (c_i32, [c_p, c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_i32),
                                     ctypes.POINTER(c_i32)]),
     "ials_set_tensor_cores": (c_i32, [c_i32]),
+    "ials_tc_redo_rows": (c_i32, [c_p, c_p, ctypes.POINTER(c_i64), c_i32]),
+    "ials_set_tc_cond_max": (c_f, [c_f]),
     "ials_debug_timestamps": (c_i32, [c_p]),
     "ials_heavy_threshold": (c_i64, [c_i32]),
     "ials_slice_len": (c_i64, [c_i32]),

@@ -17,6 +17,7 @@
 #include "ials_loss.cuh"
 #include "ials_sweep_tc.cuh"
 #include "ials_sweep_tc2.cuh"
+#include "ials_sweep_tc4.cuh"
 #include "ials_sweep_b1.cuh"
 
 using namespace ials;
@@ -24,6 +25,7 @@ using namespace ials;
 struct ials_session {
   int device;
   unsigned long long* err;  // device error word (ULLONG_MAX = clean)
+  unsigned long long* redo; // rows the fused tensor-core sweep handed to SIMT
   char msg[512];
 };
 
@@ -80,6 +82,8 @@ int ials_session_create(int device, ials_session** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMalloc(&s->err, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(s->err, 0xFF, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&s->redo, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(s->redo, 0, sizeof(unsigned long long));
   if (e != cudaSuccess) {
     fail(nullptr, IALS_E_CUDA, "session create: %s", cudaGetErrorString(e));
     delete s;
@@ -92,6 +96,7 @@ int ials_session_create(int device, ials_session** out) {
 int ials_session_destroy(ials_session* s) {
   if (!s) return IALS_OK;
   cudaFree(s->err);
+  cudaFree(s->redo);
   delete s;
   return IALS_OK;
 }
@@ -107,6 +112,16 @@ int ials_last_error(ials_session* s, char* buf, size_t len) {
 int ials_reset_singular(ials_session* s, void* stream) {
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   CUDA_TRY(s, cudaMemsetAsync(s->err, 0xFF, sizeof(unsigned long long), S(stream)));
+  return IALS_OK;
+}
+
+int ials_tc_redo_rows(ials_session* s, void* stream, int64_t* total, int32_t reset) {
+  if (!s || !total) return fail(s, IALS_E_INVALID, "tc_redo_rows: NULL argument");
+  unsigned long long v = 0;
+  CUDA_TRY(s, cudaMemcpyAsync(&v, s->redo, sizeof(v), cudaMemcpyDeviceToHost, S(stream)));
+  if (reset) CUDA_TRY(s, cudaMemsetAsync(s->redo, 0, sizeof(v), S(stream)));
+  CUDA_TRY(s, cudaStreamSynchronize(S(stream)));
+  *total = static_cast<int64_t>(v);
   return IALS_OK;
 }
 
@@ -155,7 +170,9 @@ int32_t ials_tc_wave_slices(void) { return 1024; }
 static size_t pass_ws(int32_t n_rows, int32_t b, int32_t n_slices, int32_t n_heavy) {
   const size_t bt = block_tile(b);
   return al256(size_t(n_rows) * b * 4) + al256(size_t(n_slices) * bt * bt * 4) +
-         al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4);
+         al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4) +
+         al256(size_t(kTcPKS) * 4) + al256(size_t(n_rows) * 4 + 16) +
+         al256(size_t(n_rows) * b * 4);
 }
 
 size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, int32_t b,
@@ -326,15 +343,85 @@ static int g_tc = -1;  // -1: not yet read from IALS_TC
 static bool tc_enabled() {
   if (g_tc < 0) {
     const char* e = getenv("IALS_TC");
-    g_tc = (e && e[0] == '1') ? 1 : 0;
+    // default: the fused tensor-core sweep (mode 2) for b in 65..128
+    g_tc = (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 2;
   }
   return g_tc == 1;
 }
+static float g_cond = 0.f;
+static float tc_cond_max() {
+  if (g_cond == 0.f) {
+    const char* e = getenv("IALS_TC_COND");
+    g_cond = e ? static_cast<float>(atof(e)) : 256.f;
+    if (!(g_cond > 1.f)) g_cond = 256.f;
+  }
+  return g_cond;
+}
+
+float ials_set_tc_cond_max(float v) {
+  const float prev = tc_cond_max();
+  if (v > 1.f) g_cond = v;
+  return prev;
+}
+static bool tc4_enabled() {
+  tc_enabled();
+  return g_tc == 2;
+}
 
 int ials_set_tensor_cores(int enable) {
-  const int prev = tc_enabled() ? 1 : 0;
-  g_tc = enable ? 1 : 0;
+  tc_enabled();
+  const int prev = g_tc;
+  g_tc = (enable == 1 || enable == 2) ? enable : 0;
   return prev;
+}
+
+// BT = 128, b > 64: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
+// heavy rows on the SIMT slice kernels.
+static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t st) {
+  using L = Lay<128>;
+  int rc = set_smem_attrs<128>(s);
+  if (rc) return rc;
+  if (p.n_light > 0) {
+    static bool init = false;
+    if (!init) {
+      CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TcLay4::BYTES));
+      CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc4, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       100));
+      init = true;
+    }
+    k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
+    LAUNCH_CHECK(s);
+    CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, sizeof(int), st));
+    const int grid = std::min(p.n_light, 4 * kNumSMs);   // TMEM: 4 x 128 columns per SM
+    k_sweep_tc4<<<grid, 128, TcLay4::BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    // rows the cancellation check rejected: FP32 SIMT sweep over the device
+    // list (persistent grid, the count is read on the device)
+    static int simt_sm = 0;
+    if (simt_sm == 0) {
+      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<128>,
+                                                               L::NT * L::RPC, L::CTA_BYTES));
+      if (simt_sm < 1) simt_sm = 1;
+    }
+    SweepParams q = p;
+    q.light_rows = p.redo_rows;
+    q.n_light_dev = p.redo_cnt;
+    k_sweep_light<128><<<simt_sm * kNumSMs, L::NT * L::RPC, L::CTA_BYTES, st>>>(q);
+    LAUNCH_CHECK(s);
+  }
+  if (p.n_heavy > 0) {
+    const int threads = L::NT * L::RPC;
+    k_heavy_partial<128><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    k_heavy_solve<128><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  if (p.n_light + p.n_slices > 0) {
+    k_pass_cache<<<p.n_light + p.n_slices, 256, 0, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  return IALS_OK;
 }
 
 // BT = 128 on the tensor core: light rows fused (k_sweep_tc128), heavy-row
@@ -441,6 +528,7 @@ template <int BT>
 static int launch_sweep(ials_session* s, const SweepParams& p, cudaStream_t st) {
   using L = Lay<BT>;
   if (BT == 128 && p.b > 32 && tc_enabled()) return launch_sweep_tc128(s, p, st);
+  if (BT == 128 && p.b > 64 && tc4_enabled()) return launch_sweep_tc4(s, p, st);
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
   const int threads = L::NT * L::RPC;
@@ -483,7 +571,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   const size_t need = use_tc ? need_tc : need_simt;
   if (need > ws_bytes)
     return fail(s, IALS_E_NOMEM, "side_pass: workspace %zu < %zu bytes", ws_bytes, need);
-  SweepParams p;
+  SweepParams p{};
   p.side = SideDev{side->n_rows, side->n_fixed, side->ptr, side->cols, side->labels,
                    side->weights, side->pos, side->lam};
   p.fixed = fixed;
@@ -517,6 +605,16 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.gpart = reinterpret_cast<double*>(w);
   w += al256(size_t(sched->n_slices) * bt * 8);
   p.hdelta = reinterpret_cast<float*>(w);
+  w += al256(size_t(sched->n_heavy) * bt * 4);
+  float* tpl_simt = reinterpret_cast<float*>(w);
+  w += al256(size_t(kTcPKS) * 4);
+  p.redo_cnt = reinterpret_cast<int*>(w);
+  p.redo_rows = reinterpret_cast<int*>(w + 16);
+  w += al256(size_t(side->n_rows) * 4 + 16);
+  p.drow = reinterpret_cast<float*>(w);
+  p.redo_total = s->redo;
+  p.cond_max = tc_cond_max();
+  p.n_light_dev = nullptr;
   p.proj = proj;
   p.tc_rows = sched->tc_rows;
   p.tc_row_slice0 = sched->tc_row_slice0;
@@ -535,7 +633,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     t += al256(size_t(sched->tc_max_wave_rows) * 128 * 4);
     p.tpl = reinterpret_cast<const float*>(t);
   } else {
-    p.tpl = nullptr;
+    p.tpl = tpl_simt;
     p.hbuf = nullptr;
     p.gbuf = nullptr;
     p.dbuf = nullptr;

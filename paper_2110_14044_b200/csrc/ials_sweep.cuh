@@ -72,6 +72,14 @@ struct SweepParams {
   float* dbuf;    // [wave rows][128]
   long long* dbg; // optional per-CTA phase timestamps (profiling builds only)
   const float* tpl;  // [8448] packed alpha0 * slab[pi, pi] (tensor-core plan)
+  // fused tensor-core sweep: rows whose Cholesky pivots cancel more than
+  // cond_max (H_kk / pivot_k) are left untouched and listed for the SIMT sweep
+  int* redo_rows;
+  int* redo_cnt;
+  unsigned long long* redo_total;
+  float cond_max;
+  const int* n_light_dev;  // if set, k_sweep_light reads its row count here
+  float* drow;             // [n_rows][b] per-row d of the fused sweep (k_pass_cache)
 };
 
 template <int BT>
@@ -612,7 +620,8 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   zero_stage<BT>(sm, tid);
   team_sync<L::NW>(team);
   // persistent: rows are in descending-degree order, strided over the grid
-  for (int task = blockIdx.x * L::RPC + team; task < p.n_light; task += gridDim.x * L::RPC) {
+  const int n_light = p.n_light_dev ? *p.n_light_dev : p.n_light;
+  for (int task = blockIdx.x * L::RPC + team; task < n_light; task += gridDim.x * L::RPC) {
     const int row = p.light_rows[task];
     const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
     Tiles<BT> T;

@@ -453,7 +453,13 @@ IALS_DEVI void tc_backward(const SweepParams& p, char* smem, int tid) {
       }
       dlt[q] = (gq < b) ? v * invd[gq] : 0.f;
     }
-    if (tid >= c0 && tid < c0 + 8 && tid < b) ds[tid] = dlt[tid - c0];
+    if (tid >= c0 && tid < c0 + 8 && tid < b) {  // ds[tid] = dlt[tid - c0], in registers
+      const int e = tid - c0;
+      const float a0 = (e & 1) ? dlt[1] : dlt[0], a1 = (e & 1) ? dlt[3] : dlt[2];
+      const float a2 = (e & 1) ? dlt[5] : dlt[4], a3 = (e & 1) ? dlt[7] : dlt[6];
+      const float b0 = (e & 2) ? a1 : a0, b1 = (e & 2) ? a3 : a2;
+      ds[tid] = (e & 4) ? b1 : b0;
+    }
     if (tid < c0) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {

@@ -1,0 +1,655 @@
+// ials_sweep_tc4.cuh -- fused tensor-core light-row sweep for block widths
+// 65..128 (BT = 128), four CTAs (rows in flight) per SM.
+//
+// Per row, one CTA of 128 threads (thread i <-> TMEM lane i <-> matrix row i):
+//   1. TMEM D := alpha0*slab[pi,pi] + lam*I   (tcgen05.st from the packed
+//      template k_tc_template built once per pass; identity on the padding)
+//   2. for each 16-entry chunk of the row (cp.async double-buffered gather):
+//      fp64 gradient on the SIMT pipe; transpose + tf32 split into K-major
+//      64B-swizzled operands (double-buffered, so the tensor core works on
+//      chunk c while chunk c+1 is prepared); one thread issues
+//      D += Xhi Xhi^T + Xhi Xlo^T + Xlo Xhi^T (3xTF32, M=N=128, K=8) straight
+//      into the TMEM accumulator (no register row sum: that is what caps the
+//      two-level-sum kernels at two CTAs per SM)
+//   3. blocked Cholesky in TMEM: per 8-column panel the diagonal warp factors
+//      the 8x8 block, every row solves against it (forward solve fused) and
+//      writes its L entries back into TMEM; the trailing update is 3xTF32
+//      MMAs restricted to the columns right of the panel (N = 128 - cs)
+//   4. L is copied TMEM -> packed smem (reusing the operand buffers), then
+//      backward solve, W update and the cache update yhat -= X d
+// Shared memory ~55 KB and 128 TMEM columns per CTA -> 4 CTAs per SM.
+#pragma once
+#include "ials_sweep_tc2.cuh"
+
+namespace ials {
+
+struct TcLay4 {
+  static constexpr int BT = 128, NT = 128, KC = 16, XLD = BT + 4;
+  static constexpr int MR = 8;   // metadata ring depth (chunks)
+  // overlay region (1024-aligned), by phase:
+  //   accumulate: XT hi/lo double buffer  4 x 8 KB (K-major SW64)
+  //   factor + backward: packed L         33,024 B (written as it is factored)
+  // the natural staging region holds the panel operands during the
+  // factorisation and the diagonal-block inverses during the backward solve
+  static constexpr int OFF_XT = 0;
+  static constexpr int OFF_L = 0;
+  static constexpr int OVL = 33792;
+  static constexpr int OFF_X = OVL;                            // natural staging [2][KC][XLD]
+  static constexpr int OFF_MC = OFF_X + 2 * KC * XLD * 4;      // ring [MR][KC]: cols
+  static constexpr int OFF_MP = OFF_MC + MR * KC * 4;          //                positions
+  static constexpr int OFF_MW = OFF_MP + MR * KC * 4;          //                weights
+  static constexpr int OFF_MY = OFF_MW + MR * KC * 4;          //                labels
+  static constexpr int OFF_CV = OFF_MY + MR * KC * 4;          // [4][KC] gathered yhat
+  static constexpr int OFF_DG = OFF_CV + 4 * KC * 4;
+  static constexpr int OFF_RV = OFF_DG + 64 * 4;
+  static constexpr int OFF_YP = OFF_RV + 8 * 4;
+  static constexpr int OFF_Y = OFF_YP + 8 * 4;
+  static constexpr int OFF_YF = OFF_Y + BT * 4;
+  static constexpr int OFF_ID = OFF_YF + BT * 4;
+  static constexpr int OFF_D = OFF_ID + BT * 4;
+  static constexpr int OFF_PA_HI = OFF_X;          // factor: panel operands hi / lo (2 x 4 KB)
+  static constexpr int OFF_LI = OFF_X + 8192;      // backward: 16 x 8x8 block inverses
+  static constexpr int OFF_DIAG = OFF_D + BT * 4;  // H_kk before the factorisation
+  static constexpr int OFF_FLAG = OFF_DIAG + BT * 4;
+  static constexpr int OFF_BAR = OFF_FLAG + 16;    // 2 mbarriers + TMEM base
+  static constexpr int BYTES = OFF_BAR + 32 + 1024;
+};
+
+// K-major, 64B-swizzle float index of operand element (row m, k) of a
+// 16-entry chunk: 8-row atoms of 512 B, 16-byte chunk (k/4) of row m at
+// (k/4) ^ ((m/2) % 4).
+IALS_DEVI int xt64_index(int m, int k) {
+  return (m >> 3) * 128 + (m & 7) * 16 + ((((k >> 2) ^ ((m >> 1) & 3))) << 2) + (k & 3);
+}
+
+constexpr uint32_t kSwizzle64B = 4;
+
+struct Tc4State {
+  uint32_t tmem;
+  uint32_t ph;      // bit x: phase parity of the next completion of bar[x]
+};
+
+// step 1: TMEM row i := template row i (+ lam on the diagonal), zero above
+IALS_DEVI void tc4_init(const SweepParams& p, uint32_t row_addr, float lam, int tid) {
+  const int i = tid;
+  const float* tp = p.tpl + pk_off(i);
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {
+    float4 x[16];
+#pragma unroll
+    for (int c4 = 0; c4 < 16; ++c4)
+      x[c4] = (64 * q + 4 * c4 <= i) ? __ldg(reinterpret_cast<const float4*>(tp + 64 * q) + c4)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int c8 = 0; c8 < 8; ++c8) {
+      float w8[8] = {x[2 * c8].x, x[2 * c8].y, x[2 * c8].z, x[2 * c8].w,
+                     x[2 * c8 + 1].x, x[2 * c8 + 1].y, x[2 * c8 + 1].z, x[2 * c8 + 1].w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (64 * q + 8 * c8 + j == i && i < p.b) w8[j] += lam;
+      tmem_st8(row_addr + 64 * q + 8 * c8, w8);
+    }
+  }
+}
+
+// step 2: D += sum over the row's entries of a h h^T; fp64 gradient -> gacc.
+//
+// Every load is asynchronous and addressed from shared memory: the row's
+// metadata (cols, positions, weights, labels) streams through a ring MR
+// chunks deep, fetched 4 chunks ahead; the gathered sub-rows X and the
+// predictions yhat[pos] are fetched 2 chunks ahead.  cp.async group g (one
+// per iteration) = {X(g+2), yhat(g+2), meta(g+4)}, so waiting for group c-2
+// at iteration c delivers X(c) and the metadata X(c+2) needs.
+IALS_DEVI void tc4_meta(const SweepParams& p, char* smem, int ebeg, int eend, int c, int tid) {
+  using L = TcLay4;
+  const int e = ebeg + c * L::KC + (tid & 15);
+  const int slot = (c & (L::MR - 1)) * L::KC + (tid & 15);
+  if (e >= eend) return;
+  switch (tid >> 4) {
+    case 0: cp_async4(smem + L::OFF_MC + 4 * slot, p.side.cols + e); break;
+    case 1: if (p.side.pos) cp_async4(smem + L::OFF_MP + 4 * slot, p.side.pos + e);
+            else reinterpret_cast<int*>(smem + L::OFF_MP)[slot] = e;
+            break;
+    case 2: if (p.side.weights) cp_async4(smem + L::OFF_MW + 4 * slot, p.side.weights + e);
+            else reinterpret_cast<float*>(smem + L::OFF_MW)[slot] = 1.f;
+            break;
+    case 3: if (p.side.labels) cp_async4(smem + L::OFF_MY + 4 * slot, p.side.labels + e);
+            else reinterpret_cast<float*>(smem + L::OFF_MY)[slot] = 1.f;
+            break;
+    default: break;
+  }
+}
+
+IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, int ebeg, int eend, int c, int tid) {
+  using L = TcLay4;
+  const int nk = min(L::KC, eend - (ebeg + c * L::KC));
+  if (nk <= 0) return;
+  const int* mc = reinterpret_cast<const int*>(smem + L::OFF_MC) + (c & (L::MR - 1)) * L::KC;
+  const int* mp = reinterpret_cast<const int*>(smem + L::OFF_MP) + (c & (L::MR - 1)) * L::KC;
+  float* X = reinterpret_cast<float*>(smem + L::OFF_X) + (c & 1) * L::KC * L::XLD;
+  if (p.vec) {
+    const int bv = p.b >> 2;
+    for (int i = tid; i < nk * bv; i += L::NT) {
+      const int k = i / bv, v = i - k * bv;
+      cp_async16(X + k * L::XLD + 4 * v, p.fixed + (size_t)mc[k] * p.ldf + p.b0 + 4 * v);
+    }
+  } else {
+    for (int i = tid; i < nk * p.b; i += L::NT) {
+      const int k = i / p.b, v = i - k * p.b;
+      cp_async4(X + k * L::XLD + v, p.fixed + (size_t)mc[k] * p.ldf + p.b0 + v);
+    }
+  }
+  if (tid < nk)
+    cp_async4(smem + L::OFF_CV + 4 * ((c & 3) * L::KC + tid), p.cache + mp[tid]);
+}
+
+IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, double& gacc, int ebeg,
+                             int eend, int tid) {
+  using L = TcLay4;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  const int n = eend - ebeg;
+  const int nch = (n + L::KC - 1) / L::KC;
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t idesc = make_idesc_tf32(128, 128, 0, 0, 0);
+  uint32_t pend = 0;   // bit x: bar[x] has an outstanding commit
+  if (nch == 0) return 0;
+  // prologue: metadata of chunks 0..3, then X / yhat of chunks 0 and 1
+  for (int c = 0; c < 4 && c < nch; ++c) tc4_meta(p, smem, ebeg, eend, c, tid);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  tc4_gather(p, smem, ebeg, eend, 0, tid);
+  cp_async_commit();
+  tc4_gather(p, smem, ebeg, eend, 1, tid);
+  cp_async_commit();
+  for (int c = 0; c < nch; ++c) {
+    const int xb = c & 1;
+    const int nk = min(L::KC, eend - (ebeg + c * L::KC));
+    cp_async_wait<1>();
+    __syncthreads();
+    const float* X = reinterpret_cast<const float*>(smem + L::OFF_X) + xb * L::KC * L::XLD;
+    const int ms = (c & (L::MR - 1)) * L::KC;
+    const float* mw = reinterpret_cast<const float*>(smem + L::OFF_MW) + ms;
+    const float* my = reinterpret_cast<const float*>(smem + L::OFF_MY) + ms;
+    const float* cv = reinterpret_cast<const float*>(smem + L::OFF_CV) + (c & 3) * L::KC;
+    {  // fp64 gradient, thread j <-> column j; fixed-order chains
+      double g0 = 0.0, g1 = 0.0;
+      int k = 0;
+      for (; k + 1 < nk; k += 2) {
+        g0 = fma((double)(mw[k] * (cv[k] - my[k])), (double)X[k * L::XLD + tid], g0);
+        g1 = fma((double)(mw[k + 1] * (cv[k + 1] - my[k + 1])), (double)X[(k + 1) * L::XLD + tid], g1);
+      }
+      if (k < nk) g0 = fma((double)(mw[k] * (cv[k] - my[k])), (double)X[k * L::XLD + tid], g0);
+      gacc += g0 + g1;
+    }
+    // the operand buffer xb was last read by chunk c-2's MMAs
+    if (pend & (1u << xb)) {
+      mbar_wait(bar + xb, (st.ph >> xb) & 1u);
+      st.ph ^= 1u << xb;
+      pend &= ~(1u << xb);
+    }
+    {  // transpose + scale by sqrt(a) + tf32 split: lane&15 <-> entry,
+       // rows [32 warp + 16 (lane>>4), +16)
+      float* XTH = reinterpret_cast<float*>(smem + L::OFF_XT + xb * 16384);
+      float* XTL = XTH + 2048;
+      const int k = lane & 15;
+      const bool ok = k < nk;
+      const float sa = ok ? sqrtf(mw[k]) : 0.f;
+      const int mb = warp * 32 + (lane >> 4) * 16;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int m0 = mb + 4 * q;
+        // columns >= b are not gathered (the staging buffer is reused between
+        // rows): the operand rows m >= b must be zero
+        float4 v = (ok && m0 < p.b) ? *reinterpret_cast<const float4*>(X + k * L::XLD + m0)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float e[4] = {v.x * sa, (m0 + 1 < p.b) ? v.y * sa : 0.f,
+                            (m0 + 2 < p.b) ? v.z * sa : 0.f, (m0 + 3 < p.b) ? v.w * sa : 0.f};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int idx = xt64_index(m0 + i, k);
+          const float hi = tf32_rna(e[i]);
+          XTH[idx] = hi;
+          XTL[idx] = tf32_rna(e[i] - hi);
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t hi = smem_u32(smem + L::OFF_XT + xb * 16384), lo = hi + 8192;
+      const int ksteps = (nk + 7) >> 3;
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const uint64_t ah = make_sdesc(hi + ks * 32, 16, 512, kSwizzle64B);
+        const uint64_t al = make_sdesc(lo + ks * 32, 16, 512, kSwizzle64B);
+        umma_tf32(st.tmem, ah, ah, idesc, 1);
+        umma_tf32(st.tmem, ah, al, idesc, 1);
+        umma_tf32(st.tmem, al, ah, idesc, 1);
+      }
+      umma_commit(bar + xb);
+    }
+    pend |= 1u << xb;
+    // group c: X / yhat of chunk c+2 (its buffers were consumed above), and
+    // the metadata of chunk c+4
+    if (c + 2 < nch) tc4_gather(p, smem, ebeg, eend, c + 2, tid);
+    if (c + 4 < nch) tc4_meta(p, smem, ebeg, eend, c + 4, tid);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int xb = 0; xb < 2; ++xb)
+    if (pend & (1u << xb)) {
+      mbar_wait(bar + xb, (st.ph >> xb) & 1u);
+      st.ph ^= 1u << xb;
+    }
+  tc_fence_after();
+  return nch;
+}
+
+// step 3: Cholesky of the TMEM matrix + forward solve, written straight into
+// the packed L the backward solve reads; 1/diag in OFF_ID, forward-solved y
+// in OFF_YF.  Per 8-column panel (c0 = 8p):
+//   * every row loads its panel entries from TMEM (fully updated: the
+//     trailing MMA of the previous panel has completed);
+//   * the 8 rows of the diagonal block are 8 consecutive lanes of one warp:
+//     that warp gathers the block with shuffles, factors it (forward solve
+//     included) and publishes it;
+//   * every row below solves against the block (forward solve fused);
+//   * l goes to the packed L and, split hi/lo, to the panel operand of the
+//     3xTF32 trailing update D -= L_p L_p^T (columns >= cs only).
+IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32_t row_addr, int row,
+                          int tid, bool prof = false) {
+  long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool watch = prof && (tid == 0 || tid == 64 || tid == 96);
+  using L = TcLay4;
+  float* DG = reinterpret_cast<float*>(smem + L::OFF_DG);
+  float* RV = reinterpret_cast<float*>(smem + L::OFF_RV);
+  float* YP = reinterpret_cast<float*>(smem + L::OFF_YP);
+  float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
+  float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
+  float* invd = reinterpret_cast<float*>(smem + L::OFF_ID);
+  const float* DIAG = reinterpret_cast<const float*>(smem + L::OFF_DIAG);
+  int* FLAG = reinterpret_cast<int*>(smem + L::OFF_FLAG);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  float* lrow = reinterpret_cast<float*>(smem + L::OFF_L) + tid * (tid + 1) / 2;   // packed row
+  const int b = p.b, i = tid, lane = tid & 31, warp = tid >> 5;
+  const int np = (b + 7) >> 3;
+  const unsigned full = 0xffffffffu;
+  (void)row;
+  float yi = ys[i];
+  for (int pp = 0; pp < np; ++pp) {
+    const int c0 = pp * 8;
+    float v[8];
+    tmem_ld8(row_addr + c0, v);
+    tmem_wait_ld();
+    if (watch && pp == 8) acc[6] = clock64();
+    if (warp == (c0 >> 5)) {
+      // the diagonal block's rows are lanes base..base+7 of this warp: every
+      // lane gathers the block with shuffles and factors it redundantly (a
+      // short dependent chain; a lane-parallel version is shuffle-latency
+      // bound), lane `base` publishes it
+      const int base = c0 & 31;
+      float a[8][8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int m = 0; m <= q; ++m) a[q][m] = __shfl_sync(full, v[m], base + q);
+      float py[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) py[q] = __shfl_sync(full, yi, base + q);
+      float dref[8];
+      {
+        const float4 d0 = *reinterpret_cast<const float4*>(DIAG + c0);
+        const float4 d1 = *reinterpret_cast<const float4*>(DIAG + c0 + 4);
+        dref[0] = d0.x; dref[1] = d0.y; dref[2] = d0.z; dref[3] = d0.w;
+        dref[4] = d1.x; dref[5] = d1.y; dref[6] = d1.z; dref[7] = d1.w;
+      }
+      float rinv[8];
+      bool redo = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float dk = a[k][k];
+        // a pivot that lost more than cond_max of its diagonal to
+        // cancellation (or is not positive) is beyond what the 3xTF32
+        // Hessian resolves: the row goes to the FP32 SIMT sweep
+        if (c0 + k < b && !(dk > 0.f && dk < 3.0e38f && dref[k] <= p.cond_max * dk)) redo = true;
+        if (!(dk > 0.f) || !(dk < 3.0e38f)) dk = 1.f;
+        const float r = rsqrtf(dk);
+        rinv[k] = r;
+        a[k][k] = dk * r;
+#pragma unroll
+        for (int q = k + 1; q < 8; ++q) a[q][k] *= r;
+#pragma unroll
+        for (int q = k + 1; q < 8; ++q)
+#pragma unroll
+          for (int m = k + 1; m <= q; ++m) a[q][m] = fmaf(-a[q][k], a[m][k], a[q][m]);
+      }
+      float yp[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float t = py[q];
+#pragma unroll
+        for (int m = 0; m < q; ++m) t = fmaf(-a[q][m], yp[m], t);
+        yp[q] = t * rinv[q];
+      }
+      if (lane == base) {
+        float* Lb = reinterpret_cast<float*>(smem + L::OFF_L);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float w[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) w[m] = (m <= q) ? a[q][m] : 0.f;
+          reinterpret_cast<float4*>(DG)[2 * q] = make_float4(w[0], w[1], w[2], w[3]);
+          reinterpret_cast<float4*>(DG)[2 * q + 1] = make_float4(w[4], w[5], w[6], w[7]);
+          const int gq = c0 + q;
+#pragma unroll
+          for (int m = 0; m <= q; ++m) Lb[gq * (gq + 1) / 2 + c0 + m] = a[q][m];
+        }
+        reinterpret_cast<float4*>(RV)[0] = make_float4(rinv[0], rinv[1], rinv[2], rinv[3]);
+        reinterpret_cast<float4*>(RV)[1] = make_float4(rinv[4], rinv[5], rinv[6], rinv[7]);
+        reinterpret_cast<float4*>(YP)[0] = make_float4(yp[0], yp[1], yp[2], yp[3]);
+        reinterpret_cast<float4*>(YP)[1] = make_float4(yp[4], yp[5], yp[6], yp[7]);
+        *reinterpret_cast<float4*>(invd + c0) = make_float4(rinv[0], rinv[1], rinv[2], rinv[3]);
+        *reinterpret_cast<float4*>(invd + c0 + 4) = make_float4(rinv[4], rinv[5], rinv[6], rinv[7]);
+        *reinterpret_cast<float4*>(yf + c0) = make_float4(yp[0], yp[1], yp[2], yp[3]);
+        *reinterpret_cast<float4*>(yf + c0 + 4) = make_float4(yp[4], yp[5], yp[6], yp[7]);
+      }
+      if (redo && lane == base) *FLAG = 1;
+    }
+    __syncthreads();
+    if (watch && pp == 8) acc[1] = clock64();
+    float l[8];
+    if (i >= c0 + 8 && i < b) {
+      const float4 r0 = reinterpret_cast<const float4*>(RV)[0], r1 = reinterpret_cast<const float4*>(RV)[1];
+      const float4 y0 = reinterpret_cast<const float4*>(YP)[0], y1 = reinterpret_cast<const float4*>(YP)[1];
+      const float rinv[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      const float yp[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x0 = reinterpret_cast<const float4*>(DG)[2 * q];
+        const float4 x1 = reinterpret_cast<const float4*>(DG)[2 * q + 1];
+        const float w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        float tt = v[q];
+#pragma unroll
+        for (int m = 0; m < q; ++m) tt = fmaf(-l[m], w[m], tt);
+        l[q] = tt * rinv[q];
+        yi = fmaf(-l[q], yp[q], yi);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) lrow[c0 + q] = l[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) l[q] = 0.f;   // no part in the trailing update
+    }
+    if (watch && pp == 8) acc[3] = clock64();
+    if (pp + 1 < np) {
+      float* PAH = reinterpret_cast<float*>(smem + L::OFF_PA_HI);
+      float* PAL = PAH + 1024;   // 4 KB apart
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float hi = tf32_rna(l[q]);
+        PAH[pa_index(i, q)] = hi;
+        PAL[pa_index(i, q)] = tf32_rna(l[q] - hi);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (watch && pp == 8) acc[4] = clock64();
+      if (tid == 0) {
+        tc_fence_after();
+        const int cs = ((c0 + 8) >> 4) << 4;   // N = 128 - cs, a multiple of 16
+        const uint32_t idesc_neg = make_idesc_tf32(128, 128 - cs, 0, 0, 1);
+        const uint32_t ph = smem_u32(PAH), pl = smem_u32(PAL);
+        const uint64_t ah = make_sdesc(ph, 128, 256, kSwizzleNone);
+        const uint64_t al = make_sdesc(pl, 128, 256, kSwizzleNone);
+        const uint64_t bh = make_sdesc(ph + (cs >> 3) * 256, 128, 256, kSwizzleNone);
+        const uint64_t bl = make_sdesc(pl + (cs >> 3) * 256, 128, 256, kSwizzleNone);
+        umma_tf32(st.tmem + cs, ah, bh, idesc_neg, 1);
+        umma_tf32(st.tmem + cs, ah, bl, idesc_neg, 1);
+        umma_tf32(st.tmem + cs, al, bh, idesc_neg, 1);
+        umma_commit(bar);
+      }
+      mbar_wait(bar, st.ph & 1u);
+      if (watch && pp == 8) acc[5] = clock64();
+      st.ph ^= 1u;
+      tc_fence_after();
+    }
+  }
+  __syncthreads();
+  if (watch) {
+    const int w = tid == 0 ? 0 : (tid == 64 ? 1 : 2);
+    for (int k = 0; k < 8; ++k) p.dbg[8192 + (blockIdx.x * 3 + w) * 8 + k] = acc[k];
+  }
+}
+
+// Inverses of the 8x8 diagonal blocks of L (from the packed copy), all at
+// once: thread t forms column q = t % 8 of block t / 8 by forward
+// substitution with the stored reciprocal pivots.  LI[blk][m][q].
+IALS_DEVI void tc4_block_inverses(const SweepParams& p, char* smem, int tid) {
+  using L = TcLay4;
+  const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L);
+  const float* invd = reinterpret_cast<const float*>(smem + L::OFF_ID);
+  float* LI = reinterpret_cast<float*>(smem + L::OFF_LI);
+  const int np = (p.b + 7) >> 3, blk = tid >> 3, q = tid & 7, c0 = 8 * blk;
+  if (blk >= np) return;
+  float x[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int gm = c0 + m;
+    float t = (m == q) ? 1.f : 0.f;
+#pragma unroll
+    for (int k = 0; k < m; ++k)
+      if (gm < p.b) t = fmaf(-Lp[gm * (gm + 1) / 2 + c0 + k], x[k], t);
+    x[m] = (m >= q && gm < p.b) ? t * invd[gm] : 0.f;
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) LI[blk * 64 + m * 8 + q] = x[m];
+}
+
+// Backward solve L^T d = y from the last panel: d_panel = L11^-T y_panel (a
+// mat-vec with the precomputed inverse), then every row r < c0 folds the
+// panel into its own y_r; one barrier per panel.
+IALS_DEVI void tc4_backward(const SweepParams& p, char* smem, int tid) {
+  using L = TcLay4;
+  const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L);
+  const float* LI = reinterpret_cast<const float*>(smem + L::OFF_LI);
+  float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
+  float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
+  const int b = p.b;
+  const int np = (b + 7) >> 3;
+  float yr = (tid < b) ? yf[tid] : 0.f;
+  for (int pp = np - 1; pp >= 0; --pp) {
+    const int c0 = pp * 8;
+    float yp[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) yp[m] = (c0 + m < b) ? yf[c0 + m] : 0.f;
+    const float* li = LI + pp * 64;
+    float dlt[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {   // (L11^-T y)_q = sum_{m >= q} LI[m][q] y_m
+      float t = 0.f;
+#pragma unroll
+      for (int m = q; m < 8; ++m) t = fmaf(li[m * 8 + q], yp[m], t);
+      dlt[q] = (c0 + q < b) ? t : 0.f;
+    }
+    if (tid >= c0 && tid < c0 + 8 && tid < b) {
+      const int e = tid - c0;
+      const float a0 = (e & 1) ? dlt[1] : dlt[0], a1 = (e & 1) ? dlt[3] : dlt[2];
+      const float a2 = (e & 1) ? dlt[5] : dlt[4], a3 = (e & 1) ? dlt[7] : dlt[6];
+      const float b0 = (e & 2) ? a1 : a0, b1 = (e & 2) ? a3 : a2;
+      ds[tid] = (e & 4) ? b1 : b0;
+    }
+    if (tid < c0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int gq = c0 + q;
+        if (gq < b) yr = fmaf(-Lp[gq * (gq + 1) / 2 + tid], dlt[q], yr);
+      }
+      if (tid >= c0 - 8) yf[tid] = yr;   // the next panel's entries
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
+  using L = TcLay4;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = tc_smem_base(smem_raw);
+  const int tid = threadIdx.x;
+  {  // finite staging everywhere (padding columns / short chunks read zeros)
+    float4* x = reinterpret_cast<float4*>(smem + L::OFF_X);
+    for (int i = tid; i < 2 * L::KC * L::XLD / 4; i += L::NT) x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + 16);
+  float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
+  float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
+  ds[tid] = 0.f;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  if (tid < 32) tmem_alloc(tptr, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  Tc4State st;
+  st.tmem = *tptr;
+  st.ph = 0u;
+  const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
+  const int b = p.b;
+  int ndone = 0;
+  long long tph[8];
+  // profiling: phase clocks of the CTA's rec_row-th row (dbg[32767] picks it; dbg holds 32K int64)
+  const int rec_row = p.dbg ? (int)p.dbg[32767] : -1;
+  for (int task = blockIdx.x; task < p.n_light; task += gridDim.x) {
+    const bool rec = ndone == rec_row && tid == 0;
+    if (rec) tph[0] = clock64();
+    const int row = p.light_rows[task];
+    const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
+    const float lam = p.side.lam[row];
+    tc4_init(p, row_addr, lam, tid);
+    if (rec) tph[1] = clock64();
+    tmem_wait_st();
+    tc_fence_before();   // the first chunk's barrier orders these stores before the MMAs
+    double gacc = 0.0;
+    const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid);
+    if (rec) tph[2] = clock64();
+    {  // the diagonal before factorisation (for the cancellation check):
+       // lane l of warp w picks column 32w + l with a select tree (an indexed
+       // register read would go through local memory)
+      const int lane = tid & 31, e = lane & 7;
+      float dg = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v[8];
+        tmem_ld8(row_addr + 32 * (tid >> 5) + 8 * j, v);
+        tmem_wait_ld();
+        const float a0 = (e & 1) ? v[1] : v[0], a1 = (e & 1) ? v[3] : v[2];
+        const float a2 = (e & 1) ? v[5] : v[4], a3 = (e & 1) ? v[7] : v[6];
+        const float b0 = (e & 2) ? a1 : a0, b1 = (e & 2) ? a3 : a2;
+        if ((lane >> 3) == j) dg = (e & 4) ? b1 : b0;
+      }
+      reinterpret_cast<float*>(smem + L::OFF_DIAG)[tid] = dg;
+      if (tid == 0) *reinterpret_cast<int*>(smem + L::OFF_FLAG) = 0;
+    }
+    {
+      float gv = 0.f;
+      if (tid < b)
+        gv = (float)(gacc + (double)p.proj[(size_t)row * b + tid] +
+                     (double)lam * (double)p.own[(size_t)row * p.ldo + p.b0 + tid]);
+      ys[tid] = gv;
+    }
+    __syncthreads();
+    if (rec) tph[3] = clock64();
+    tc4_factor(p, smem, st, row_addr, row, tid, ndone == rec_row);
+    if (rec) tph[4] = clock64();
+    (void)nch;
+    if (*reinterpret_cast<volatile int*>(smem + L::OFF_FLAG)) {
+      // the SIMT sweep redoes this row (its own cache update included)
+      if (tid == 0) {
+        p.redo_rows[atomicAdd(p.redo_cnt, 1)] = row;
+        atomicAdd(p.redo_total, 1ull);
+      }
+      if (tid < b) p.drow[(size_t)row * b + tid] = 0.f;
+    } else {
+      tc4_block_inverses(p, smem, tid);
+      __syncthreads();
+      tc4_backward(p, smem, tid);
+      if (rec) tph[5] = clock64();
+      if (tid < b) {
+        p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
+        p.drow[(size_t)row * b + tid] = ds[tid];   // for k_pass_cache
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (rec) {
+      tph[6] = clock64();
+      tph[7] = eend - ebeg;
+      for (int k = 0; k < 8; ++k) p.dbg[blockIdx.x * 8 + k] = tph[k];
+    }
+    ++ndone;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_free(st.tmem, 128);
+}
+
+// yhat[pos] -= x . d for every entry of the pass: light rows take d from
+// drow (the fused sweep's output; zero for rows the SIMT sweep redid), heavy
+// slices from hdelta.  8 lanes x 16 columns per entry, 32 entries in flight
+// per CTA; bandwidth-bound gather, so it runs as its own full-occupancy pass.
+__global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
+  const int tid = threadIdx.x, g = tid & 7, slot = tid >> 3;
+  const int blk = blockIdx.x;
+  const float* d;
+  int ebeg, eend;
+  if (blk < p.n_light) {
+    const int row = p.light_rows[blk];
+    ebeg = p.side.ptr[row];
+    eend = p.side.ptr[row + 1];
+    d = p.drow + (size_t)row * p.b;
+  } else {
+    const int sl = blk - p.n_light;
+    ebeg = p.slice_begin[sl];
+    eend = p.slice_end[sl];
+    d = p.hdelta + (size_t)p.slice_heavy[sl] * 128;
+  }
+  const int b = p.b, c0 = 16 * g;
+  float dv[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) dv[j] = (c0 + j < b) ? __ldg(d + c0 + j) : 0.f;
+  for (int e = ebeg + slot; e < eend; e += 32) {
+    const int col = __ldg(p.side.cols + e);
+    const float* xr = p.fixed + (size_t)col * p.ldf + p.b0 + c0;
+    float s = 0.f;
+    if (p.vec) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c0 + 4 * q < b) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(xr) + q);
+          s = fmaf(x.x, dv[4 * q], s);
+          s = fmaf(x.y, dv[4 * q + 1], s);
+          s = fmaf(x.z, dv[4 * q + 2], s);
+          s = fmaf(x.w, dv[4 * q + 3], s);
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < b) s = fmaf(__ldg(xr + j), dv[j], s);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (g == 0) {
+      const int pos = p.side.pos ? __ldg(p.side.pos + e) : e;
+      p.cache[pos] -= s;
+    }
+  }
+}
+
+}  // namespace ials

@@ -143,4 +143,12 @@ IALS_DEVI float tf32_lo(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+// round-to-nearest tf32 (low 13 bits zero): the unbiased split
+// hi = rna(x), lo = rna(x - hi) leaves |x - hi - lo| <= 2^-22 |x|.
+IALS_DEVI float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 }  // namespace ials

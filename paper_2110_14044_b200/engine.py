@@ -76,6 +76,13 @@ class Session:
             raise ValueError(f"{what}: {msg}")
         raise RuntimeError(f"{what}: {msg}")
 
+    def tc_redo_rows(self, reset: bool = False) -> int:
+        """Rows the fused tensor-core sweep handed back to the SIMT sweep."""
+        n = ctypes.c_int64()
+        self.check(self.lib.ials_tc_redo_rows(self.handle, current_stream_handle(self.device),
+                                              ctypes.byref(n), int(reset)), "tc_redo_rows")
+        return int(n.value)
+
     def reset_singular(self):
         self.check(self.lib.ials_reset_singular(self.handle, current_stream_handle(self.device)),
                    "reset_singular")

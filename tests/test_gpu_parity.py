@@ -169,8 +169,9 @@ def test_heavy_rows_vs_oracle(ials, d, b, I):
 @pytest.mark.parametrize("d,b", [(128, 128), (200, 100), (96, 72), (128, 40), (120, 60),
                                  (100, 98)])
 def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
-    """b in (32, 128] runs the tcgen05 3xTF32 sweep; compare with the oracle
-    and with the FP32 SIMT sweep on the same input (2 epochs)."""
+    """b in (32, 128] runs the tcgen05 3xTF32 sweep (mode 1: wave kernels;
+    mode 2: fused 4-CTA/SM kernel for b > 64); compare with the oracle and
+    with the FP32 SIMT sweep on the same input (2 epochs)."""
     from oracle import ialspp_oracle as orc
     from paper_2110_14044_b200 import _lib
     lib = _lib.load()
@@ -182,22 +183,24 @@ def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
     init.user_factors[:] = init.user_factors.astype(np.float32)
     init.item_factors[:] = init.item_factors.astype(np.float32)
     got = {}
+    prev = lib.ials_set_tensor_cores(0)
     try:
-        for tc in (1, 0):
+        for tc in (1, 2, 0):
             lib.ials_set_tensor_cores(tc)
             m = init.copy()
             ials.train(m, data, cfg)
             got[tc] = m
     finally:
-        lib.ials_set_tensor_cores(0)
+        lib.ials_set_tensor_cores(prev)
     w, h = init.user_factors.copy(), init.item_factors.copy()
     csr = orc.build_csr(U, I, users, items)
     orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
-    for tc in (1, 0):
+    for tc in (1, 2, 0):
         m = got[tc]
         assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL, tc
         assert relmax(m.user_factors, w) < TOL and relmax(m.item_factors, h) < TOL, tc
     assert relf(got[1].user_factors, got[0].user_factors) < 1e-4
+    assert relf(got[2].user_factors, got[0].user_factors) < 1e-4
 
 
 def test_sharded_path_gpu_ops_single_rank(ials):
