@@ -328,6 +328,7 @@ static int set_smem_attrs(ials_session* s) {
   CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_light<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_cache<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   done = true;
   return IALS_OK;
@@ -381,6 +382,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
   using L = Lay<128>;
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
+  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, sizeof(int), st));
   if (p.n_light > 0) {
     static bool init = false;
     if (!init) {
@@ -392,12 +394,28 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
     }
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
-    CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, sizeof(int), st));
     const int grid = std::min(p.n_light, 4 * kNumSMs);   // TMEM: 4 x 128 columns per SM
     k_sweep_tc4<<<grid, 128, TcLay4::BYTES, st>>>(p);
     LAUNCH_CHECK(s);
-    // rows the cancellation check rejected: FP32 SIMT sweep over the device
-    // list (persistent grid, the count is read on the device)
+  }
+  if (p.n_heavy > 0) {
+    static bool hinit = false;
+    if (!hinit) {
+      CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc4,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
+      CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc4,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      hinit = true;
+    }
+    const int threads = L::NT * L::RPC;
+    k_heavy_partial_tc4<<<std::min(p.n_slices, 4 * kNumSMs), 128, TcLay4::BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+    k_heavy_solve<128, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    LAUNCH_CHECK(s);
+  }
+  if (p.n_light + p.n_heavy > 0) {
+    // rows the cancellation checks rejected (light or heavy): FP32 SIMT sweep
+    // over the device list (persistent grid, the count is read on the device)
     static int simt_sm = 0;
     if (simt_sm == 0) {
       CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<128>,
@@ -408,13 +426,6 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
     q.light_rows = p.redo_rows;
     q.n_light_dev = p.redo_cnt;
     k_sweep_light<128><<<simt_sm * kNumSMs, L::NT * L::RPC, L::CTA_BYTES, st>>>(q);
-    LAUNCH_CHECK(s);
-  }
-  if (p.n_heavy > 0) {
-    const int threads = L::NT * L::RPC;
-    k_heavy_partial<128><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-    k_heavy_solve<128><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
   }
   if (p.n_light + p.n_slices > 0) {

@@ -323,7 +323,11 @@ IALS_DEVI int accumulate_range(const SweepParams& p, Tiles<BT>& T, double& gacc,
 //       are final or unused), then the owners publish the next raw panel.
 // The backward solve L^T d = y runs on warp 0 panel by panel from the packed
 // L kept in shared memory.
-template <int BT>
+// GUARD (heavy rows whose Hessian partials came from the tensor core): the
+// original diagonal is kept in the (unused) staging area, and a pivot that
+// lost more than cond_max of it to cancellation flags the row (OFF_X + BT)
+// for the FP32 redo instead of reporting it.
+template <int BT, bool GUARD = false>
 IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gacc, float* sm,
                                   int row, int tid, int team) {
   using L = Lay<BT>;
@@ -350,6 +354,7 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
     ys[tid] = (float)g;
   }
   const float a0 = p.alpha0;
+  if (GUARD && tid == 0) reinterpret_cast<int*>(sm + L::OFF_X + BT)[0] = 0;
 #pragma unroll
   for (int t = 0; t < L::TPW; ++t) {
     if (!T.valid[t]) continue;
@@ -362,7 +367,10 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
         float v;
         if (gi < b && gj < b) {
           v = T.acc[t][i][j] + a0 * __ldg(p.slab + (size_t)(p.b0 + gi) * b + gj);
-          if (gi == gj) v += lam;
+          if (gi == gj) {
+            v += lam;
+            if (GUARD) sm[L::OFF_X + gi] = v;
+          }
         } else {
           v = (gi == gj) ? 1.f : 0.f;
         }
@@ -398,8 +406,11 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
       float rinv[PW];
       int bad = -1;
 #pragma unroll
+      bool cancel = false;
       for (int k = 0; k < PW; ++k) {
         float dk = a[k][k];
+        if (GUARD && c0 + k < b && !(dk > 0.f && dk < 3.0e38f && sm[L::OFF_X + c0 + k] <= p.cond_max * dk))
+          cancel = true;
         if (!(dk > 0.f) || !(dk < 3.0e38f)) {
           if (bad < 0) bad = k;
           dk = 1.f;
@@ -414,7 +425,11 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
 #pragma unroll
           for (int j = k + 1; j <= i; ++j) a[i][j] = fmaf(-a[i][k], a[j][k], a[i][j]);
       }
-      if (bad >= 0 && c0 + bad < b && lane == 0) report_singular(p.err, p.side_id, row, c0 + bad);
+      if (GUARD) {
+        if (cancel && lane == 0) reinterpret_cast<int*>(sm + L::OFF_X + BT)[0] = 1;
+      } else if (bad >= 0 && c0 + bad < b && lane == 0) {
+        report_singular(p.err, p.side_id, row, c0 + bad);
+      }
       float y[PW];
 #pragma unroll
       for (int q = 0; q < PW; ++q) {
@@ -664,7 +679,7 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   if (tid < BT) p.gpart[(size_t)sl * BT + tid] = gacc;
 }
 
-template <int BT>
+template <int BT, bool GUARD = false>
 __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
     k_heavy_solve(SweepParams p) {
   using L = Lay<BT>;
@@ -693,8 +708,18 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
     }
     if (tid < BT) gacc += p.gpart[(size_t)sl * BT + tid];
   }
-  finalize_and_solve<BT>(p, T, gacc, sm, row, tid, team);
+  finalize_and_solve<BT, GUARD>(p, T, gacc, sm, row, tid, team);
   const float* ds = sm + L::OFF_D;
+  if (GUARD && reinterpret_cast<const int*>(sm + L::OFF_X + BT)[0]) {
+    // cancelled pivot: the FP32 SIMT sweep redoes the whole row (its own
+    // cache update included), so nothing of this solve is applied
+    if (tid < p.b) p.hdelta[(size_t)h * BT + tid] = 0.f;
+    if (tid == 0) {
+      p.redo_rows[atomicAdd(p.redo_cnt, 1)] = row;
+      atomicAdd(p.redo_total, 1ull);
+    }
+    return;
+  }
   if (tid < p.b) {
     p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
     p.hdelta[(size_t)h * BT + tid] = ds[tid];

@@ -172,15 +172,26 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
     const float* mw = reinterpret_cast<const float*>(smem + L::OFF_MW) + ms;
     const float* my = reinterpret_cast<const float*>(smem + L::OFF_MY) + ms;
     const float* cv = reinterpret_cast<const float*>(smem + L::OFF_CV) + (c & 3) * L::KC;
-    {  // fp64 gradient, thread j <-> column j; fixed-order chains
+    // thread m <-> factor column m = operand row m: its 16 entries of the
+    // chunk (conflict-free loads) feed the fp64 gradient and the hi/lo split
+    float x[16];
+    const bool colok = tid < p.b;   // columns >= b are not gathered
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = (colok && k < nk) ? X[k * L::XLD + tid] : 0.f;
+    {  // gradient: two fixed-order fp64 chains (even / odd entries)
       double g0 = 0.0, g1 = 0.0;
-      int k = 0;
-      for (; k + 1 < nk; k += 2) {
-        g0 = fma((double)(mw[k] * (cv[k] - my[k])), (double)X[k * L::XLD + tid], g0);
-        g1 = fma((double)(mw[k + 1] * (cv[k + 1] - my[k + 1])), (double)X[(k + 1) * L::XLD + tid], g1);
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) {
+        const float r0 = (k < nk) ? mw[k] * (cv[k] - my[k]) : 0.f;
+        const float r1 = (k + 1 < nk) ? mw[k + 1] * (cv[k + 1] - my[k + 1]) : 0.f;
+        g0 = fma((double)r0, (double)x[k], g0);
+        g1 = fma((double)r1, (double)x[k + 1], g1);
       }
-      if (k < nk) g0 = fma((double)(mw[k] * (cv[k] - my[k])), (double)X[k * L::XLD + tid], g0);
       gacc += g0 + g1;
+    }
+    if (p.side.weights) {  // a h h^T = (sqrt(a) h)(sqrt(a) h)^T
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] *= (k < nk) ? sqrtf(mw[k]) : 0.f;
     }
     // the operand buffer xb was last read by chunk c-2's MMAs
     if (pend & (1u << xb)) {
@@ -188,30 +199,22 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       st.ph ^= 1u << xb;
       pend &= ~(1u << xb);
     }
-    {  // transpose + scale by sqrt(a) + tf32 split: lane&15 <-> entry,
-       // rows [32 warp + 16 (lane>>4), +16)
+    {  // row m of the K-major 64B-swizzled operands: 16-byte chunk c (entries
+       // 4c..4c+3) at chunk c ^ ((m / 2) % 4) of the row's 64 bytes
       float* XTH = reinterpret_cast<float*>(smem + L::OFF_XT + xb * 16384);
       float* XTL = XTH + 2048;
-      const int k = lane & 15;
-      const bool ok = k < nk;
-      const float sa = ok ? sqrtf(mw[k]) : 0.f;
-      const int mb = warp * 32 + (lane >> 4) * 16;
+      const int m = tid, rb = (m >> 3) * 128 + (m & 7) * 16, sw = (m >> 1) & 3;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int m0 = mb + 4 * q;
-        // columns >= b are not gathered (the staging buffer is reused between
-        // rows): the operand rows m >= b must be zero
-        float4 v = (ok && m0 < p.b) ? *reinterpret_cast<const float4*>(X + k * L::XLD + m0)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float e[4] = {v.x * sa, (m0 + 1 < p.b) ? v.y * sa : 0.f,
-                            (m0 + 2 < p.b) ? v.z * sa : 0.f, (m0 + 3 < p.b) ? v.w * sa : 0.f};
+      for (int c = 0; c < 4; ++c) {
+        float hi[4], lo[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int idx = xt64_index(m0 + i, k);
-          const float hi = tf32_rna(e[i]);
-          XTH[idx] = hi;
-          XTL[idx] = tf32_rna(e[i] - hi);
+        for (int j = 0; j < 4; ++j) {
+          hi[j] = tf32_rna(x[4 * c + j]);
+          lo[j] = tf32_rna(x[4 * c + j] - hi[j]);
         }
+        const int o = rb + ((c ^ sw) << 2);
+        *reinterpret_cast<float4*>(XTH + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(XTL + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
       }
     }
     fence_proxy_async_smem();
@@ -593,6 +596,60 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
       for (int k = 0; k < 8; ++k) p.dbg[blockIdx.x * 8 + k] = tph[k];
     }
     ++ndone;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_free(st.tmem, 128);
+}
+
+// Heavy-row slices on the tensor core: each slice's partial Hessian is summed
+// from zero in TMEM (same pipelined gather / 3xTF32 MMAs as the light rows)
+// and written row-major (the layout k_heavy_solve<128> reads) with its fp64
+// partial gradient; the slices of a row are combined in k_heavy_solve.
+__global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p) {
+  using L = TcLay4;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = tc_smem_base(smem_raw);
+  const int tid = threadIdx.x;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + 16);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  if (tid < 32) tmem_alloc(tptr, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  Tc4State st;
+  st.tmem = *tptr;
+  st.ph = 0u;
+  const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
+  for (int sl = blockIdx.x; sl < p.n_slices; sl += gridDim.x) {
+    {
+      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c8 = 0; c8 < 16; ++c8) tmem_st8(row_addr + 8 * c8, z);
+      tmem_wait_st();
+      tc_fence_before();   // ordered before the MMAs by the first chunk's barrier
+    }
+    double gacc = 0.0;
+    tc4_accumulate(p, smem, st, gacc, p.slice_begin[sl], p.slice_end[sl], tid);
+    float* hp = p.hpart + (size_t)sl * 128 * 128 + (size_t)tid * 128;
+#pragma unroll
+    for (int c32 = 0; c32 < 4; ++c32) {
+      float v[32];
+      tmem_ld32(row_addr + 32 * c32, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(hp + 32 * c32 + 4 * q) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    p.gpart[(size_t)sl * 128 + tid] = gacc;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
   }
   tc_fence_before();
   __syncthreads();
