@@ -41,9 +41,11 @@ struct TcLay4 {
   static constexpr int OFF_MY = OFF_MW + MR * KC * 4;          //                labels
   static constexpr int OFF_CV = OFF_MY + MR * KC * 4;          // [4][KC] gathered yhat
   static constexpr int OFF_DG = OFF_CV + 4 * KC * 4;
+  // factored diagonal block of the panel (DG 8x8, 1/pivots RV, y YP),
+  // double-buffered by panel parity: buffer x = OFF_DG + x * 320
   static constexpr int OFF_RV = OFF_DG + 64 * 4;
   static constexpr int OFF_YP = OFF_RV + 8 * 4;
-  static constexpr int OFF_Y = OFF_YP + 8 * 4;
+  static constexpr int OFF_Y = OFF_DG + 2 * 320;
   static constexpr int OFF_YF = OFF_Y + BT * 4;
   static constexpr int OFF_ID = OFF_YF + BT * 4;
   static constexpr int OFF_D = OFF_ID + BT * 4;
@@ -267,9 +269,6 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
   long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const bool watch = prof && (tid == 0 || tid == 64 || tid == 96);
   using L = TcLay4;
-  float* DG = reinterpret_cast<float*>(smem + L::OFF_DG);
-  float* RV = reinterpret_cast<float*>(smem + L::OFF_RV);
-  float* YP = reinterpret_cast<float*>(smem + L::OFF_YP);
   float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
   float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
   float* invd = reinterpret_cast<float*>(smem + L::OFF_ID);
@@ -284,6 +283,9 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
   float yi = ys[i];
   for (int pp = 0; pp < np; ++pp) {
     const int c0 = pp * 8;
+    float* DG = reinterpret_cast<float*>(smem + L::OFF_DG + (pp & 1) * 320);
+    float* RV = reinterpret_cast<float*>(smem + L::OFF_RV + (pp & 1) * 320);
+    float* YP = reinterpret_cast<float*>(smem + L::OFF_YP + (pp & 1) * 320);
     float v[8];
     tmem_ld8(row_addr + c0, v);
     tmem_wait_ld();
@@ -302,13 +304,6 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
       float py[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) py[q] = __shfl_sync(full, yi, base + q);
-      float dref[8];
-      {
-        const float4 d0 = *reinterpret_cast<const float4*>(DIAG + c0);
-        const float4 d1 = *reinterpret_cast<const float4*>(DIAG + c0 + 4);
-        dref[0] = d0.x; dref[1] = d0.y; dref[2] = d0.z; dref[3] = d0.w;
-        dref[4] = d1.x; dref[5] = d1.y; dref[6] = d1.z; dref[7] = d1.w;
-      }
       float rinv[8];
       bool redo = false;
 #pragma unroll
@@ -317,8 +312,10 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         // a pivot that lost more than cond_max of its diagonal to
         // cancellation (or is not positive) is beyond what the 3xTF32
         // Hessian resolves: the row goes to the FP32 SIMT sweep
-        if (c0 + k < b && !(dk > 0.f && dk < 3.0e38f && dref[k] <= p.cond_max * dk)) redo = true;
-        if (!(dk > 0.f) || !(dk < 3.0e38f)) dk = 1.f;
+        if (!(dk > 0.f && dk < 3.0e38f)) {
+          redo = true;   // non-positive pivot (the cancellation test is done off the chain)
+          dk = 1.f;
+        }
         const float r = rsqrtf(dk);
         rinv[k] = r;
         a[k][k] = dk * r;
@@ -337,8 +334,7 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         for (int m = 0; m < q; ++m) t = fmaf(-a[q][m], yp[m], t);
         yp[q] = t * rinv[q];
       }
-      if (lane == base) {
-        float* Lb = reinterpret_cast<float*>(smem + L::OFF_L);
+      if (lane == base) {   // only what the other rows wait for
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float w[8];
@@ -346,23 +342,35 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
           for (int m = 0; m < 8; ++m) w[m] = (m <= q) ? a[q][m] : 0.f;
           reinterpret_cast<float4*>(DG)[2 * q] = make_float4(w[0], w[1], w[2], w[3]);
           reinterpret_cast<float4*>(DG)[2 * q + 1] = make_float4(w[4], w[5], w[6], w[7]);
-          const int gq = c0 + q;
-#pragma unroll
-          for (int m = 0; m <= q; ++m) Lb[gq * (gq + 1) / 2 + c0 + m] = a[q][m];
         }
         reinterpret_cast<float4*>(RV)[0] = make_float4(rinv[0], rinv[1], rinv[2], rinv[3]);
         reinterpret_cast<float4*>(RV)[1] = make_float4(rinv[4], rinv[5], rinv[6], rinv[7]);
         reinterpret_cast<float4*>(YP)[0] = make_float4(yp[0], yp[1], yp[2], yp[3]);
         reinterpret_cast<float4*>(YP)[1] = make_float4(yp[4], yp[5], yp[6], yp[7]);
-        *reinterpret_cast<float4*>(invd + c0) = make_float4(rinv[0], rinv[1], rinv[2], rinv[3]);
-        *reinterpret_cast<float4*>(invd + c0 + 4) = make_float4(rinv[4], rinv[5], rinv[6], rinv[7]);
-        *reinterpret_cast<float4*>(yf + c0) = make_float4(yp[0], yp[1], yp[2], yp[3]);
-        *reinterpret_cast<float4*>(yf + c0 + 4) = make_float4(yp[4], yp[5], yp[6], yp[7]);
       }
       if (redo && lane == base) *FLAG = 1;
     }
     __syncthreads();
     if (watch && pp == 8) acc[1] = clock64();
+    // the block's rows record their part of L, 1/pivot and y, and test the
+    // pivot for cancellation: one that lost more than cond_max of its
+    // diagonal is beyond what the 3xTF32 Hessian resolves (FP32 SIMT redo).
+    // Runs in the shadow of the trailing MMA (buffers are double-buffered).
+    auto record_block = [&]() {
+      if (i >= c0 && i < c0 + 8) {
+        const int j = i - c0;
+        const float4 x0 = reinterpret_cast<const float4*>(DG)[2 * j];
+        const float4 x1 = reinterpret_cast<const float4*>(DG)[2 * j + 1];
+        const float w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          if (m <= j) lrow[c0 + m] = w[m];
+        const float r = RV[j];
+        invd[i] = r;
+        yf[i] = YP[j];
+        if (i < b && !(DIAG[i] * (r * r) <= p.cond_max)) *FLAG = 1;
+      }
+    };
     float l[8];
     if (i >= c0 + 8 && i < b) {
       const float4 r0 = reinterpret_cast<const float4*>(RV)[0], r1 = reinterpret_cast<const float4*>(RV)[1];
@@ -414,10 +422,13 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         umma_tf32(st.tmem + cs, al, bh, idesc_neg, 1);
         umma_commit(bar);
       }
+      record_block();
       mbar_wait(bar, st.ph & 1u);
       if (watch && pp == 8) acc[5] = clock64();
       st.ph ^= 1u;
       tc_fence_after();
+    } else {
+      record_block();
     }
   }
   __syncthreads();
