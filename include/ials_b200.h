@@ -181,6 +181,18 @@ int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sch
 /* One full iALS++ epoch (ialspp_epoch, solvers.py:340-375) over contiguous
  * blocks of width b (the last keeps the remainder): cache recompute, then
  * per block slab(H) -> user pass -> slab(W) -> item pass. */
+/* Profiling: cudaEvent_t handles that ials_epoch records at its phase
+ * boundaries (0: start, 1: after the prediction cache, then per block: after
+ * the user-side Gramian, after the user pass, after the item-side Gramian,
+ * after the item pass); n = 0 disables.  At most 2 + 4 * 1024 events. */
+int ials_epoch_events(void* const* events, int32_t n);
+
+/* Extra workspace ials_epoch can use for its tensor-core GEMM path (b in
+ * 65..128 with the fused sweep): K-major copies of W and H and the Gramian
+ * split partials.  Pass a workspace of ials_workspace_bytes(...) plus this
+ * to enable it; with less, the epoch uses the FP32 SIMT GEMMs. */
+size_t ials_epoch_tc_bytes(int32_t n_users, int32_t n_items, int32_t d, int32_t b);
+
 int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
                float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,

@@ -59,6 +59,8 @@ SIGNATURES = {
     "ials_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
     "ials_tc_workspace_bytes": (c_sz, [c_i32, c_i32]),
     "ials_tc_wave_slices": (c_i32, []),
+    "ials_epoch_tc_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32]),
+    "ials_epoch_events": (c_i32, [ctypes.POINTER(c_p), c_i32]),
     "ials_predictions": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_i32, c_p, c_i32, c_i32, c_p, c_p]),
     "ials_predictions_segments": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_i32, c_p, c_i32,
                                           c_i32, c_p, c_p]),

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "../../include/ials_b200.h"
 #include "ials_common.cuh"
@@ -18,6 +19,7 @@
 #include "ials_sweep_tc.cuh"
 #include "ials_sweep_tc2.cuh"
 #include "ials_sweep_tc4.cuh"
+#include "ials_gemm_tc.cuh"
 #include "ials_sweep_b1.cuh"
 
 using namespace ials;
@@ -569,7 +571,8 @@ static int launch_sweep(ials_session* s, const SweepParams& p, cudaStream_t st) 
 static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sched* sched,
                           const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
                           int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
-                          int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st) {
+                          int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st,
+                          bool proj_ready = false) {
   if (!side || !sched || !fixed || !own || !slab || !cache)
     return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
   if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
@@ -649,7 +652,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.gbuf = nullptr;
     p.dbuf = nullptr;
   }
-  if (side->n_rows > 0) {
+  if (side->n_rows > 0 && !proj_ready) {
     if (b <= 16) {
       k_project_narrow<<<(side->n_rows + 127) / 128, 256, 0, st>>>(own, side->n_rows, ldo, d, slab,
                                                                     b, alpha0, proj);
@@ -695,6 +698,163 @@ int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sch
                         side_id, static_cast<char*>(workspace), ws_bytes, S(stream));
 }
 
+
+// ------------------------------------------------------------------ tensor-core GEMMs (epoch)
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encode(ials_session* s) {
+  if (g_encode) return IALS_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(s, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return IALS_OK;
+}
+
+// 2-D fp32 map: `inner` contiguous elements per row, `rows` rows ld_floats
+// apart; boxes of 32 x box_rows land 128B-swizzled (K-major operand rows)
+static int make_map(ials_session* s, CUtensorMap* m, const float* ptr, uint64_t inner, uint64_t rows,
+                    uint64_t ld_floats, uint32_t box_rows) {
+  cuuint64_t gdim[2] = {inner, rows};
+  cuuint64_t gstr[1] = {ld_floats * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim,
+                              gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return IALS_OK;
+}
+
+static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+// split-K plan of the Gramian: >= 2 CTAs per SM and at most 2048 rows
+// accumulated in TMEM per CTA
+static void gram_plan(int n, int d, int* splits, int* span) {
+  const int mt = (d + 127) / 128;
+  int S = std::max((n + 2047) / 2048, (2 * kNumSMs + mt - 1) / mt);
+  S = std::max(1, std::min(S, std::max(1, n / 32)));
+  int sp = rup((n + S - 1) / S, kGemmKC);
+  *span = std::max(sp, kGemmKC);
+  *splits = std::max(1, (n + *span - 1) / *span);
+}
+
+struct TcCopies {   // K-major copies of one factor matrix F (n x d)
+  float* FT;        // d x ldt
+  float* FT_lo;
+  float* F_lo;      // n x d
+  int n, ldt;
+};
+
+static size_t copies_bytes(int n, int d) {
+  const size_t ldt = rup(std::max(n, 1), 4);
+  return 2 * al256(size_t(d) * ldt * 4) + al256(size_t(std::max(n, 1)) * d * 4);
+}
+
+static char* carve_copies(char* w, int n, int d, TcCopies* c) {
+  c->n = n;
+  c->ldt = rup(std::max(n, 1), 4);
+  c->FT = reinterpret_cast<float*>(w);
+  w += al256(size_t(d) * c->ldt * 4);
+  c->FT_lo = reinterpret_cast<float*>(w);
+  w += al256(size_t(d) * c->ldt * 4);
+  c->F_lo = reinterpret_cast<float*>(w);
+  return w + al256(size_t(std::max(n, 1)) * d * 4);
+}
+
+static size_t tc_gemm_bytes(int n_users, int n_items, int d, int b) {
+  int su, spu, si, spi;
+  gram_plan(std::max(n_users, 1), d, &su, &spu);
+  gram_plan(std::max(n_items, 1), d, &si, &spi);
+  return copies_bytes(n_users, d) + copies_bytes(n_items, d) +
+         al256(size_t(std::max(su, si)) * d * b * 4) + 2 * al256(size_t(b) * d * 4) + 1024;
+}
+
+size_t ials_epoch_tc_bytes(int32_t n_users, int32_t n_items, int32_t d, int32_t b) {
+  return tc_gemm_bytes(n_users, n_items, d, b);
+}
+
+static int sync_copies(ials_session* s, const float* F, int ldf, int d, int c0, int cw,
+                       const TcCopies& c, cudaStream_t st) {
+  if (c.n <= 0 || cw <= 0) return IALS_OK;
+  dim3 g((c.n + 31) / 32, (cw + 31) / 32), t(32, 8);
+  k_sync_copies<<<g, t, 0, st>>>(F, c.n, ldf, c0, cw, c.FT, c.FT_lo, c.ldt, c.F_lo, d);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+static int gemm_attrs(ials_session* s) {
+  static bool init = false;
+  if (!init) {
+    CUDA_TRY(s, cudaFuncSetAttribute(k_gemm3_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     GemmLay::BYTES));
+    init = true;
+  }
+  return IALS_OK;
+}
+
+// slab = F^T F[:, b0:b0+bb] (d x bb) and slabT hi / lo (bb x d)
+static int gram_tc(ials_session* s, const TcCopies& F, int d, int b0, int bb, float* P, float* slab,
+                   float* slabT_hi, float* slabT_lo, cudaStream_t st) {
+  int rc = gemm_attrs(s);
+  if (rc) return rc;
+  const int bn = rup(bb, 16);
+  int S, span;
+  gram_plan(F.n, d, &S, &span);
+  CUtensorMap ah, al, bh, bl;
+  rc = make_map(s, &ah, F.FT, F.n, d, F.ldt, 128);
+  if (!rc) rc = make_map(s, &al, F.FT_lo, F.n, d, F.ldt, 128);
+  if (!rc) rc = make_map(s, &bh, F.FT, F.n, d, F.ldt, bn);
+  if (!rc) rc = make_map(s, &bl, F.FT_lo, F.n, d, F.ldt, bn);
+  if (rc) return rc;
+  GemmJob job{d, 0, b0, bb, bn, F.n, span, P, bb, (long long)d * bb, 1.f};
+  k_gemm3_tf32<<<dim3((d + 127) / 128, S), 128, GemmLay::BYTES, st>>>(ah, al, bh, bl, job);
+  LAUNCH_CHECK(s);
+  k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(P, S, (long long)d * bb, d, bb, slab,
+                                                      slabT_hi, slabT_lo);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+// proj = alpha0 * own @ slab (rows x bb)
+static int proj_tc(ials_session* s, const float* own, int ldo, const TcCopies& O, int d, int bb,
+                   const float* slabT_hi, const float* slabT_lo, float alpha0, float* proj,
+                   cudaStream_t st) {
+  if (O.n <= 0) return IALS_OK;
+  int rc = gemm_attrs(s);
+  if (rc) return rc;
+  const int bn = rup(bb, 16);
+  CUtensorMap ah, al, bh, bl;
+  rc = make_map(s, &ah, own, d, O.n, ldo, 128);
+  if (!rc) rc = make_map(s, &al, O.F_lo, d, O.n, d, 128);
+  if (!rc) rc = make_map(s, &bh, slabT_hi, d, bb, d, bn);
+  if (!rc) rc = make_map(s, &bl, slabT_lo, d, bb, d, bn);
+  if (rc) return rc;
+  GemmJob job{O.n, 0, 0, bb, bn, d, rup(d, kGemmKC), proj, bb, 0, alpha0};
+  k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), 128, GemmLay::BYTES, st>>>(ah, al, bh, bl, job);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+// optional phase events: 0 start, 1 after the cache, then per block
+// (user Gramian, user pass, item Gramian, item pass) -> 2 + 4 * blocks
+static cudaEvent_t g_ev[2 + 4 * 1024];
+static int g_nev = 0;
+
+int ials_epoch_events(void* const* events, int32_t n) {
+  if (n < 0 || n > 2 + 4 * 1024 || (n > 0 && !events)) return IALS_E_INVALID;
+  for (int i = 0; i < n; ++i) g_ev[i] = static_cast<cudaEvent_t>(events[i]);
+  g_nev = n;
+  return IALS_OK;
+}
+
+static void rec_event(int k, cudaStream_t st) {
+  if (k < g_nev && g_ev[k]) cudaEventRecord(g_ev[k], st);
+}
+
 // ------------------------------------------------------------------ epoch
 int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
@@ -712,22 +872,72 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
   float* slab = reinterpret_cast<float*>(ws);
   float* part = reinterpret_cast<float*>(ws + slab_bytes);
   char* pws = ws + slab_bytes + gbytes;
-  const size_t pbytes = ws_bytes - slab_bytes - gbytes;
+  size_t pbytes = ws_bytes - slab_bytes - gbytes;
+  // tensor-core GEMMs (with the fused tensor-core sweep, b in 65..128): the
+  // K-major copies live at the end of the workspace when it has room
+  const size_t tcb = tc_gemm_bytes(users->n_rows, items->n_rows, d, b);
+  const size_t pass_need = std::max(pass_ws(users->n_rows, b, user_sched->n_slices, user_sched->n_heavy),
+                                    pass_ws(items->n_rows, b, item_sched->n_slices, item_sched->n_heavy));
+  const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 64 && d % 4 == 0 &&
+                       ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= pass_need + tcb &&
+                       get_encode(s) == IALS_OK;
+  TcCopies cw{}, ch{};
+  float *P = nullptr, *sth = nullptr, *stl = nullptr;
+  if (tc_gemm) {
+    char* t = ws + ((ws_bytes - tcb) & ~size_t(1023));
+    pbytes = size_t(t - pws);
+    t = carve_copies(t, users->n_rows, d, &cw);
+    t = carve_copies(t, items->n_rows, d, &ch);
+    int su, spu, si, spi;
+    gram_plan(std::max(users->n_rows, 1), d, &su, &spu);
+    gram_plan(std::max(items->n_rows, 1), d, &si, &spi);
+    P = reinterpret_cast<float*>(t);
+    t += al256(size_t(std::max(su, si)) * d * b * 4);
+    sth = reinterpret_cast<float*>(t);
+    t += al256(size_t(b) * d * 4);
+    stl = reinterpret_cast<float*>(t);
+    int rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
+    if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+    if (rc) return rc;
+  }
+  rec_event(0, st);
   int rc = ials_predictions(s, users->n_rows, users->ptr, users->cols, W, ldw, H, ldh, d, cache,
                             stream);
   if (rc) return rc;
+  rec_event(1, st);
+  int ek = 2;
   for (int b0 = 0; b0 < d; b0 += b) {
     const int bb = std::min(b, d - b0);
-    rc = gramian_impl(s, H, items->n_rows, ldh, d, b0, bb, slab, part, gbytes, st);
+    if (tc_gemm) {
+      rc = gram_tc(s, ch, d, b0, bb, P, slab, sth, stl, st);
+      if (!rc) rc = proj_tc(s, W, ldw, cw, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
+    } else {
+      rc = gramian_impl(s, H, items->n_rows, ldh, d, b0, bb, slab, part, gbytes, st);
+    }
     if (rc) return rc;
+    rec_event(ek++, st);
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
-                        pws, pbytes, st);
+                        pws, pbytes, st, tc_gemm);
     if (rc) return rc;
-    rc = gramian_impl(s, W, users->n_rows, ldw, d, b0, bb, slab, part, gbytes, st);
+    rec_event(ek++, st);
+    if (tc_gemm) {
+      rc = sync_copies(s, W, ldw, d, b0, bb, cw, st);
+      if (!rc) rc = gram_tc(s, cw, d, b0, bb, P, slab, sth, stl, st);
+      if (!rc) rc = proj_tc(s, H, ldh, ch, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
+    } else {
+      rc = gramian_impl(s, W, users->n_rows, ldw, d, b0, bb, slab, part, gbytes, st);
+    }
     if (rc) return rc;
+    rec_event(ek++, st);
     rc = side_pass_impl(s, items, item_sched, W, ldw, H, ldh, d, b0, bb, slab, alpha0, cache, 1,
-                        pws, pbytes, st);
+                        pws, pbytes, st, tc_gemm);
     if (rc) return rc;
+    if (tc_gemm) {
+      rc = sync_copies(s, H, ldh, d, b0, bb, ch, st);
+      if (rc) return rc;
+    }
+    rec_event(ek++, st);
   }
   return IALS_OK;
 }

@@ -1,0 +1,200 @@
+// ials_gemm_tc.cuh -- the two dense GEMMs of an iALS++ block step on the
+// tensor core (tcgen05, 3xTF32, TMA-fed), used by ials_epoch:
+//
+//   Gramian slab  G[:, pi] = F^T F[:, pi]          (d x b, K = rows of F)
+//   projection    proj     = alpha0 * own G[:, pi] (rows x b, K = d)
+//
+// Both operands must be K-major for kind::tf32, so the epoch keeps, per
+// factor matrix F (n x d): F^T (d x n) and the tf32 low parts F^T_lo, F_lo
+// (x - trunc_tf32(x)); k_sync_copies refreshes them for the column block a
+// side pass just changed (solvers.py:340-375 updates one block at a time).
+// D = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T accumulates in TMEM.
+//
+// One CTA = 128 threads: warp 0 / lane 0 issues TMA loads into a 3-stage
+// ring (full / empty mbarriers), warp 1 / lane 0 issues the MMAs, then all
+// four warps drain the 128 x N accumulator (thread i <-> TMEM lane i).
+#pragma once
+#include <cuda.h>
+#include "ials_common.cuh"
+#include "ials_umma.cuh"
+
+namespace ials {
+
+IALS_DEVI void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c_inner, int c_row,
+                           uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c_inner), "r"(c_row), "r"(smem_u32(bar))
+      : "memory");
+}
+IALS_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+IALS_DEVI void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+struct GemmJob {
+  int m_rows;              // valid output rows (rows of A)
+  int a_row0;              // first A row of tile 0 (row coordinate in the A maps)
+  int b_row0;              // first B row
+  int n;                   // valid output columns; the MMA runs N = bn = round_up(n, 16)
+  int bn;
+  int k_total;             // K extent
+  int k_span;              // K per split (multiple of 32)
+  float* out;              // out[split][row][col]
+  int ldo;
+  long long split_stride;  // floats between splits
+  float scale;
+};
+
+constexpr int kGemmStages = 3;
+constexpr int kGemmKC = 32;  // K per stage: one 128-byte swizzle row
+
+struct GemmLay {
+  static constexpr int A_BYTES = 128 * 128;  // 128 rows x 128 B
+  static constexpr int B_BYTES = 128 * 128;  // up to 128 rows
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int OFF_BAR = kGemmStages * STAGE;
+  static constexpr int BYTES = OFF_BAR + 8 * (2 * kGemmStages + 1) + 16 + 1024;
+};
+
+__global__ void __launch_bounds__(128, 1)
+    k_gemm3_tf32(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap a_lo,
+                 const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo,
+                 GemmJob job) {
+  extern __shared__ __align__(1024) char smem_g[];
+  char* smem = smem_g + ((1024u - (smem_u32(smem_g) & 1023u)) & 1023u);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GemmLay::OFF_BAR);
+  uint64_t* empty = full + kGemmStages;
+  uint64_t* done = empty + kGemmStages;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(done + 1);
+  const int m0 = blockIdx.x * 128;
+  const int kb = blockIdx.y * job.k_span;
+  const int ke = min(kb + job.k_span, job.k_total);
+  const int nk = (ke - kb + kGemmKC - 1) / kGemmKC;
+  if (tid == 0) {
+    prefetch_tmap(&a_hi);
+    prefetch_tmap(&a_lo);
+    prefetch_tmap(&b_hi);
+    prefetch_tmap(&b_lo);
+    for (int s = 0; s < kGemmStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(done, 1);
+  }
+  if (warp == 2) tmem_alloc(tptr, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tptr;
+  const uint32_t stage_bytes = 2 * GemmLay::A_BYTES + 2 * job.bn * 128;
+  if (warp == 0 && (tid & 31) == 0) {  // TMA producer
+    for (int c = 0; c < nk; ++c) {
+      const int s = c % kGemmStages;
+      if (c >= kGemmStages) mbar_wait(empty + s, ((c / kGemmStages) - 1) & 1);
+      char* st = smem + s * GemmLay::STAGE;
+      mbar_expect_tx(full + s, stage_bytes);
+      const int kc = kb + c * kGemmKC;
+      tma_load_2d(smem_u32(st), &a_hi, kc, job.a_row0 + m0, full + s);
+      tma_load_2d(smem_u32(st + GemmLay::A_BYTES), &a_lo, kc, job.a_row0 + m0, full + s);
+      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, kc, job.b_row0, full + s);
+      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, kc, job.b_row0,
+                  full + s);
+    }
+  } else if (warp == 1 && (tid & 31) == 0) {  // MMA issuer
+    const uint32_t idesc = make_idesc_tf32(128, job.bn, 0, 0, 0);
+    for (int c = 0; c < nk; ++c) {
+      const int s = c % kGemmStages;
+      mbar_wait(full + s, (c / kGemmStages) & 1);
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + s * GemmLay::STAGE);
+      const uint32_t ah = base, al = base + GemmLay::A_BYTES;
+      const uint32_t bh = base + 2 * GemmLay::A_BYTES, bl = bh + GemmLay::B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < kGemmKC / 8; ++ks) {
+        const uint64_t dah = make_sdesc(ah + ks * 32, 16, 1024, kSwizzle128B);
+        const uint64_t dal = make_sdesc(al + ks * 32, 16, 1024, kSwizzle128B);
+        const uint64_t dbh = make_sdesc(bh + ks * 32, 16, 1024, kSwizzle128B);
+        const uint64_t dbl = make_sdesc(bl + ks * 32, 16, 1024, kSwizzle128B);
+        umma_tf32(tmem, dah, dbh, idesc, (c | ks) > 0);
+        umma_tf32(tmem, dah, dbl, idesc, 1);
+        umma_tf32(tmem, dal, dbh, idesc, 1);
+      }
+      umma_commit(empty + s);   // frees the stage once these MMAs have read it
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+  // epilogue: thread i drains TMEM lane i = output row m0 + i
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int row = m0 + tid;
+  float* o = job.out + (long long)blockIdx.y * job.split_stride + (long long)row * job.ldo;
+  const uint32_t raddr = tmem + ((uint32_t)(warp * 32) << 16);
+  for (int c32 = 0; c32 < job.bn; c32 += 32) {   // warp-uniform
+    float v[32];
+    tmem_ld32(raddr + c32, v);
+    tmem_wait_ld();
+    if (row < job.m_rows && nk > 0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c32 + j < job.n) o[c32 + j] = job.scale * v[j];
+    } else if (row < job.m_rows) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c32 + j < job.n) o[c32 + j] = 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_free(tmem, 128);
+}
+
+// slab[k][j] = sum_s P[s][k][j] (fixed split order), and its transpose
+// split into tf32 hi / lo for the projection's B operand.
+__global__ void k_gram_reduce(const float* __restrict__ P, int splits, long long split_stride, int d,
+                              int b, float* slab, float* slabT_hi, float* slabT_lo) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= d * b) return;
+  const int k = idx / b, j = idx - k * b;
+  float s = 0.f;
+  for (int t = 0; t < splits; ++t) s += P[(long long)t * split_stride + idx];
+  slab[idx] = s;
+  slabT_hi[(size_t)j * d + k] = s;
+  slabT_lo[(size_t)j * d + k] = tf32_lo(s);
+}
+
+// Refresh the K-major copies of F for columns [c0, c0 + cw): F^T, F^T_lo
+// (d x ldt) and F_lo (n x ldl).  32 x 32 tiles through shared memory.
+__global__ void k_sync_copies(const float* __restrict__ F, int n, int ldf, int c0, int cw,
+                              float* FT, float* FT_lo, int ldt, float* F_lo, int ldl) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.x * 32, cb = c0 + blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int r = r0 + i, c = cb + tx;
+    float x = 0.f;
+    if (r < n && c < c0 + cw) {
+      x = F[(size_t)r * ldf + c];
+      F_lo[(size_t)r * ldl + c] = tf32_lo(x);
+    }
+    tile[i][tx] = x;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int c = cb + i, r = r0 + tx;
+    if (r < n && c < c0 + cw) {
+      const float x = tile[tx][i];
+      FT[(size_t)c * ldt + r] = x;
+      FT_lo[(size_t)c * ldt + r] = tf32_lo(x);
+    }
+  }
+}
+
+}  // namespace ials

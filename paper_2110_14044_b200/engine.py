@@ -16,6 +16,7 @@ Layout in HBM (fp32 factors, int32 indices):
 from __future__ import annotations
 
 import ctypes
+from ctypes import c_void_p
 from dataclasses import dataclass
 
 import numpy as np
@@ -294,6 +295,9 @@ class Engine:
         need += int(self.lib.ials_tc_workspace_bytes(max(sch_u.tc_max_wave_rows, sch_i.tc_max_wave_rows),
                                                       max(sch_u.tc_max_wave_slices,
                                                           sch_i.tc_max_wave_slices)))
+        # room for the epoch's tensor-core GEMM path (K-major factor copies)
+        need += int(self.lib.ials_epoch_tc_bytes(max(self.p.num_users, 1),
+                                                 max(self.p.num_items, 1), d, b))
         need = max(need, int(self.lib.ials_loss_workspace_bytes(d)))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
@@ -329,16 +333,28 @@ class Engine:
                                      self.stream())
         self.sess.check(rc, f"{side} side pass")
 
-    def epoch(self, W, H, cache, b, alpha0):
-        """One uniform-block iALS++ epoch entirely on the device."""
+    def epoch(self, W, H, cache, b, alpha0, events=None):
+        """One uniform-block iALS++ epoch entirely on the device.  `events`
+        (torch.cuda.Event list, 2 + 4 * blocks) are recorded at the phase
+        boundaries (see ials_epoch_events)."""
         d = W.shape[1]
         ws = self.workspace(d, b)
         su, si = self.p.users.schedule(b), self.p.items.schedule(b)
-        rc = self.lib.ials_epoch(self.sess.handle, ctypes.byref(self.p.users.struct),
-                                 ctypes.byref(su.struct), ctypes.byref(self.p.items.struct),
-                                 ctypes.byref(si.struct), _ptr(W), W.stride(0), _ptr(H),
-                                 H.stride(0), d, b, float(alpha0), _ptr(cache), _ptr(ws),
-                                 ws.numel(), self.stream())
+        if events:
+            for e in events:
+                if not e.cuda_event:   # created lazily by torch on first record
+                    e.record(torch.cuda.current_stream(self.device))
+            arr = (c_void_p * len(events))(*[c_void_p(e.cuda_event) for e in events])
+            self.sess.check(self.lib.ials_epoch_events(arr, len(events)), "epoch events")
+        try:
+            rc = self.lib.ials_epoch(self.sess.handle, ctypes.byref(self.p.users.struct),
+                                     ctypes.byref(su.struct), ctypes.byref(self.p.items.struct),
+                                     ctypes.byref(si.struct), _ptr(W), W.stride(0), _ptr(H),
+                                     H.stride(0), d, b, float(alpha0), _ptr(cache), _ptr(ws),
+                                     ws.numel(), self.stream())
+        finally:
+            if events:
+                self.lib.ials_epoch_events(None, 0)
         self.sess.check(rc, "epoch")
 
     def epoch_graph(self, W, H, cache, b, alpha0):

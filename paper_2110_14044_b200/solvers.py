@@ -148,6 +148,22 @@ class DeviceTrainer:
         ev = lambda: torch.cuda.Event(enable_timing=True)
         marks = [ev()]
         marks[0].record()
+        if self.uniform:
+            # one ials_epoch call (tensor-core GEMMs when b in 65..128), with
+            # the phase events recorded inside it
+            nb = len(self.spans)
+            evs = [ev() for _ in range(2 + 4 * nb)]
+            e.epoch(self.W, self.H, self.cache, self.spans[0][1], a0, events=evs)
+            names = ["cache"] + [n for _ in range(nb) for n in ("gramian", "user", "gramian", "item")]
+            phases = list(zip(names, evs[1:]))
+            prev = evs[0]
+            torch.cuda.synchronize(self.rt.device)
+            for name, m in phases:
+                secs = prev.elapsed_time(m) / 1e3
+                setattr(rep, f"{name}_seconds", getattr(rep, f"{name}_seconds") + secs)
+                prev = m
+            self._check()
+            return rep
         e.predictions(self.W, self.H, self.cache)
         phases = [("cache", ev())]
         phases[-1][1].record()
