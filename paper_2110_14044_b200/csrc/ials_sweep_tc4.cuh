@@ -50,7 +50,7 @@ struct TcLay4 {
   static constexpr int OFF_ID = OFF_YF + BT * 4;
   static constexpr int OFF_D = OFF_ID + BT * 4;
   static constexpr int OFF_PA_HI = OFF_X;          // factor: panel operands hi / lo (2 x 4 KB)
-  static constexpr int OFF_LI = OFF_X + 8192;      // backward: 16 x 8x8 block inverses
+  static constexpr int OFF_LI = OFF_X + 8192;      // backward: 8 x 16x16 block inverses
   static constexpr int OFF_DIAG = OFF_D + BT * 4;  // H_kk before the factorisation
   static constexpr int OFF_FLAG = OFF_DIAG + BT * 4;
   static constexpr int OFF_BAR = OFF_FLAG + 16;    // 2 mbarriers + TMEM base
@@ -305,17 +305,12 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
 #pragma unroll
       for (int q = 0; q < 8; ++q) py[q] = __shfl_sync(full, yi, base + q);
       float rinv[8];
-      bool redo = false;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        float dk = a[k][k];
-        // a pivot that lost more than cond_max of its diagonal to
-        // cancellation (or is not positive) is beyond what the 3xTF32
-        // Hessian resolves: the row goes to the FP32 SIMT sweep
-        if (!(dk > 0.f && dk < 3.0e38f)) {
-          redo = true;   // non-positive pivot (the cancellation test is done off the chain)
-          dk = 1.f;
-        }
+        // a non-positive / non-finite pivot yields a NaN, infinite or zero
+        // 1/pivot, which the cancellation test (record_block) flags; the
+        // row's own numbers are then discarded and it is redone in FP32
+        const float dk = a[k][k];
         const float r = rsqrtf(dk);
         rinv[k] = r;
         a[k][k] = dk * r;
@@ -348,7 +343,6 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         reinterpret_cast<float4*>(YP)[0] = make_float4(yp[0], yp[1], yp[2], yp[3]);
         reinterpret_cast<float4*>(YP)[1] = make_float4(yp[4], yp[5], yp[6], yp[7]);
       }
-      if (redo && lane == base) *FLAG = 1;
     }
     __syncthreads();
     if (watch && pp == 8) acc[1] = clock64();
@@ -368,7 +362,7 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         const float r = RV[j];
         invd[i] = r;
         yf[i] = YP[j];
-        if (i < b && !(DIAG[i] * (r * r) <= p.cond_max)) *FLAG = 1;
+        if (i < b && !(r > 0.f && DIAG[i] * (r * r) <= p.cond_max)) *FLAG = 1;
       }
     };
     float l[8];
@@ -438,33 +432,35 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
   }
 }
 
-// Inverses of the 8x8 diagonal blocks of L (from the packed copy), all at
-// once: thread t forms column q = t % 8 of block t / 8 by forward
-// substitution with the stored reciprocal pivots.  LI[blk][m][q].
+// Inverses of the 16x16 diagonal blocks of L (from the packed copy), all at
+// once: thread t forms column q = t % 16 of block t / 16 by forward
+// substitution with the stored reciprocal pivots.  LI[blk][m][q] (16 x 16,
+// lower triangular).
 IALS_DEVI void tc4_block_inverses(const SweepParams& p, char* smem, int tid) {
   using L = TcLay4;
   const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L);
   const float* invd = reinterpret_cast<const float*>(smem + L::OFF_ID);
   float* LI = reinterpret_cast<float*>(smem + L::OFF_LI);
-  const int np = (p.b + 7) >> 3, blk = tid >> 3, q = tid & 7, c0 = 8 * blk;
-  if (blk >= np) return;
-  float x[8];
+  const int nb = (p.b + 15) >> 4, blk = tid >> 4, q = tid & 15, c0 = 16 * blk;
+  if (blk >= nb) return;
+  float x[16];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
+  for (int m = 0; m < 16; ++m) {
     const int gm = c0 + m;
     float t = (m == q) ? 1.f : 0.f;
+    const float* lr = Lp + gm * (gm + 1) / 2 + c0;
 #pragma unroll
     for (int k = 0; k < m; ++k)
-      if (gm < p.b) t = fmaf(-Lp[gm * (gm + 1) / 2 + c0 + k], x[k], t);
+      if (k >= q && gm < p.b) t = fmaf(-lr[k], x[k], t);
     x[m] = (m >= q && gm < p.b) ? t * invd[gm] : 0.f;
   }
 #pragma unroll
-  for (int m = 0; m < 8; ++m) LI[blk * 64 + m * 8 + q] = x[m];
+  for (int m = 0; m < 16; ++m) LI[blk * 256 + m * 16 + q] = x[m];
 }
 
-// Backward solve L^T d = y from the last panel: d_panel = L11^-T y_panel (a
-// mat-vec with the precomputed inverse), then every row r < c0 folds the
-// panel into its own y_r; one barrier per panel.
+// Backward solve L^T d = y by 16-wide blocks from the last: 16 threads form
+// the block's unknowns d = L11^-T y_blk (dot products with the precomputed
+// inverse), then every row r < c0 folds them into its own y_r.
 IALS_DEVI void tc4_backward(const SweepParams& p, char* smem, int tid) {
   using L = TcLay4;
   const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L);
@@ -472,36 +468,36 @@ IALS_DEVI void tc4_backward(const SweepParams& p, char* smem, int tid) {
   float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
   float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
   const int b = p.b;
-  const int np = (b + 7) >> 3;
+  const int nb = (b + 15) >> 4;
   float yr = (tid < b) ? yf[tid] : 0.f;
-  for (int pp = np - 1; pp >= 0; --pp) {
-    const int c0 = pp * 8;
-    float yp[8];
+  for (int pb = nb - 1; pb >= 0; --pb) {
+    const int c0 = pb * 16;
+    if (tid < 16) {   // d_q = sum_{m >= q} LI[m][q] y_m
+      const int q = tid;
+      const float* li = LI + pb * 256 + q;
+      float t0 = 0.f, t1 = 0.f;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) yp[m] = (c0 + m < b) ? yf[c0 + m] : 0.f;
-    const float* li = LI + pp * 64;
-    float dlt[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {   // (L11^-T y)_q = sum_{m >= q} LI[m][q] y_m
-      float t = 0.f;
-#pragma unroll
-      for (int m = q; m < 8; ++m) t = fmaf(li[m * 8 + q], yp[m], t);
-      dlt[q] = (c0 + q < b) ? t : 0.f;
-    }
-    if (tid >= c0 && tid < c0 + 8 && tid < b) {
-      const int e = tid - c0;
-      const float a0 = (e & 1) ? dlt[1] : dlt[0], a1 = (e & 1) ? dlt[3] : dlt[2];
-      const float a2 = (e & 1) ? dlt[5] : dlt[4], a3 = (e & 1) ? dlt[7] : dlt[6];
-      const float b0 = (e & 2) ? a1 : a0, b1 = (e & 2) ? a3 : a2;
-      ds[tid] = (e & 4) ? b1 : b0;
-    }
-    if (tid < c0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int gq = c0 + q;
-        if (gq < b) yr = fmaf(-Lp[gq * (gq + 1) / 2 + tid], dlt[q], yr);
+      for (int m = 0; m < 16; m += 2) {
+        if (m >= q && c0 + m < b) t0 = fmaf(li[m * 16], yf[c0 + m], t0);
+        if (m + 1 >= q && c0 + m + 1 < b) t1 = fmaf(li[(m + 1) * 16], yf[c0 + m + 1], t1);
       }
-      if (tid >= c0 - 8) yf[tid] = yr;   // the next panel's entries
+      if (c0 + q < b) ds[c0 + q] = t0 + t1;
+    }
+    __syncthreads();
+    if (tid < c0) {
+      const float4* dq = reinterpret_cast<const float4*>(ds + c0);
+      float a0 = yr, a1 = 0.f;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const float4 dv = dq[q4];
+        const int g = c0 + 4 * q4;   // rows >= b of the packed L were never written
+        if (g < b) a0 = fmaf(-Lp[g * (g + 1) / 2 + tid], dv.x, a0);
+        if (g + 1 < b) a1 = fmaf(-Lp[(g + 1) * (g + 2) / 2 + tid], dv.y, a1);
+        if (g + 2 < b) a0 = fmaf(-Lp[(g + 2) * (g + 3) / 2 + tid], dv.z, a0);
+        if (g + 3 < b) a1 = fmaf(-Lp[(g + 3) * (g + 4) / 2 + tid], dv.w, a1);
+      }
+      yr = a0 + a1;
+      if (tid >= c0 - 16) yf[tid] = yr;   // the next block's entries
     }
     __syncthreads();
   }
