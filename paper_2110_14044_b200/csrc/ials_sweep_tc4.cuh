@@ -72,7 +72,9 @@ struct Tc4State {
 };
 
 // step 1: TMEM row i := template row i (+ lam on the diagonal), zero above
-IALS_DEVI void tc4_init(const SweepParams& p, uint32_t row_addr, float lam, int tid) {
+// (lam I is added where the diagonal is consumed: the factorisation's
+// diagonal block and the cancellation reference)
+IALS_DEVI void tc4_init(const SweepParams& p, uint32_t row_addr, int tid) {
   const int i = tid;
   const float* tp = p.tpl + pk_off(i);
 #pragma unroll 1
@@ -84,11 +86,8 @@ IALS_DEVI void tc4_init(const SweepParams& p, uint32_t row_addr, float lam, int 
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int c8 = 0; c8 < 8; ++c8) {
-      float w8[8] = {x[2 * c8].x, x[2 * c8].y, x[2 * c8].z, x[2 * c8].w,
-                     x[2 * c8 + 1].x, x[2 * c8 + 1].y, x[2 * c8 + 1].z, x[2 * c8 + 1].w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (64 * q + 8 * c8 + j == i && i < p.b) w8[j] += lam;
+      const float w8[8] = {x[2 * c8].x, x[2 * c8].y, x[2 * c8].z, x[2 * c8].w,
+                           x[2 * c8 + 1].x, x[2 * c8 + 1].y, x[2 * c8 + 1].z, x[2 * c8 + 1].w};
       tmem_st8(row_addr + 64 * q + 8 * c8, w8);
     }
   }
@@ -392,12 +391,17 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
     if (pp + 1 < np) {
       float* PAH = reinterpret_cast<float*>(smem + L::OFF_PA_HI);
       float* PAL = PAH + 1024;   // 4 KB apart
+      float hi[8], lo[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float hi = tf32_rna(l[q]);
-        PAH[pa_index(i, q)] = hi;
-        PAL[pa_index(i, q)] = tf32_rna(l[q] - hi);
+        hi[q] = tf32_rna(l[q]);
+        lo[q] = tf32_rna(l[q] - hi[q]);
       }
+      const int pa = pa_index(i, 0);   // q 0..3 contiguous, q 4..7 at +32
+      *reinterpret_cast<float4*>(PAH + pa) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(PAH + pa + 32) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+      *reinterpret_cast<float4*>(PAL + pa) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<float4*>(PAL + pa + 32) = make_float4(lo[4], lo[5], lo[6], lo[7]);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -540,28 +544,36 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
     const int row = p.light_rows[task];
     const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
     const float lam = p.side.lam[row];
-    tc4_init(p, row_addr, lam, tid);
+    tc4_init(p, row_addr, tid);
     if (rec) tph[1] = clock64();
     tmem_wait_st();
     tc_fence_before();   // the first chunk's barrier orders these stores before the MMAs
     double gacc = 0.0;
     const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid);
     if (rec) tph[2] = clock64();
-    {  // the diagonal before factorisation (for the cancellation check):
-       // lane l of warp w picks column 32w + l with a select tree (an indexed
-       // register read would go through local memory)
+    {  // + lam on the diagonal, and the diagonal itself (the cancellation
+       // test's reference): lane l of warp w owns column 32w + l, reached with
+       // 8-wide TMEM loads / stores of the warp's diagonal block and selects
+       // (an indexed register read would go through local memory)
       const int lane = tid & 31, e = lane & 7;
+      const float lv = (tid < b) ? lam : 0.f;
       float dg = 0.f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float v[8];
-        tmem_ld8(row_addr + 32 * (tid >> 5) + 8 * j, v);
+        const uint32_t ca = row_addr + 32 * (tid >> 5) + 8 * j;
+        tmem_ld8(ca, v);
         tmem_wait_ld();
+        const bool mine = (lane >> 3) == j;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] += (mine && m == e) ? lv : 0.f;
+        tmem_st8(ca, v);
         const float a0 = (e & 1) ? v[1] : v[0], a1 = (e & 1) ? v[3] : v[2];
         const float a2 = (e & 1) ? v[5] : v[4], a3 = (e & 1) ? v[7] : v[6];
         const float b0 = (e & 2) ? a1 : a0, b1 = (e & 2) ? a3 : a2;
-        if ((lane >> 3) == j) dg = (e & 4) ? b1 : b0;
+        if (mine) dg = (e & 4) ? b1 : b0;
       }
+      tmem_wait_st();
       reinterpret_cast<float*>(smem + L::OFF_DIAG)[tid] = dg;
       if (tid == 0) *reinterpret_cast<int*>(smem + L::OFF_FLAG) = 0;
     }
