@@ -128,11 +128,13 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, int ebeg, int eend, 
   const int* mc = reinterpret_cast<const int*>(smem + L::OFF_MC) + (c & (L::MR - 1)) * L::KC;
   const int* mp = reinterpret_cast<const int*>(smem + L::OFF_MP) + (c & (L::MR - 1)) * L::KC;
   float* X = reinterpret_cast<float*>(smem + L::OFF_X) + (c & 1) * L::KC * L::XLD;
-  if (p.vec) {
-    const int bv = p.b >> 2;
-    for (int i = tid; i < nk * bv; i += L::NT) {
-      const int k = i / bv, v = i - k * bv;
-      cp_async16(X + k * L::XLD + 4 * v, p.fixed + (size_t)mc[k] * p.ldf + p.b0 + 4 * v);
+  if (p.vec) {   // lane <-> 16-byte piece of a sub-row (b <= 128: 32 pieces), warp <-> entry
+    const int lane = tid & 31, warp = tid >> 5;
+    if (lane < (p.b >> 2)) {
+      const float* src = p.fixed + p.b0 + 4 * lane;
+#pragma unroll
+      for (int k = warp; k < L::KC; k += L::NT / 32)
+        if (k < nk) cp_async16(X + k * L::XLD + 4 * lane, src + (size_t)mc[k] * p.ldf);
     }
   } else {
     for (int i = tid; i < nk * p.b; i += L::NT) {
@@ -145,7 +147,10 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, int ebeg, int eend, 
 }
 
 IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, double& gacc, int ebeg,
-                             int eend, int tid) {
+                             int eend, int tid, bool prof = false) {
+  // profiling: timestamps of chunk 3 (thread 0 and thread 64)
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool watch = prof && (tid == 0 || tid == 64);
   using L = TcLay4;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   const int n = eend - ebeg;
@@ -166,8 +171,11 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
   for (int c = 0; c < nch; ++c) {
     const int xb = c & 1;
     const int nk = min(L::KC, eend - (ebeg + c * L::KC));
+    if (watch && c == 3) tp[0] = clock64();
     cp_async_wait<1>();
+    if (watch && c == 3) tp[1] = clock64();
     __syncthreads();
+    if (watch && c == 3) tp[2] = clock64();
     const float* X = reinterpret_cast<const float*>(smem + L::OFF_X) + xb * L::KC * L::XLD;
     const int ms = (c & (L::MR - 1)) * L::KC;
     const float* mw = reinterpret_cast<const float*>(smem + L::OFF_MW) + ms;
@@ -179,22 +187,32 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
     const bool colok = tid < p.b;   // columns >= b are not gathered
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = (colok && k < nk) ? X[k * L::XLD + tid] : 0.f;
-    {  // gradient: two fixed-order fp64 chains (even / odd entries)
-      double g0 = 0.0, g1 = 0.0;
+    float wk[16];   // the chunk's weights: 16-byte broadcast reads of the rings
+    {  // gradient: four fixed-order fp64 chains (entries k mod 4)
+      double g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int k = 0; k < 16; k += 2) {
-        const float r0 = (k < nk) ? mw[k] * (cv[k] - my[k]) : 0.f;
-        const float r1 = (k + 1 < nk) ? mw[k + 1] * (cv[k + 1] - my[k + 1]) : 0.f;
-        g0 = fma((double)r0, (double)x[k], g0);
-        g1 = fma((double)r1, (double)x[k + 1], g1);
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const float4 w4 = reinterpret_cast<const float4*>(mw)[k4];
+        const float4 c4 = reinterpret_cast<const float4*>(cv)[k4];
+        const float4 y4 = reinterpret_cast<const float4*>(my)[k4];
+        const float w[4] = {w4.x, w4.y, w4.z, w4.w}, cc[4] = {c4.x, c4.y, c4.z, c4.w},
+                    yy[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 4 * k4 + j;
+          wk[k] = w[j];
+          const float r = (k < nk) ? w[j] * (cc[j] - yy[j]) : 0.f;
+          g[j] = fma((double)r, (double)x[k], g[j]);
+        }
       }
-      gacc += g0 + g1;
+      gacc += (g[0] + g[1]) + (g[2] + g[3]);
     }
     if (p.side.weights) {  // a h h^T = (sqrt(a) h)(sqrt(a) h)^T
 #pragma unroll
-      for (int k = 0; k < 16; ++k) x[k] *= (k < nk) ? sqrtf(mw[k]) : 0.f;
+      for (int k = 0; k < 16; ++k) x[k] *= (k < nk) ? sqrtf(wk[k]) : 0.f;
     }
     // the operand buffer xb was last read by chunk c-2's MMAs
+    if (watch && c == 3) tp[3] = clock64();
     if (pend & (1u << xb)) {
       mbar_wait(bar + xb, (st.ph >> xb) & 1u);
       st.ph ^= 1u << xb;
@@ -218,6 +236,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
         *reinterpret_cast<float4*>(XTL + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
       }
     }
+    if (watch && c == 3) tp[4] = clock64();
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -234,12 +253,14 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       }
       umma_commit(bar + xb);
     }
+    if (watch && c == 3) tp[5] = clock64();
     pend |= 1u << xb;
     // group c: X / yhat of chunk c+2 (its buffers were consumed above), and
     // the metadata of chunk c+4
     if (c + 2 < nch) tc4_gather(p, smem, ebeg, eend, c + 2, tid);
     if (c + 4 < nch) tc4_meta(p, smem, ebeg, eend, c + 4, tid);
     cp_async_commit();
+    if (watch && c == 3) tp[6] = clock64();
   }
   cp_async_wait<0>();
 #pragma unroll
@@ -249,6 +270,10 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       st.ph ^= 1u << xb;
     }
   tc_fence_after();
+  if (watch && nch > 3) {
+    const int w = tid == 0 ? 0 : 1;
+    for (int k = 0; k < 8; ++k) p.dbg[16384 + (blockIdx.x * 2 + w) * 8 + k] = tp[k];
+  }
   return nch;
 }
 
@@ -549,7 +574,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
     tmem_wait_st();
     tc_fence_before();   // the first chunk's barrier orders these stores before the MMAs
     double gacc = 0.0;
-    const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid);
+    const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid, ndone == rec_row);
     if (rec) tph[2] = clock64();
     {  // + lam on the diagonal, and the diagonal itself (the cancellation
        // test's reference): lane l of warp w owns column 32w + l, reached with

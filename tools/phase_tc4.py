@@ -41,6 +41,16 @@ for side, fixed, own, tgt in [(sd, f, o, t) for (sd, f, o) in (("user", H, W), (
     for name, col in zip(["init", "accumulate", "diag+grad", "factor", "copy+backward", "update+cache"], dif.T):
         print(f"  {name:14s} median {np.median(col):9.0f}  p90 {np.percentile(col, 90):9.0f} cycles")
     print(f"  accumulate cycles/entry median {np.median(dif[:, 1] / np.maximum(n, 1)):.1f}")
+    a = dbg[16384:16384 + 592 * 16].view(-1, 2, 8).cpu().numpy().astype(np.float64)
+    a = a[a[:, 0, 0] > 0]
+    if len(a):
+        # 0 before cp.async wait, 1 after wait, 2 after barrier, 3 after gradient,
+        # 4 after MMA(c-2) wait + operand writes, 5 after barrier + MMA issue, 6 after next gathers
+        base = a[:, 0, 0:1]
+        print("  accumulate chunk 3 timeline (cycles after thread 0 reached the cp.async wait):")
+        for w, wn in enumerate(["thread 0 (MMA issuer)", "thread 64"]):
+            t = np.median(a[:, w, :7] - base, axis=0)
+            print(f"    {wn:24s} " + "  ".join(f"{int(x):6d}" for x in t))
     f = dbg[8192:8192 + 592 * 24].view(-1, 3, 8).cpu().numpy().astype(np.float64)
     f = f[f[:, 0, 6] > 0]
     if len(f):
