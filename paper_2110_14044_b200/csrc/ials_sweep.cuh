@@ -405,8 +405,8 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
         for (int m = 0; m <= q; ++m) a[q][m] = PB[m * L::PLD + c0 + q];
       float rinv[PW];
       int bad = -1;
-#pragma unroll
       bool cancel = false;
+#pragma unroll
       for (int k = 0; k < PW; ++k) {
         float dk = a[k][k];
         if (GUARD && c0 + k < b && !(dk > 0.f && dk < 3.0e38f && sm[L::OFF_X + c0 + k] <= p.cond_max * dk))
