@@ -156,9 +156,12 @@ int64_t ials_slice_len(int32_t b) {
   return bt <= 16 ? 256 : bt == 32 ? 512 : (bt == 256 ? 1024 : 2048);
 }
 
+static constexpr int kGemvSplits = 4 * 148;   // b <= 4: one GEMV split per 64+ rows
+
 static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
   (void)n;
-  return al256(size_t(kMaxSplits) * d * b * sizeof(float));
+  const size_t narrow = b <= 4 ? size_t(kGemvSplits) * d * b : 0;
+  return al256(std::max(size_t(kMaxSplits) * d * b, narrow) * sizeof(float));
 }
 
 size_t ials_tc_workspace_bytes(int32_t max_wave_rows, int32_t max_wave_slices) {
@@ -169,12 +172,18 @@ size_t ials_tc_workspace_bytes(int32_t max_wave_rows, int32_t max_wave_slices) {
 // 1024 partial Hessians (35 MB) stay L2-resident between k_tc_hess and k_tc_factor
 int32_t ials_tc_wave_slices(void) { return 1024; }
 
-static size_t pass_ws(int32_t n_rows, int32_t b, int32_t n_slices, int32_t n_heavy) {
+// narrow blocks gather from a compact copy of the fixed side's column block
+// (n_fixed x ldc): L2-resident, unlike the full d-wide rows
+static constexpr int kCompactMaxB = 32;
+static inline int compact_ld(int b) { return (b + 3) & ~3; }
+
+static size_t pass_ws(int32_t n_rows, int32_t n_fixed, int32_t b, int32_t n_slices, int32_t n_heavy) {
   const size_t bt = block_tile(b);
   return al256(size_t(n_rows) * b * 4) + al256(size_t(n_slices) * bt * bt * 4) +
          al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4) +
          al256(size_t(kTcPKS) * 4) + al256(size_t(n_rows) * 4 + 16) +
-         al256(size_t(n_rows) * b * 4);
+         al256(size_t(n_rows) * b * 4) +
+         (b <= kCompactMaxB ? al256(size_t(n_fixed) * compact_ld(b) * 4) : 0);
 }
 
 size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, int32_t b,
@@ -182,7 +191,8 @@ size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, 
   // epoch layout: [slab d*b][gram partials][pass scratch]; loss needs at most
   // 2 d x d gramians + partials, covered separately by ials_loss_workspace.
   return al256(size_t(d) * b * 4) + gram_ws(std::max(n_rows_max, n_fixed_max), d, b) +
-         pass_ws(std::max(n_rows_max, n_fixed_max), b, n_slices_max, n_heavy_max);
+         pass_ws(std::max(n_rows_max, n_fixed_max), std::max(n_rows_max, n_fixed_max), b,
+                 n_slices_max, n_heavy_max);
 }
 
 // ------------------------------------------------------------------ predictions
@@ -288,7 +298,22 @@ static int gramian_impl(ials_session* s, const float* M, int32_t n, int32_t ldm,
     CUDA_TRY(s, cudaMemsetAsync(slab, 0, size_t(d) * b * 4, st));
     return IALS_OK;
   }
-  if (b <= 16) {  // narrow 128 x 16 tiles: no wasted 64-wide tile columns
+  if (b <= 4) {  // GEMV: thread per column, split-K over rows (bandwidth-bound)
+    const int ct = (d + 255) / 256;
+    int ns = std::max(1, std::min((4 * kNumSMs + ct - 1) / ct, (n + 63) / 64));
+    ns = std::min(ns, kGemvSplits);
+    while (ns > 1 && size_t(ns) * d * b * 4 > part_bytes) --ns;
+    nsplit = ns;
+    rps = (n + nsplit - 1) / nsplit;
+    nsplit = (n + rps - 1) / rps;
+    dim3 g(ct, nsplit);
+    switch (b) {
+      case 1: k_slab_gemv<1><<<g, 256, 0, st>>>(M, n, ldm, d, b0, rps, part); break;
+      case 2: k_slab_gemv<2><<<g, 256, 0, st>>>(M, n, ldm, d, b0, rps, part); break;
+      case 3: k_slab_gemv<3><<<g, 256, 0, st>>>(M, n, ldm, d, b0, rps, part); break;
+      default: k_slab_gemv<4><<<g, 256, 0, st>>>(M, n, ldm, d, b0, rps, part); break;
+    }
+  } else if (b <= 16) {  // narrow 128 x 16 tiles: no wasted 64-wide tile columns
     const int ct = (d + 127) / 128;
     int ns = std::max(1, std::min(2 * kNumSMs / ct, (n + 255) / 256));
     ns = std::min(ns, kMaxSplits);
@@ -305,8 +330,12 @@ static int gramian_impl(ials_session* s, const float* M, int32_t n, int32_t ldm,
   }
   LAUNCH_CHECK(s);
   const size_t cnt = size_t(d) * b;
-  const int rb = (int)std::min<size_t>((cnt + 255) / 256, 4096);
-  k_reduce_splits<<<rb, 256, 0, st>>>(part, nsplit, cnt, slab);
+  if (nsplit > 64 && cnt < (size_t(1) << 26)) {
+    k_reduce_splits_warp<<<(unsigned)((cnt + 7) / 8), 256, 0, st>>>(part, nsplit, (int)cnt, slab);
+  } else {
+    const int rb = (int)std::min<size_t>((cnt + 255) / 256, 4096);
+    k_reduce_splits<<<rb, 256, 0, st>>>(part, nsplit, cnt, slab);
+  }
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
@@ -579,7 +608,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     return fail(s, IALS_E_INVALID, "side_pass: bad block (d=%d b0=%d b=%d)", d, b0, b);
   const int bt = block_tile(b);
   const bool use_tc = bt == 128 && b > 32 && tc_enabled() && sched->tc_n_rows > 0;
-  const size_t need_simt = pass_ws(side->n_rows, b, sched->n_slices, sched->n_heavy);
+  const size_t need_simt = pass_ws(side->n_rows, side->n_fixed, b, sched->n_slices, sched->n_heavy);
   const size_t need_tc = al256(size_t(side->n_rows) * b * 4) +
                          ials_tc_workspace_bytes(sched->tc_max_wave_rows, sched->tc_max_wave_slices);
   const size_t need = use_tc ? need_tc : need_simt;
@@ -594,6 +623,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.ldo = ldo;
   p.d = d;
   p.b0 = b0;
+  p.fb0 = b0;
   p.b = b;
   p.slab = slab;
   p.alpha0 = alpha0;
@@ -626,6 +656,20 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.redo_rows = reinterpret_cast<int*>(w + 16);
   w += al256(size_t(side->n_rows) * 4 + 16);
   p.drow = reinterpret_cast<float*>(w);
+  w += al256(size_t(side->n_rows) * b * 4);
+  if (b <= kCompactMaxB && !use_tc && side->n_fixed > 0) {
+    // gather from a compact, L2-resident copy of fixed[:, b0:b0+b]
+    const int ldc = compact_ld(b);
+    float* compact = reinterpret_cast<float*>(w);
+    const long long cnt = (long long)side->n_fixed * ldc;
+    k_compact_cols<<<(int)std::min<long long>((cnt + 255) / 256, 65535), 256, 0, st>>>(
+        fixed, side->n_fixed, ldf, b0, b, compact, ldc);
+    LAUNCH_CHECK(s);
+    p.fixed = compact;
+    p.ldf = ldc;
+    p.fb0 = 0;
+    p.vec = (b % 4 == 0) && (reinterpret_cast<uintptr_t>(compact) % 16 == 0);
+  }
   p.redo_total = s->redo;
   p.cond_max = tc_cond_max();
   p.n_light_dev = nullptr;
@@ -653,7 +697,16 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.dbuf = nullptr;
   }
   if (side->n_rows > 0 && !proj_ready) {
-    if (b <= 16) {
+    if (b <= 4) {
+      const int g = (side->n_rows + 7) / 8;
+      const int vec = (d % 4 == 0) && (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(own) % 16 == 0);
+      switch (b) {
+        case 1: k_project_gemv<1><<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, alpha0, vec, proj); break;
+        case 2: k_project_gemv<2><<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, alpha0, vec, proj); break;
+        case 3: k_project_gemv<3><<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, alpha0, vec, proj); break;
+        default: k_project_gemv<4><<<g, 256, 0, st>>>(own, side->n_rows, ldo, d, slab, alpha0, vec, proj); break;
+      }
+    } else if (b <= 16) {
       k_project_narrow<<<(side->n_rows + 127) / 128, 256, 0, st>>>(own, side->n_rows, ldo, d, slab,
                                                                     b, alpha0, proj);
     } else {
@@ -672,7 +725,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
       const int g = std::min((p.n_slices + 7) / 8, kNumSMs * 16);
       k_b1_partial<<<g, 256, 0, st>>>(p);
       LAUNCH_CHECK(s);
-      k_b1_solve<<<(p.n_heavy + 127) / 128, 128, 0, st>>>(p);
+      k_b1_solve<<<(p.n_heavy + 7) / 8, 256, 0, st>>>(p);
       LAUNCH_CHECK(s);
       k_b1_cache<<<g, 256, 0, st>>>(p);
       LAUNCH_CHECK(s);
@@ -876,8 +929,9 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
   // tensor-core GEMMs (with the fused tensor-core sweep, b in 65..128): the
   // K-major copies live at the end of the workspace when it has room
   const size_t tcb = tc_gemm_bytes(users->n_rows, items->n_rows, d, b);
-  const size_t pass_need = std::max(pass_ws(users->n_rows, b, user_sched->n_slices, user_sched->n_heavy),
-                                    pass_ws(items->n_rows, b, item_sched->n_slices, item_sched->n_heavy));
+  const size_t pass_need =
+      std::max(pass_ws(users->n_rows, users->n_fixed, b, user_sched->n_slices, user_sched->n_heavy),
+               pass_ws(items->n_rows, items->n_fixed, b, item_sched->n_slices, item_sched->n_heavy));
   const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 64 && d % 4 == 0 &&
                        ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= pass_need + tcb &&

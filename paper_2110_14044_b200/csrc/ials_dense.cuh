@@ -331,4 +331,118 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+
+// ---------------------------------------------------------------- b <= 4
+// For the narrowest blocks (b = 1 is the iCD case) the slab and the
+// projection are GEMVs over a whole factor matrix: bandwidth-bound, so they
+// read each row once, coalesced, with many rows in flight.
+//
+// slab partial: part[split][k][j] = sum_{r in split} M[r][k] M[r][b0 + j];
+// thread <-> column k, 8 rows per step (the M[r][b0+j] values are warp-wide
+// broadcasts).
+template <int B>
+__global__ void __launch_bounds__(256)
+    k_slab_gemv(const float* __restrict__ M, int n, int ldm, int d, int b0, int rows_per_split,
+                float* __restrict__ part) {
+  const int split = blockIdx.y;
+  const int k = blockIdx.x * 256 + threadIdx.x;
+  const int r_beg = split * rows_per_split, r_end = min(n, r_beg + rows_per_split);
+  const bool ok = k < d;
+  float a0[B], a1[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) a0[j] = a1[j] = 0.f;
+  int r = r_beg;
+  for (; r + 7 < r_end; r += 8) {
+    float x[8], f[8][B];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float* row = M + (size_t)(r + u) * ldm;
+      x[u] = ok ? __ldg(row + k) : 0.f;
+#pragma unroll
+      for (int j = 0; j < B; ++j) f[u][j] = __ldg(row + b0 + j);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u += 2)
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        a0[j] = fmaf(x[u], f[u][j], a0[j]);
+        a1[j] = fmaf(x[u + 1], f[u + 1][j], a1[j]);
+      }
+  }
+  for (; r < r_end; ++r) {
+    const float* row = M + (size_t)r * ldm;
+    const float x = ok ? __ldg(row + k) : 0.f;
+#pragma unroll
+    for (int j = 0; j < B; ++j) a0[j] = fmaf(x, __ldg(row + b0 + j), a0[j]);
+  }
+  if (ok) {
+    float* o = part + (size_t)split * d * B + (size_t)k * B;
+#pragma unroll
+    for (int j = 0; j < B; ++j) o[j] = a0[j] + a1[j];
+  }
+}
+
+// projection: proj[r][j] = alpha0 * sum_k own[r][k] slab[k][j]; warp per
+// row, 16-byte coalesced loads, shuffle reduction.
+template <int B>
+__global__ void __launch_bounds__(256)
+    k_project_gemv(const float* __restrict__ own, int n_rows, int ldo, int d,
+                   const float* __restrict__ slab, float alpha0, int vec, float* __restrict__ proj) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= n_rows) return;
+  const float* row = own + (size_t)r * ldo;
+  float acc[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) acc[j] = 0.f;
+  if (vec) {
+    for (int k4 = lane; 4 * k4 < d; k4 += 32) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(row) + k4);
+      const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < B; ++j) acc[j] = fmaf(xs[q], __ldg(slab + (size_t)(4 * k4 + q) * B + j), acc[j]);
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) {
+      const float x = __ldg(row + k);
+#pragma unroll
+      for (int j = 0; j < B; ++j) acc[j] = fmaf(x, __ldg(slab + (size_t)k * B + j), acc[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    float v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) proj[(size_t)r * B + j] = alpha0 * v;
+  }
+}
+
+
+// out[r][j] = F[r][b0 + j] for j < b (0 for the padding up to ldc)
+__global__ void k_compact_cols(const float* __restrict__ F, int n, int ldf, int b0, int b,
+                               float* __restrict__ out, int ldc) {
+  const long long cnt = (long long)n * ldc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldc), j = (int)(i - (long long)r * ldc);
+    out[i] = j < b ? __ldg(F + (size_t)r * ldf + b0 + j) : 0.f;
+  }
+}
+
+// many splits (the b <= 4 GEMV slab): warp per output element, lanes stride
+// the splits, fixed shuffle tree
+__global__ void __launch_bounds__(256)
+    k_reduce_splits_warp(const float* __restrict__ part, int nsplit, int count, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= count) return;
+  float s = 0.f;
+  for (int k = lane; k < nsplit; k += 32) s += part[(size_t)k * count + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[i] = s;
+}
 }  // namespace ials

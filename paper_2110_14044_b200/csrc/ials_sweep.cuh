@@ -80,6 +80,7 @@ struct SweepParams {
   float cond_max;
   const int* n_light_dev;  // if set, k_sweep_light reads its row count here
   float* drow;             // [n_rows][b] per-row d of the fused sweep (k_pass_cache)
+  int fb0;                 // column of the block in `fixed` (b0, or 0 for a compact copy)
 };
 
 template <int BT>
@@ -183,13 +184,13 @@ IALS_DEVI void stage_chunk(const SweepParams& p, float* sm, int buf, int ebeg, i
       const int k = i >> LG, v = i & (SL - 1);
       if (v >= bv) continue;
       const int col = __ldg(p.side.cols + ebeg + k);
-      cp_async16(X + k * L::XLD + 4 * v, p.fixed + (size_t)col * p.ldf + p.b0 + 4 * v);
+      cp_async16(X + k * L::XLD + 4 * v, p.fixed + (size_t)col * p.ldf + p.fb0 + 4 * v);
     }
   } else {
     for (int i = tid; i < nk * p.b; i += L::NT) {
       int k = i / p.b, v = i - k * p.b;
       int col = __ldg(p.side.cols + ebeg + k);
-      cp_async4(X + k * L::XLD + v, p.fixed + (size_t)col * p.ldf + p.b0 + v);
+      cp_async4(X + k * L::XLD + v, p.fixed + (size_t)col * p.ldf + p.fb0 + v);
     }
   }
   cp_async_commit();

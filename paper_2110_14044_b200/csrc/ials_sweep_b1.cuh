@@ -12,7 +12,7 @@ namespace ials {
 
 IALS_DEVI void b1_entry(const SweepParams& p, int e, float& h, float& a, int& pos, float& rho) {
   const int col = __ldg(p.side.cols + e);
-  h = __ldg(p.fixed + (size_t)col * p.ldf + p.b0);
+  h = __ldg(p.fixed + (size_t)col * p.ldf + p.fb0);
   a = p.side.weights ? __ldg(p.side.weights + e) : 1.f;
   const float y = p.side.labels ? __ldg(p.side.labels + e) : 1.f;
   pos = p.side.pos ? __ldg(p.side.pos + e) : e;
@@ -55,13 +55,13 @@ IALS_DEVI void b1_cache(const SweepParams& p, int first, int end, int stride, fl
       pos[u] = p.side.pos ? __ldg(p.side.pos + e + u * stride) : e + u * stride;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) h[u] = __ldg(p.fixed + (size_t)col[u] * p.ldf + p.b0);
+    for (int u = 0; u < 4; ++u) h[u] = __ldg(p.fixed + (size_t)col[u] * p.ldf + p.fb0);
 #pragma unroll
     for (int u = 0; u < 4; ++u) p.cache[pos[u]] -= h[u] * dl;
   }
   for (; e < end; e += stride) {
     const int col = __ldg(p.side.cols + e);
-    const float h = __ldg(p.fixed + (size_t)col * p.ldf + p.b0);
+    const float h = __ldg(p.fixed + (size_t)col * p.ldf + p.fb0);
     const int pos = p.side.pos ? __ldg(p.side.pos + e) : e;
     p.cache[pos] -= h * dl;
   }
@@ -126,15 +126,25 @@ __global__ void __launch_bounds__(256) k_b1_partial(SweepParams p) {
   }
 }
 
-__global__ void k_b1_solve(SweepParams p) {
-  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < p.n_heavy; h += gridDim.x * blockDim.x) {
+// warp per heavy row: lanes stride the row's slices, then a fixed shuffle
+// tree (deterministic; the longest rows have hundreds of slices)
+__global__ void __launch_bounds__(256) k_b1_solve(SweepParams p) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int h = gw; h < p.n_heavy; h += nw) {
     float hh = 0.f;
     double gg = 0.0;
-    for (int sl = p.heavy_slice0[h]; sl < p.heavy_slice0[h + 1]; ++sl) {
+    for (int sl = p.heavy_slice0[h] + lane; sl < p.heavy_slice0[h + 1]; sl += 32) {
       hh += p.hpart[sl];
       gg += p.gpart[sl];
     }
-    p.hdelta[h] = b1_solve(p, p.heavy_rows[h], hh, gg);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      hh += __shfl_xor_sync(0xffffffffu, hh, o);
+      gg += __shfl_xor_sync(0xffffffffu, gg, o);
+    }
+    if (lane == 0) p.hdelta[h] = b1_solve(p, p.heavy_rows[h], hh, gg);
   }
 }
 

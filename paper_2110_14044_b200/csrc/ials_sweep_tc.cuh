@@ -72,13 +72,13 @@ IALS_DEVI void stage_entries(const SweepParams& p, float* X, float* aw, float* r
     for (int i = tid; i < nk * bv; i += NT) {
       const int k = i / bv, v = i - k * bv;
       const int col = __ldg(p.side.cols + ebeg + k);
-      cp_async16(X + k * XLD + 4 * v, p.fixed + (size_t)col * p.ldf + p.b0 + 4 * v);
+      cp_async16(X + k * XLD + 4 * v, p.fixed + (size_t)col * p.ldf + p.fb0 + 4 * v);
     }
   } else {
     for (int i = tid; i < nk * p.b; i += NT) {
       const int k = i / p.b, v = i - k * p.b;
       const int col = __ldg(p.side.cols + ebeg + k);
-      cp_async4(X + k * XLD + v, p.fixed + (size_t)col * p.ldf + p.b0 + v);
+      cp_async4(X + k * XLD + v, p.fixed + (size_t)col * p.ldf + p.fb0 + v);
     }
   }
   cp_async_commit();

@@ -131,7 +131,7 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, int ebeg, int eend, 
   if (p.vec) {   // lane <-> 16-byte piece of a sub-row (b <= 128: 32 pieces), warp <-> entry
     const int lane = tid & 31, warp = tid >> 5;
     if (lane < (p.b >> 2)) {
-      const float* src = p.fixed + p.b0 + 4 * lane;
+      const float* src = p.fixed + p.fb0 + 4 * lane;
 #pragma unroll
       for (int k = warp; k < L::KC; k += L::NT / 32)
         if (k < nk) cp_async16(X + k * L::XLD + 4 * lane, src + (size_t)mc[k] * p.ldf);
@@ -139,7 +139,7 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, int ebeg, int eend, 
   } else {
     for (int i = tid; i < nk * p.b; i += L::NT) {
       const int k = i / p.b, v = i - k * p.b;
-      cp_async4(X + k * L::XLD + v, p.fixed + (size_t)mc[k] * p.ldf + p.b0 + v);
+      cp_async4(X + k * L::XLD + v, p.fixed + (size_t)mc[k] * p.ldf + p.fb0 + v);
     }
   }
   if (tid < nk)
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
   for (int j = 0; j < 16; ++j) dv[j] = (c0 + j < b) ? __ldg(d + c0 + j) : 0.f;
   for (int e = ebeg + slot; e < eend; e += 32) {
     const int col = __ldg(p.side.cols + e);
-    const float* xr = p.fixed + (size_t)col * p.ldf + p.b0 + c0;
+    const float* xr = p.fixed + (size_t)col * p.ldf + p.fb0 + c0;
     float s = 0.f;
     if (p.vec) {
 #pragma unroll
