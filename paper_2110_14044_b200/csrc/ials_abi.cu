@@ -407,6 +407,50 @@ int ials_set_tensor_cores(int enable) {
   return prev;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encode(ials_session* s) {
+  if (g_encode) return IALS_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(s, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return IALS_OK;
+}
+
+// 2-D fp32 map: `inner` contiguous elements per row, `rows` rows ld_floats
+// apart; boxes of 32 x box_rows land 128B-swizzled (K-major operand rows)
+static int make_map(ials_session* s, CUtensorMap* m, const float* ptr, uint64_t inner, uint64_t rows,
+                    uint64_t ld_floats, uint32_t box_rows) {
+  cuuint64_t gdim[2] = {inner, rows};
+  cuuint64_t gstr[1] = {ld_floats * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim,
+                              gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return IALS_OK;
+}
+
+// rows of `fixed` (n_fixed x d, ld ldf) in boxes of 128 columns x 1 row: the
+// tile::gather4 source of the fused sweep (out-of-range columns read as 0)
+static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, uint64_t d, uint64_t rows,
+                           uint64_t ld_floats) {
+  cuuint64_t gdim[2] = {d, rows};
+  cuuint64_t gstr[1] = {ld_floats * 4};
+  cuuint32_t box[2] = {128, 1};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim,
+                              gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled (gather) failed (%d)", (int)r);
+  return IALS_OK;
+}
+
 // BT = 128, b > 64: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
 // heavy rows on the SIMT slice kernels.
 static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t st) {
@@ -414,6 +458,13 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
   CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, sizeof(int), st));
+  // sub-row gathers by TMA (tile::gather4) when the fixed matrix allows it
+  CUtensorMap fmap;
+  memset(&fmap, 0, sizeof(fmap));
+  int use_tma = 0;
+  if (p.vec && p.side.n_fixed > 0 && get_encode(s) == IALS_OK &&
+      make_gather_map(s, &fmap, p.fixed, p.d, p.side.n_fixed, p.ldf) == IALS_OK)
+    use_tma = 1;
   if (p.n_light > 0) {
     static bool init = false;
     if (!init) {
@@ -426,7 +477,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
     const int grid = std::min(p.n_light, 4 * kNumSMs);   // TMEM: 4 x 128 columns per SM
-    k_sweep_tc4<<<grid, 128, TcLay4::BYTES, st>>>(p);
+    k_sweep_tc4<<<grid, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
     LAUNCH_CHECK(s);
   }
   if (p.n_heavy > 0) {
@@ -439,7 +490,8 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
       hinit = true;
     }
     const int threads = L::NT * L::RPC;
-    k_heavy_partial_tc4<<<std::min(p.n_slices, 4 * kNumSMs), 128, TcLay4::BYTES, st>>>(p);
+    k_heavy_partial_tc4<<<std::min(p.n_slices, 4 * kNumSMs), 128, TcLay4::BYTES, st>>>(p, fmap,
+                                                                                     use_tma);
     LAUNCH_CHECK(s);
     k_heavy_solve<128, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
@@ -753,35 +805,6 @@ int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sch
 
 
 // ------------------------------------------------------------------ tensor-core GEMMs (epoch)
-static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-
-static int get_encode(ials_session* s) {
-  if (g_encode) return IALS_OK;
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  CUDA_TRY(s, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-  if (!fn || q != cudaDriverEntryPointSuccess)
-    return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled is unavailable");
-  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  return IALS_OK;
-}
-
-// 2-D fp32 map: `inner` contiguous elements per row, `rows` rows ld_floats
-// apart; boxes of 32 x box_rows land 128B-swizzled (K-major operand rows)
-static int make_map(ials_session* s, CUtensorMap* m, const float* ptr, uint64_t inner, uint64_t rows,
-                    uint64_t ld_floats, uint32_t box_rows) {
-  cuuint64_t gdim[2] = {inner, rows};
-  cuuint64_t gstr[1] = {ld_floats * 4};
-  cuuint32_t box[2] = {32, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim,
-                              gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(s, IALS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return IALS_OK;
-}
-
 static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 
 // split-K plan of the Gramian: >= 2 CTAs per SM and at most 2048 rows

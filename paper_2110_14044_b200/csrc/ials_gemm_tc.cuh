@@ -20,23 +20,6 @@
 
 namespace ials {
 
-IALS_DEVI void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c_inner, int c_row,
-                           uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c_inner), "r"(c_row), "r"(smem_u32(bar))
-      : "memory");
-}
-IALS_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-IALS_DEVI void prefetch_tmap(const CUtensorMap* m) {
-  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-}
-
 struct GemmJob {
   int m_rows;              // valid output rows (rows of A)
   int a_row0;              // first A row of tile 0 (row coordinate in the A maps)

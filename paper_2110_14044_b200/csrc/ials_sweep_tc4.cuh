@@ -24,7 +24,7 @@
 namespace ials {
 
 struct TcLay4 {
-  static constexpr int BT = 128, NT = 128, KC = 16, XLD = BT + 4;
+  static constexpr int BT = 128, NT = 128, KC = 16, XLD = BT;   // X rows as TMA gathers them
   static constexpr int MR = 8;   // metadata ring depth (chunks)
   // overlay region (1024-aligned), by phase:
   //   accumulate: XT hi/lo double buffer  4 x 8 KB (K-major SW64)
@@ -53,8 +53,8 @@ struct TcLay4 {
   static constexpr int OFF_LI = OFF_X + 8192;      // backward: 8 x 16x16 block inverses
   static constexpr int OFF_DIAG = OFF_D + BT * 4;  // H_kk before the factorisation
   static constexpr int OFF_FLAG = OFF_DIAG + BT * 4;
-  static constexpr int OFF_BAR = OFF_FLAG + 16;    // 2 mbarriers + TMEM base
-  static constexpr int BYTES = OFF_BAR + 32 + 1024;
+  static constexpr int OFF_BAR = OFF_FLAG + 16;    // MMA mbarriers [2], gather mbarriers [2], TMEM base
+  static constexpr int BYTES = OFF_BAR + 48 + 1024;
 };
 
 // K-major, 64B-swizzle float index of operand element (row m, k) of a
@@ -69,6 +69,8 @@ constexpr uint32_t kSwizzle64B = 4;
 struct Tc4State {
   uint32_t tmem;
   uint32_t ph;      // bit x: phase parity of the next completion of bar[x]
+  uint32_t gph;     // bit x: the same for the gather barrier of staging buffer x
+  const CUtensorMap* fmap;   // fixed[:, fb0:fb0+128] rows for tile::gather4, or null (cp.async)
 };
 
 // step 1: TMEM row i := template row i (+ lam on the diagonal), zero above
@@ -121,14 +123,27 @@ IALS_DEVI void tc4_meta(const SweepParams& p, char* smem, int ebeg, int eend, in
   }
 }
 
-IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, int ebeg, int eend, int c, int tid) {
+IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, const Tc4State& st, int ebeg, int eend,
+                          int c, int tid) {
   using L = TcLay4;
   const int nk = min(L::KC, eend - (ebeg + c * L::KC));
   if (nk <= 0) return;
   const int* mc = reinterpret_cast<const int*>(smem + L::OFF_MC) + (c & (L::MR - 1)) * L::KC;
   const int* mp = reinterpret_cast<const int*>(smem + L::OFF_MP) + (c & (L::MR - 1)) * L::KC;
   float* X = reinterpret_cast<float*>(smem + L::OFF_X) + (c & 1) * L::KC * L::XLD;
-  if (p.vec) {   // lane <-> 16-byte piece of a sub-row (b <= 128: 32 pieces), warp <-> entry
+  if (st.fmap) {   // one thread (warp 1: warp 0 issues the MMAs): ceil(nk / 4) TMA
+                   // gathers of 4 sub-rows (128 floats each)
+    if (tid == 32) {
+      uint64_t* gb = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR) + 2 + (c & 1);
+      const int ng = (nk + 3) >> 2;
+      mbar_expect_tx(gb, (uint32_t)ng * 4 * L::XLD * 4);
+      for (int g = 0; g < ng; ++g) {
+        const int k = 4 * g, last = nk - 1;
+        tma_gather4(smem_u32(X + k * L::XLD), st.fmap, p.fb0, mc[min(k, last)],
+                    mc[min(k + 1, last)], mc[min(k + 2, last)], mc[min(k + 3, last)], gb);
+      }
+    }
+  } else if (p.vec) {   // lane <-> 16-byte piece of a sub-row (b <= 128: 32 pieces), warp <-> entry
     const int lane = tid & 31, warp = tid >> 5;
     if (lane < (p.b >> 2)) {
       const float* src = p.fixed + p.fb0 + 4 * lane;
@@ -164,15 +179,19 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  tc4_gather(p, smem, ebeg, eend, 0, tid);
+  tc4_gather(p, smem, st, ebeg, eend, 0, tid);
   cp_async_commit();
-  tc4_gather(p, smem, ebeg, eend, 1, tid);
+  tc4_gather(p, smem, st, ebeg, eend, 1, tid);
   cp_async_commit();
   for (int c = 0; c < nch; ++c) {
     const int xb = c & 1;
     const int nk = min(L::KC, eend - (ebeg + c * L::KC));
     if (watch && c == 3) tp[0] = clock64();
     cp_async_wait<1>();
+    if (st.fmap) {   // the sub-rows of chunk c (TMA gather)
+      mbar_wait(reinterpret_cast<uint64_t*>(smem + L::OFF_BAR) + 2 + xb, (st.gph >> xb) & 1u);
+      st.gph ^= 1u << xb;
+    }
     if (watch && c == 3) tp[1] = clock64();
     __syncthreads();
     if (watch && c == 3) tp[2] = clock64();
@@ -188,8 +207,10 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
 #pragma unroll
     for (int k = 0; k < 16; ++k) x[k] = (colok && k < nk) ? X[k * L::XLD + tid] : 0.f;
     float wk[16];   // the chunk's weights: 16-byte broadcast reads of the rings
-    {  // gradient: four fixed-order fp64 chains (entries k mod 4)
-      double g[4] = {0.0, 0.0, 0.0, 0.0};
+    {  // gradient: the chunk's 16 products in four fixed-order fp32 chains
+       // (entries k mod 4), folded into the fp64 row sum (long rows cancel
+       // across chunks, so the row sum itself stays fp64)
+      float g[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int k4 = 0; k4 < 4; ++k4) {
         const float4 w4 = reinterpret_cast<const float4*>(mw)[k4];
@@ -202,10 +223,10 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
           const int k = 4 * k4 + j;
           wk[k] = w[j];
           const float r = (k < nk) ? w[j] * (cc[j] - yy[j]) : 0.f;
-          g[j] = fma((double)r, (double)x[k], g[j]);
+          g[j] = fmaf(r, x[k], g[j]);
         }
       }
-      gacc += (g[0] + g[1]) + (g[2] + g[3]);
+      gacc += ((double)g[0] + (double)g[1]) + ((double)g[2] + (double)g[3]);
     }
     if (p.side.weights) {  // a h h^T = (sqrt(a) h)(sqrt(a) h)^T
 #pragma unroll
@@ -257,7 +278,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
     pend |= 1u << xb;
     // group c: X / yhat of chunk c+2 (its buffers were consumed above), and
     // the metadata of chunk c+4
-    if (c + 2 < nch) tc4_gather(p, smem, ebeg, eend, c + 2, tid);
+    if (c + 2 < nch) tc4_gather(p, smem, st, ebeg, eend, c + 2, tid);
     if (c + 4 < nch) tc4_meta(p, smem, ebeg, eend, c + 4, tid);
     cp_async_commit();
     if (watch && c == 3) tp[6] = clock64();
@@ -532,7 +553,9 @@ IALS_DEVI void tc4_backward(const SweepParams& p, char* smem, int tid) {
   }
 }
 
-__global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
+__global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
+                                                          const __grid_constant__ CUtensorMap fmap,
+                                                          int use_tma) {
   using L = TcLay4;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = tc_smem_base(smem_raw);
@@ -542,13 +565,16 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
     for (int i = tid; i < 2 * L::KC * L::XLD / 4; i += L::NT) x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + 16);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + 32);
   float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
   float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
   ds[tid] = 0.f;
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
+    mbar_init(bar + 2, 1);
+    mbar_init(bar + 3, 1);
+    if (use_tma) prefetch_tmap(&fmap);
   }
   if (tid < 32) tmem_alloc(tptr, 128);
   tc_fence_before();
@@ -557,6 +583,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
   Tc4State st;
   st.tmem = *tptr;
   st.ph = 0u;
+  st.gph = 0u;
+  st.fmap = use_tma ? &fmap : nullptr;
   const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
   const int b = p.b;
   int ndone = 0;
@@ -650,16 +678,21 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p) {
 // from zero in TMEM (same pipelined gather / 3xTF32 MMAs as the light rows)
 // and written row-major (the layout k_heavy_solve<128> reads) with its fp64
 // partial gradient; the slices of a row are combined in k_heavy_solve.
-__global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p) {
+__global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
+                                                          const __grid_constant__ CUtensorMap fmap,
+                                                          int use_tma) {
   using L = TcLay4;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = tc_smem_base(smem_raw);
   const int tid = threadIdx.x;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + 16);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_BAR + 32);
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
+    mbar_init(bar + 2, 1);
+    mbar_init(bar + 3, 1);
+    if (use_tma) prefetch_tmap(&fmap);
   }
   if (tid < 32) tmem_alloc(tptr, 128);
   tc_fence_before();
@@ -668,6 +701,8 @@ __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p) {
   Tc4State st;
   st.tmem = *tptr;
   st.ph = 0u;
+  st.gph = 0u;
+  st.fmap = use_tma ? &fmap : nullptr;
   const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
   for (int sl = blockIdx.x; sl < p.n_slices; sl += gridDim.x) {
     {

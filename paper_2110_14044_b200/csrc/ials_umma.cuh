@@ -4,6 +4,7 @@
 // (shared-memory matrix descriptor, instruction descriptor for kind::tf32).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #ifndef IALS_DEVI
@@ -134,6 +135,35 @@ IALS_DEVI void mbar_wait(uint64_t* bar, uint32_t phase) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
+      : "memory");
+}
+
+IALS_DEVI void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c_inner, int c_row,
+                           uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c_inner), "r"(c_row), "r"(smem_u32(bar))
+      : "memory");
+}
+IALS_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+IALS_DEVI void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+// tile::gather4: four rows (row coordinates r0..r3) of a 2-D map whose box is
+// {width, 1} land back to back in shared memory
+IALS_DEVI void tma_gather4(uint32_t dst, const CUtensorMap* map, int c_inner, int r0, int r1, int r2,
+                           int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c_inner), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "r"(smem_u32(bar))
       : "memory");
 }
 
