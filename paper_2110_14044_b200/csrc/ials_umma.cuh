@@ -175,10 +175,11 @@ IALS_DEVI float tf32_lo(float x) {
 
 // round-to-nearest tf32 (low 13 bits zero): the unbiased split
 // hi = rna(x), lo = rna(x - hi) leaves |x - hi - lo| <= 2^-22 |x|.
+// (integer form of cvt.rna.tf32.f32 -- half an ulp of the 10-bit mantissa
+// added to the magnitude, low 13 bits cleared -- so it runs on the ALU pipe
+// instead of the conversion unit; identical for finite inputs)
 IALS_DEVI float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 }  // namespace ials
