@@ -266,19 +266,21 @@ IALS_DEVI void accumulate_chunk(Tiles<BT>& T, double& gacc, const float* sm, int
       for (int j = 0; j < L::SC; ++j) T.acc[t][i][j] += loc[i][j];
   }
   if (tid < BT) {
-    // fp64: g = sum rho_k h_k + alpha0 w G + lam w cancels by orders of magnitude
-    // on long rows, so the sum is formed in double and rounded once (four
-    // independent chains hide the DFMA latency; fixed combination order).
-    double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+    // g = sum rho_k h_k + alpha0 w G + lam w cancels by orders of magnitude
+    // on long rows, so the row sum is kept in double; each chunk's products
+    // are summed in four fixed-order fp32 chains and folded in (4 fp64
+    // conversions per chunk instead of 2 per entry: the conversion unit is
+    // narrow).
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
     int k = 0;
     for (; k + 3 < nk; k += 4) {
-      g0 = fma((double)rh[k], (double)X[k * L::XLD + tid], g0);
-      g1 = fma((double)rh[k + 1], (double)X[(k + 1) * L::XLD + tid], g1);
-      g2 = fma((double)rh[k + 2], (double)X[(k + 2) * L::XLD + tid], g2);
-      g3 = fma((double)rh[k + 3], (double)X[(k + 3) * L::XLD + tid], g3);
+      g0 = fmaf(rh[k], X[k * L::XLD + tid], g0);
+      g1 = fmaf(rh[k + 1], X[(k + 1) * L::XLD + tid], g1);
+      g2 = fmaf(rh[k + 2], X[(k + 2) * L::XLD + tid], g2);
+      g3 = fmaf(rh[k + 3], X[(k + 3) * L::XLD + tid], g3);
     }
-    for (; k < nk; ++k) g0 = fma((double)rh[k], (double)X[k * L::XLD + tid], g0);
-    gacc += (g0 + g1) + (g2 + g3);
+    for (; k < nk; ++k) g0 = fmaf(rh[k], X[k * L::XLD + tid], g0);
+    gacc += ((double)g0 + (double)g1) + ((double)g2 + (double)g3);
   }
 }
 
