@@ -737,8 +737,10 @@ __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
 
 // yhat[pos] -= x . d for every entry of the pass: light rows take d from
 // drow (the fused sweep's output; zero for rows the SIMT sweep redid), heavy
-// slices from hdelta.  8 lanes x 16 columns per entry, 32 entries in flight
-// per CTA; bandwidth-bound gather, so it runs as its own full-occupancy pass.
+// slices from hdelta.  One CTA per row (or slice), 8 lanes per entry, 32
+// entries in flight; lane g of an entry reads the 16-byte pieces 4g + 32q
+// (q = 0..3), so each load instruction covers whole 128-byte lines.
+// Bandwidth-bound gather: its own full-occupancy pass.
 __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
   const int tid = threadIdx.x, g = tid & 7, slot = tid >> 3;
   const int blk = blockIdx.x;
@@ -755,33 +757,51 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
     eend = p.slice_end[sl];
     d = p.hdelta + (size_t)p.slice_heavy[sl] * 128;
   }
-  const int b = p.b, c0 = 16 * g;
+  const int b = p.b;
   float dv[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) dv[j] = (c0 + j < b) ? __ldg(d + c0 + j) : 0.f;
-  for (int e = ebeg + slot; e < eend; e += 32) {
-    const int col = __ldg(p.side.cols + e);
-    const float* xr = p.fixed + (size_t)col * p.ldf + p.fb0 + c0;
-    float s = 0.f;
+  for (int q = 0; q < 4; ++q) {
+    const int c = 32 * q + 4 * g;
     if (p.vec) {
+      const float4 t = (c < b) ? __ldg(reinterpret_cast<const float4*>(d + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      dv[4 * q] = t.x; dv[4 * q + 1] = t.y; dv[4 * q + 2] = t.z; dv[4 * q + 3] = t.w;
+    } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (c0 + 4 * q < b) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(xr) + q);
+      for (int j = 0; j < 4; ++j) dv[4 * q + j] = (c + j < b) ? __ldg(d + c + j) : 0.f;
+    }
+  }
+  for (int e0 = ebeg; e0 < eend; e0 += 32) {   // block-uniform trip count (shuffles below)
+    const int e = e0 + slot;
+    const bool live = e < eend;
+    const int col = live ? __ldg(p.side.cols + e) : 0;
+    const float* xr = p.fixed + (size_t)col * p.ldf + p.fb0;
+    float s = 0.f;
+    if (!live) {
+    } else if (p.vec) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 32 * q + 4 * g;
+        if (c < b) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(xr + c));
           s = fmaf(x.x, dv[4 * q], s);
           s = fmaf(x.y, dv[4 * q + 1], s);
           s = fmaf(x.z, dv[4 * q + 2], s);
           s = fmaf(x.w, dv[4 * q + 3], s);
         }
+      }
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < b) s = fmaf(__ldg(xr + j), dv[j], s);
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = 32 * q + 4 * g + j;
+          if (c < b) s = fmaf(__ldg(xr + c), dv[4 * q + j], s);
+        }
     }
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
-    if (g == 0) {
+    if (live && g == 0) {
       const int pos = p.side.pos ? __ldg(p.side.pos + e) : e;
       p.cache[pos] -= s;
     }
