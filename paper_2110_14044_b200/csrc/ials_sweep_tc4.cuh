@@ -162,15 +162,11 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, const Tc4State& st, 
 }
 
 IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, double& gacc, int ebeg,
-                             int eend, int tid, bool prof = false) {
-  // profiling: timestamps of chunk 3 (thread 0 and thread 64)
-  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const bool watch = prof && (tid == 0 || tid == 64);
+                             int eend, int tid) {
   using L = TcLay4;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   const int n = eend - ebeg;
   const int nch = (n + L::KC - 1) / L::KC;
-  const int lane = tid & 31, warp = tid >> 5;
   const uint32_t idesc = make_idesc_tf32(128, 128, 0, 0, 0);
   uint32_t pend = 0;   // bit x: bar[x] has an outstanding commit
   if (nch == 0) return 0;
@@ -180,21 +176,20 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
   cp_async_wait<0>();
   __syncthreads();
   tc4_gather(p, smem, st, ebeg, eend, 0, tid);
-  cp_async_commit();
   tc4_gather(p, smem, st, ebeg, eend, 1, tid);
   cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // one block barrier per chunk: it publishes chunk c's operands to the MMA
+  // issuer, the yhat / metadata loads of the chunks ahead to every thread,
+  // and frees chunk c's staging buffer for the gather of chunk c+2
   for (int c = 0; c < nch; ++c) {
     const int xb = c & 1;
     const int nk = min(L::KC, eend - (ebeg + c * L::KC));
-    if (watch && c == 3) tp[0] = clock64();
-    cp_async_wait<1>();
     if (st.fmap) {   // the sub-rows of chunk c (TMA gather)
       mbar_wait(reinterpret_cast<uint64_t*>(smem + L::OFF_BAR) + 2 + xb, (st.gph >> xb) & 1u);
       st.gph ^= 1u << xb;
     }
-    if (watch && c == 3) tp[1] = clock64();
-    __syncthreads();
-    if (watch && c == 3) tp[2] = clock64();
     const float* X = reinterpret_cast<const float*>(smem + L::OFF_X) + xb * L::KC * L::XLD;
     const int ms = (c & (L::MR - 1)) * L::KC;
     const float* mw = reinterpret_cast<const float*>(smem + L::OFF_MW) + ms;
@@ -233,7 +228,6 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       for (int k = 0; k < 16; ++k) x[k] *= (k < nk) ? sqrtf(wk[k]) : 0.f;
     }
     // the operand buffer xb was last read by chunk c-2's MMAs
-    if (watch && c == 3) tp[3] = clock64();
     if (pend & (1u << xb)) {
       mbar_wait(bar + xb, (st.ph >> xb) & 1u);
       st.ph ^= 1u << xb;
@@ -257,7 +251,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
         *reinterpret_cast<float4*>(XTL + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
       }
     }
-    if (watch && c == 3) tp[4] = clock64();
+    cp_async_wait<0>();   // this thread's yhat / metadata loads of the chunks ahead
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -274,14 +268,12 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       }
       umma_commit(bar + xb);
     }
-    if (watch && c == 3) tp[5] = clock64();
     pend |= 1u << xb;
-    // group c: X / yhat of chunk c+2 (its buffers were consumed above), and
-    // the metadata of chunk c+4
+    // X / yhat of chunk c+2 (its staging buffer was consumed above), and the
+    // metadata of chunk c+4
     if (c + 2 < nch) tc4_gather(p, smem, st, ebeg, eend, c + 2, tid);
     if (c + 4 < nch) tc4_meta(p, smem, ebeg, eend, c + 4, tid);
     cp_async_commit();
-    if (watch && c == 3) tp[6] = clock64();
   }
   cp_async_wait<0>();
 #pragma unroll
@@ -291,10 +283,6 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       st.ph ^= 1u << xb;
     }
   tc_fence_after();
-  if (watch && nch > 3) {
-    const int w = tid == 0 ? 0 : 1;
-    for (int k = 0; k < 8; ++k) p.dbg[16384 + (blockIdx.x * 2 + w) * 8 + k] = tp[k];
-  }
   return nch;
 }
 
@@ -602,7 +590,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
     tmem_wait_st();
     tc_fence_before();   // the first chunk's barrier orders these stores before the MMAs
     double gacc = 0.0;
-    const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid, ndone == rec_row);
+    const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid);
     if (rec) tph[2] = clock64();
     {  // + lam on the diagonal, and the diagonal itself (the cancellation
        // test's reference): lane l of warp w owns column 32w + l, reached with
