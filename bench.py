@@ -59,6 +59,21 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_traffic(cfg_key):
+    """DRAM bytes per side pass of the sweep kernels from the committed ncu
+    capture (tools/traffic.py over tools/profile_pass.py), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"traffic_{cfg_key}.json")),
+                       reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)
+            return float(t["dram_bytes_per_side_pass"]), os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 # ----------------------------------------------------------------------- data
 def dataset(shape, seed=0):
     """(U, I, CSR dict) of the synthetic set; cached on disk (inputs only)."""
@@ -288,8 +303,12 @@ def run_ours(args, cfg_key):
         achieved = rl["Q_sw"] / (sweep_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4)}
+    traffic, traffic_src = load_traffic(cfg_key)
     roof.update({
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_unit": "DRAM bytes per side pass (dram__bytes_read.sum + dram__bytes_write.sum, ncu)",
+        "traffic_source": traffic_src,
+        "algorithmic_bytes_per_side_pass": rl["Q_sw"] / (2 * rl["B"]),
         "kernel": "block sweep per side pass (b 65..128: k_sweep_tc4 + k_heavy_partial_tc4/solve + "
                   "k_pass_cache; else k_sweep_light + k_heavy_*)",
         "per_launch_algorithmic": (rl["F_sw"] if roof["unit"] == "TFLOP/s" else rl["Q_sw"]) / (2 * rl["B"]),
