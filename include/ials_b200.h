@@ -13,6 +13,8 @@
  *                             (+ _solve_rows :101-114, SingularMatrixError linalg.py:18-28)
  *   ials_epoch             <- ialspp_epoch          solvers.py:340-375
  *   ials_loss_terms        <- compute_loss          model.py:168-188 (device reductions)
+ *   ials_build_csr         <- InteractionDataset.__init__ + user_view / item_view
+ *                             data.py:98-134,148-162 (device stable radix sorts)
  *
  * Conventions
  *   - All array arguments are DEVICE pointers (memory owned by the caller,
@@ -207,6 +209,26 @@ size_t ials_loss_workspace_bytes(int32_t d);
 int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* items,
                     const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                     double* out, void* workspace, size_t ws_bytes, void* stream);
+
+/* Workspace bytes for ials_build_csr over n interactions. */
+size_t ials_build_csr_workspace_bytes(int64_t n);
+
+/* Device CSR construction, bit-exact with the reference
+ * (InteractionDataset.__init__, data.py:98-134; user_view / item_view,
+ * data.py:148-162), from COO ids already range-checked by the caller
+ * (0 <= users < U, 0 <= items < I):
+ *   order[k]     = argsort(users, stable)[k]     (canonical user-major order)
+ *   user_ptr     = [0, cumsum(bincount(users, minlength=U))]   (U+1)
+ *   user_cols[k] = items[order[k]]
+ *   item_pos[k]  = argsort(user_cols, stable)[k] (the item view's cache_pos)
+ *   item_ptr     = [0, cumsum(bincount(items, minlength=I))]   (I+1)
+ *   item_cols[k] = users[order[item_pos[k]]]
+ * Labels / weights follow as gathers by `order` / `item_pos` on the caller's
+ * side.  Deterministic (no atomics on the outputs).  n < 2^31. */
+int ials_build_csr(ials_session* s, int32_t U, int32_t I, int64_t n, const int32_t* users,
+                   const int32_t* items, int32_t* user_ptr, int32_t* user_cols, int32_t* order,
+                   int32_t* item_ptr, int32_t* item_cols, int32_t* item_pos, void* workspace,
+                   size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

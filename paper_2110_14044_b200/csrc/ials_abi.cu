@@ -14,6 +14,7 @@
 #include "../../include/ials_b200.h"
 #include "ials_common.cuh"
 #include "ials_dense.cuh"
+#include "ials_csr.cuh"
 #include "ials_sweep.cuh"
 #include "ials_loss.cuh"
 #include "ials_sweep_tc.cuh"
@@ -1016,6 +1017,94 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
     }
     rec_event(ek++, st);
   }
+  return IALS_OK;
+}
+
+// ------------------------------------------------------------------ CSR
+static int radix_passes(int K) {
+  int p = 0;
+  while (p < 4 && (int64_t(1) << (8 * p)) < int64_t(K)) ++p;
+  return p;
+}
+
+size_t ials_build_csr_workspace_bytes(int64_t n) {
+  const int64_t ntiles = (n + kRadixTile - 1) / kRadixTile;
+  return 4 * al256(size_t(std::max<int64_t>(n, 1)) * 4) + al256(size_t(std::max<int64_t>(ntiles, 1)) * 256 * 4) +
+         al256(256 * 4);
+}
+
+// stable sort of (keys, index) by keys in [0, K): LSD radix, 8-bit digits
+static int radix_sort_index(ials_session* s, const int* keys, int64_t n, int K, int* keys_out,
+                            int* vals_out, int* tk, int* tv, int* hist, int* tot, cudaStream_t st) {
+  const int P = radix_passes(K);
+  const int g = (int)((n + 255) / 256);
+  if (P == 0) {   // one key: the identity permutation
+    CUDA_TRY(s, cudaMemcpyAsync(keys_out, keys, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
+    k_iota_i32<<<g, 256, 0, st>>>(n, vals_out);
+    LAUNCH_CHECK(s);
+    return IALS_OK;
+  }
+  const int ntiles = (int)((n + kRadixTile - 1) / kRadixTile);
+  const int* ki = keys;
+  const int* vi = nullptr;   // pass 0: value = index
+  for (int p = 0; p < P; ++p) {
+    // the last pass lands in keys_out / vals_out
+    const bool to_out = ((P - 1 - p) % 2) == 0;
+    int* ko = to_out ? keys_out : tk;
+    int* vo = to_out ? vals_out : tv;
+    k_radix_hist<<<ntiles, kRadixThreads, 0, st>>>(ki, n, 8 * p, hist);
+    LAUNCH_CHECK(s);
+    k_radix_scan<<<256, 256, 0, st>>>(hist, ntiles, tot);
+    LAUNCH_CHECK(s);
+    k_radix_scatter<<<ntiles, kRadixThreads, 0, st>>>(ki, vi, n, 8 * p, hist, tot, ko, vo);
+    LAUNCH_CHECK(s);
+    ki = ko;
+    vi = vo;
+  }
+  return IALS_OK;
+}
+
+int ials_build_csr(ials_session* s, int32_t U, int32_t I, int64_t n, const int32_t* users,
+                   const int32_t* items, int32_t* user_ptr, int32_t* user_cols, int32_t* order,
+                   int32_t* item_ptr, int32_t* item_cols, int32_t* item_pos, void* workspace,
+                   size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (U < 1 || I < 1 || n < 0 || n >= (int64_t(1) << 31))
+    return fail(s, IALS_E_INVALID, "build_csr: bad sizes (U=%d I=%d n=%lld)", U, I, (long long)n);
+  if (!user_ptr || !item_ptr || (n > 0 && (!users || !items || !user_cols || !order || !item_cols || !item_pos)))
+    return fail(s, IALS_E_INVALID, "build_csr: NULL argument");
+  if (ws_bytes < ials_build_csr_workspace_bytes(n))
+    return fail(s, IALS_E_NOMEM, "build_csr: workspace %zu < %zu bytes", ws_bytes,
+                ials_build_csr_workspace_bytes(n));
+  cudaStream_t st = S(stream);
+  char* w = static_cast<char*>(workspace);
+  const size_t vb = al256(size_t(std::max<int64_t>(n, 1)) * 4);
+  int* tk = reinterpret_cast<int*>(w);
+  int* tv = reinterpret_cast<int*>(w + vb);
+  int* su = reinterpret_cast<int*>(w + 2 * vb);   // users in canonical order
+  int* si = reinterpret_cast<int*>(w + 3 * vb);   // user_cols in item order
+  int* hist = reinterpret_cast<int*>(w + 4 * vb);
+  int* tot = reinterpret_cast<int*>(w + 4 * vb + al256(size_t(std::max<int64_t>((n + kRadixTile - 1) / kRadixTile, 1)) * 256 * 4));
+  const int g = (int)((n + 255) / 256);
+  const int gp = (int)((n + 1 + 255) / 256);
+  int rc = IALS_OK;
+  if (n > 0) rc = radix_sort_index(s, users, n, U, su, order, tk, tv, hist, tot, st);
+  if (rc) return rc;
+  k_row_ptr<<<gp, 256, 0, st>>>(su, n, U, user_ptr);
+  LAUNCH_CHECK(s);
+  if (n == 0) {
+    k_row_ptr<<<1, 256, 0, st>>>(su, 0, I, item_ptr);
+    LAUNCH_CHECK(s);
+    return IALS_OK;
+  }
+  k_gather_i32<<<g, 256, 0, st>>>(items, order, n, user_cols);
+  LAUNCH_CHECK(s);
+  rc = radix_sort_index(s, user_cols, n, I, si, item_pos, tk, tv, hist, tot, st);
+  if (rc) return rc;
+  k_row_ptr<<<gp, 256, 0, st>>>(si, n, I, item_ptr);
+  LAUNCH_CHECK(s);
+  k_gather_i32<<<g, 256, 0, st>>>(su, item_pos, n, item_cols);
+  LAUNCH_CHECK(s);
   return IALS_OK;
 }
 

@@ -112,14 +112,17 @@ class DeviceSide:
     """One side of the interaction matrix on the device (SideView, data.py:26-52)."""
 
     def __init__(self, device, ptr, cols, labels, weights, pos, lam, n_fixed):
-        ptr = np.asarray(ptr, dtype=np.int64)
+        # host arrays, or device tensors straight from build_csr_device
+        ptr = ptr.cpu().numpy().astype(np.int64) if isinstance(ptr, torch.Tensor) else np.asarray(ptr, dtype=np.int64)
         self.n_rows = int(ptr.size - 1)
         self.n_fixed = int(n_fixed)
         self.nnz = int(ptr[-1])
         if self.nnz >= 2 ** 31 - 1:
             raise ValueError("more than 2^31-1 interactions are not supported")
         self.counts = np.diff(ptr)
-        to = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
+        tdt = {np.int32: torch.int32, np.float32: torch.float32}
+        to = lambda a, dt: (a.to(device=device, dtype=tdt[dt]).contiguous() if isinstance(a, torch.Tensor)
+                            else torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device))
         self.ptr = to(ptr, np.int32)
         self.cols = to(cols, np.int32)
         self.labels = None if labels is None else to(labels, np.float32)
@@ -265,6 +268,14 @@ class DeviceProblem:
         iv = data.item_view()
         return cls(device, data.num_users, data.num_items, data.user_ptr, data.items,
                    data.item_ptr, iv.cols, iv.cache_pos, data.labels, data.weights)
+
+    @classmethod
+    def from_device_csr(cls, csr, device=None):
+        """From ``csr.build_csr_device`` (both views already on the device;
+        labels and weights all ones, the BASELINE configuration)."""
+        dev = device if device is not None else csr.user_cols.device
+        return cls(dev, csr.num_users, csr.num_items, csr.user_ptr, csr.user_cols, csr.item_ptr,
+                   csr.item_cols, csr.item_pos)
 
     def set_regularizer(self, alpha0, reg, exponent):
         key = (float(alpha0), float(reg), float(exponent))
