@@ -263,10 +263,12 @@ def run_ours(args, cfg_key):
     with clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
+        n_launch0 = int(eng.lib.ials_launch_count())
         t_start.record(stream)
         for s in range(args.steps):
             eng.epoch(W, H, cache, b, ALPHA0, events=events[s])
         t_end.record(stream)
+        n_launches = int(eng.lib.ials_launch_count()) - n_launch0
         torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -376,7 +378,8 @@ def run_ours(args, cfg_key):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": launches_per_epoch * args.steps,
+            "gpu_launches": n_launches,
+            "gpu_launches_model": launches_per_epoch * args.steps,
         }
         print(json.dumps(line))
     if world > 1:
@@ -415,9 +418,13 @@ def run_sharded(args, cfg_key, ds, dev, rank, world):
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     with clk:
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        from paper_2110_14044_b200 import _lib as _l
+        lib = _l.load()
+        n_launch0 = int(lib.ials_launch_count())
         a.record(stream)
         for _ in range(args.steps):
             tr.epoch(b)
+        n_launches = int(lib.ials_launch_count()) - n_launch0
         z.record(stream)
         torch.cuda.synchronize(dev)
     dist.barrier()
@@ -469,7 +476,7 @@ def run_sharded(args, cfg_key, ds, dev, rank, world):
                          "epoch_frac_of_Ngpu_roofline": round(rl["t_epoch"] * 1e3 / world / ms_step, 4),
                          "traffic": None},
             "e2e": e2e, "cpu_baseline": None, "clocks": clk.summary(),
-            "gpu_launches": None,
+            "gpu_launches": n_launches,
         }))
     dist.destroy_process_group()
 

@@ -210,6 +210,11 @@ int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* it
                     const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                     double* out, void* workspace, size_t ws_bytes, void* stream);
 
+/* Number of kernels this library has launched since it was loaded (every
+ * launch site counts itself; stream captures count when captured, graph
+ * replays do not).  bench.py reads it around its timed region. */
+int64_t ials_launch_count(void);
+
 /* Workspace bytes for ials_build_csr over n interactions. */
 size_t ials_build_csr_workspace_bytes(int64_t n);
 

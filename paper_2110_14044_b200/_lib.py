@@ -76,6 +76,7 @@ SIGNATURES = {
                            c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p]),
     "ials_loss_workspace_bytes": (c_sz, [c_i32]),
     "ials_build_csr_workspace_bytes": (c_sz, [c_i64]),
+    "ials_launch_count": (c_i64, []),
     "ials_build_csr": (c_i32, [c_p, c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                                c_p, c_sz, c_p]),
     "ials_loss_terms": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSide), c_p,

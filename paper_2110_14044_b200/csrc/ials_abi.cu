@@ -7,6 +7,7 @@
 #include <cstring>
 #include <cstdarg>
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -51,8 +52,13 @@ static int fail(ials_session* s, int code, const char* fmt, ...) {
                   __FILE__, __LINE__);                                                \
   } while (0)
 
+// every kernel launch of the library is followed by exactly one LAUNCH_CHECK,
+// which also counts it (ials_launch_count)
+static std::atomic<long long> g_launches{0};
+
 #define LAUNCH_CHECK(s)                                                               \
   do {                                                                                \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                               \
     cudaError_t _e = cudaGetLastError();                                              \
     if (_e != cudaSuccess)                                                            \
       return fail((s), IALS_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(_e), \
@@ -60,6 +66,8 @@ static int fail(ials_session* s, int code, const char* fmt, ...) {
   } while (0)
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+int64_t ials_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static int block_tile(int b) {
