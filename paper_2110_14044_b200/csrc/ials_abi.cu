@@ -464,6 +464,7 @@ static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, ui
 // heavy rows on the SIMT slice kernels.
 static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t st) {
   using L = Lay<128>;
+  const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
   CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, sizeof(int), st));
@@ -477,30 +478,36 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
   if (p.n_light > 0) {
     static bool init = false;
     if (!init) {
-      CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       TcLay4::BYTES));
-      CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc4, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                       100));
+      for (auto k : {k_sweep_tc4<false>, k_sweep_tc4<true>}) {
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
       init = true;
     }
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
     const int grid = std::min(p.n_light, 4 * kNumSMs);   // TMEM: 4 x 128 columns per SM
-    k_sweep_tc4<<<grid, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
+    if (unit)
+      k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
+    else
+      k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
     LAUNCH_CHECK(s);
   }
   if (p.n_heavy > 0) {
     static bool hinit = false;
     if (!hinit) {
-      CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc4,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
-      CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc4,
-                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      for (auto k : {k_heavy_partial_tc4<false>, k_heavy_partial_tc4<true>}) {
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
       hinit = true;
     }
     const int threads = L::NT * L::RPC;
-    k_heavy_partial_tc4<<<std::min(p.n_slices, 4 * kNumSMs), 128, TcLay4::BYTES, st>>>(p, fmap,
-                                                                                     use_tma);
+    const int hg = std::min(p.n_slices, 4 * kNumSMs);
+    if (unit)
+      k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
+    else
+      k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
     LAUNCH_CHECK(s);
     k_heavy_solve<128, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);

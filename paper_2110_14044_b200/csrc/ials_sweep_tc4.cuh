@@ -103,11 +103,13 @@ IALS_DEVI void tc4_init(const SweepParams& p, uint32_t row_addr, int tid) {
 // predictions yhat[pos] are fetched 2 chunks ahead.  cp.async group g (one
 // per iteration) = {X(g+2), yhat(g+2), meta(g+4)}, so waiting for group c-2
 // at iteration c delivers X(c) and the metadata X(c+2) needs.
+template <bool UNIT>
 IALS_DEVI void tc4_meta(const SweepParams& p, char* smem, int ebeg, int eend, int c, int tid) {
   using L = TcLay4;
   const int e = ebeg + c * L::KC + (tid & 15);
   const int slot = (c & (L::MR - 1)) * L::KC + (tid & 15);
   if (e >= eend) return;
+  if (UNIT && tid >= 32) return;   // all weights and labels are one: not staged
   switch (tid >> 4) {
     case 0: cp_async4(smem + L::OFF_MC + 4 * slot, p.side.cols + e); break;
     case 1: if (p.side.pos) cp_async4(smem + L::OFF_MP + 4 * slot, p.side.pos + e);
@@ -161,6 +163,9 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, const Tc4State& st, 
     cp_async4(smem + L::OFF_CV + 4 * ((c & 3) * L::KC + tid), p.cache + mp[tid]);
 }
 
+// UNIT: every weight and label is one (the BASELINE configurations), so the
+// residual is yhat - 1 and a h h^T = h h^T.
+template <bool UNIT>
 IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, double& gacc, int ebeg,
                              int eend, int tid) {
   using L = TcLay4;
@@ -171,7 +176,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
   uint32_t pend = 0;   // bit x: bar[x] has an outstanding commit
   if (nch == 0) return 0;
   // prologue: metadata of chunks 0..3, then X / yhat of chunks 0 and 1
-  for (int c = 0; c < 4 && c < nch; ++c) tc4_meta(p, smem, ebeg, eend, c, tid);
+  for (int c = 0; c < 4 && c < nch; ++c) tc4_meta<UNIT>(p, smem, ebeg, eend, c, tid);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
@@ -208,22 +213,27 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
       float g[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int k4 = 0; k4 < 4; ++k4) {
-        const float4 w4 = reinterpret_cast<const float4*>(mw)[k4];
         const float4 c4 = reinterpret_cast<const float4*>(cv)[k4];
-        const float4 y4 = reinterpret_cast<const float4*>(my)[k4];
-        const float w[4] = {w4.x, w4.y, w4.z, w4.w}, cc[4] = {c4.x, c4.y, c4.z, c4.w},
-                    yy[4] = {y4.x, y4.y, y4.z, y4.w};
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+        float w[4] = {1.f, 1.f, 1.f, 1.f}, yy[4] = {1.f, 1.f, 1.f, 1.f};
+        if (!UNIT) {
+          const float4 w4 = reinterpret_cast<const float4*>(mw)[k4];
+          const float4 y4 = reinterpret_cast<const float4*>(my)[k4];
+          w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+          yy[0] = y4.x; yy[1] = y4.y; yy[2] = y4.z; yy[3] = y4.w;
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int k = 4 * k4 + j;
           wk[k] = w[j];
-          const float r = (k < nk) ? w[j] * (cc[j] - yy[j]) : 0.f;
+          // (stale ring slots past nk may hold anything: select, do not multiply)
+          const float r = (k < nk) ? (UNIT ? cc[j] - 1.f : w[j] * (cc[j] - yy[j])) : 0.f;
           g[j] = fmaf(r, x[k], g[j]);
         }
       }
       gacc += ((double)g[0] + (double)g[1]) + ((double)g[2] + (double)g[3]);
     }
-    if (p.side.weights) {  // a h h^T = (sqrt(a) h)(sqrt(a) h)^T
+    if (!UNIT && p.side.weights) {  // a h h^T = (sqrt(a) h)(sqrt(a) h)^T
 #pragma unroll
       for (int k = 0; k < 16; ++k) x[k] *= (k < nk) ? sqrtf(wk[k]) : 0.f;
     }
@@ -272,7 +282,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
     // X / yhat of chunk c+2 (its staging buffer was consumed above), and the
     // metadata of chunk c+4
     if (c + 2 < nch) tc4_gather(p, smem, st, ebeg, eend, c + 2, tid);
-    if (c + 4 < nch) tc4_meta(p, smem, ebeg, eend, c + 4, tid);
+    if (c + 4 < nch) tc4_meta<UNIT>(p, smem, ebeg, eend, c + 4, tid);
     cp_async_commit();
   }
   cp_async_wait<0>();
@@ -541,6 +551,7 @@ IALS_DEVI void tc4_backward(const SweepParams& p, char* smem, int tid) {
   }
 }
 
+template <bool UNIT>
 __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
                                                           const __grid_constant__ CUtensorMap fmap,
                                                           int use_tma) {
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
     tmem_wait_st();
     tc_fence_before();   // the first chunk's barrier orders these stores before the MMAs
     double gacc = 0.0;
-    const int nch = tc4_accumulate(p, smem, st, gacc, ebeg, eend, tid);
+    const int nch = tc4_accumulate<UNIT>(p, smem, st, gacc, ebeg, eend, tid);
     if (rec) tph[2] = clock64();
     {  // + lam on the diagonal, and the diagonal itself (the cancellation
        // test's reference): lane l of warp w owns column 32w + l, reached with
@@ -666,6 +677,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
 // from zero in TMEM (same pipelined gather / 3xTF32 MMAs as the light rows)
 // and written row-major (the layout k_heavy_solve<128> reads) with its fp64
 // partial gradient; the slices of a row are combined in k_heavy_solve.
+template <bool UNIT>
 __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
                                                           const __grid_constant__ CUtensorMap fmap,
                                                           int use_tma) {
@@ -701,7 +713,7 @@ __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
       tc_fence_before();   // ordered before the MMAs by the first chunk's barrier
     }
     double gacc = 0.0;
-    tc4_accumulate(p, smem, st, gacc, p.slice_begin[sl], p.slice_end[sl], tid);
+    tc4_accumulate<UNIT>(p, smem, st, gacc, p.slice_begin[sl], p.slice_end[sl], tid);
     float* hp = p.hpart + (size_t)sl * 128 * 128 + (size_t)tid * 128;
 #pragma unroll
     for (int c32 = 0; c32 < 4; ++c32) {
