@@ -254,7 +254,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           hi[j] = tf32_rna(x[4 * c + j]);
-          lo[j] = tf32_rna(x[4 * c + j] - hi[j]);
+          lo[j] = x[4 * c + j] - hi[j];   // fed as is: the MMA drops its low 13 bits
         }
         const int o = rb + ((c ^ sw) << 2);
         *reinterpret_cast<float4*>(XTH + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
@@ -439,7 +439,7 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         hi[q] = tf32_rna(l[q]);
-        lo[q] = tf32_rna(l[q] - hi[q]);
+        lo[q] = l[q] - hi[q];
       }
       const int pa = pa_index(i, 0);   // q 0..3 contiguous, q 4..7 at +32
       *reinterpret_cast<float4*>(PAH + pa) = make_float4(hi[0], hi[1], hi[2], hi[3]);
