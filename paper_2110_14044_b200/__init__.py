@@ -10,8 +10,9 @@ from .data import InteractionDataset, SideView
 from .linalg import SingularMatrixError, check_block, gramian, partial_gramian
 from .model import (FactorModel, PredictionCache, SolverConfig, cache_drift, compute_loss,
                     compute_predictions, effective_reg, init_model)
-from .solvers import (BlockPartition, DeviceTrainer, EpochReport, block_update, ialspp_epoch,
-                      iterate_epochs, partition_dims, train)
+from .solvers import (BlockPartition, DeviceTrainer, EpochReport, block_update,
+                      coordinate_update, ials_epoch, ialspp_epoch, icd_epoch, iterate_epochs,
+                      partition_dims, train)
 
 __version__ = "0.1.0"
 
@@ -20,6 +21,6 @@ __all__ = [
     "SingularMatrixError", "check_block", "gramian", "partial_gramian",
     "FactorModel", "PredictionCache", "SolverConfig", "cache_drift", "compute_loss",
     "compute_predictions", "effective_reg", "init_model",
-    "BlockPartition", "DeviceTrainer", "EpochReport", "block_update", "ialspp_epoch",
-    "iterate_epochs", "partition_dims", "train",
+    "BlockPartition", "DeviceTrainer", "EpochReport", "block_update", "coordinate_update",
+    "ials_epoch", "ialspp_epoch", "icd_epoch", "iterate_epochs", "partition_dims", "train",
 ]

@@ -497,9 +497,10 @@ IALS_DEVI void tc4_block_inverses(const SweepParams& p, char* smem, int tid) {
     const int gm = c0 + m;
     float t = (m == q) ? 1.f : 0.f;
     const float* lr = Lp + gm * (gm + 1) / 2 + c0;
+    // x[k] = 0 for k < q, so those terms add exactly nothing; rows >= b read
+    // unwritten packed rows, but their x is selected to zero below
 #pragma unroll
-    for (int k = 0; k < m; ++k)
-      if (k >= q && gm < p.b) t = fmaf(-lr[k], x[k], t);
+    for (int k = 0; k < m; ++k) t = fmaf(-lr[k], x[k], t);
     x[m] = (m >= q && gm < p.b) ? t * invd[gm] : 0.f;
   }
 #pragma unroll

@@ -251,6 +251,40 @@ def ialspp_epoch(model: FactorModel, data, cache: PredictionCache, config: Solve
     return rep
 
 
+def ials_epoch(model: FactorModel, data, config: SolverConfig, epoch_index: int = 0,
+               device=None) -> EpochReport:
+    """Full-vector epoch (solvers.py:275-300): an exact user pass, then an
+    exact item pass.  On the device this is the block sweep with one block of
+    width d: a Newton step from an exact cache solves the row's quadratic in
+    closed form, so it equals the reference's direct solve (pinned by the
+    reference's own equivalence test, test_solvers.py:125-149).  The cache
+    is internal and discarded, as in the reference."""
+    if model.dim > 256:
+        raise ValueError("ials_epoch on the device supports dim <= 256 (block width of the sweep)")
+    cache = PredictionCache(np.zeros(data.n_interactions))
+    return ialspp_epoch(model, data, cache, config, partition_dims(model.dim, model.dim),
+                        epoch_index, device)
+
+
+def icd_epoch(model: FactorModel, data, cache: PredictionCache, config: SolverConfig,
+              epoch_index: int = 0, device=None) -> EpochReport:
+    """Coordinate epoch (solvers.py:303-337): per dimension a user and an item
+    pass with the cache maintained; the block sweep with width 1."""
+    return ialspp_epoch(model, data, cache, config, partition_dims(model.dim, 1), epoch_index,
+                        device)
+
+
+def coordinate_update(model: FactorModel, data, cache: PredictionCache, config: SolverConfig,
+                      dim_index: int, side="user", device=None):
+    """One scalar-coordinate pass over one side (solvers.py:255-272)."""
+    f = int(dim_index)
+    if not 0 <= f < model.dim:
+        raise ValueError("dim_index out of range")
+    if side not in ("user", "item"):
+        raise ValueError("side must be 'user' or 'item'")
+    block_update(model, data, cache, config, np.array([f]), side, device)
+
+
 def _solver_partition(config: SolverConfig):
     if config.solver == "ials":
         return partition_dims(config.dim, config.dim)

@@ -257,3 +257,30 @@ def test_sharded_path_gpu_ops_single_rank(ials):
     ref_cache = orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
     assert relf(W.double().cpu().numpy(), w) < TOL and relf(H.double().cpu().numpy(), h) < TOL
     assert relmax(cache, ref_cache) < TOL
+
+
+@pytest.mark.parametrize("which", ["ials", "icd"])
+def test_dedicated_solver_entry_points(ials, which):
+    """ials_epoch / icd_epoch (solvers.py:275-337) run the block sweep with
+    b = d / b = 1; one epoch of each vs the f64 oracle at that block width."""
+    from oracle import ialspp_oracle as orc
+    rng = np.random.default_rng(21)
+    U, I, n, d = 400, 150, 6000, 24
+    users = rng.integers(0, U, n)
+    items = np.minimum(rng.zipf(1.3, n) - 1, I - 1)
+    data = ials.InteractionDataset(U, I, users, items)
+    cfg = ials.SolverConfig(dim=d, block_size=8, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=1, seed=2)
+    m = ials.init_model(cfg, U, I)
+    m.user_factors[:] = m.user_factors.astype(np.float32)
+    m.item_factors[:] = m.item_factors.astype(np.float32)
+    w, h = m.user_factors.copy(), m.item_factors.copy()
+    if which == "ials":
+        ials.ials_epoch(m, data, cfg)
+        bw = d
+    else:
+        cache = ials.PredictionCache(np.zeros(n))
+        ials.icd_epoch(m, data, cache, cfg)
+        bw = 1
+    orc.train(w, h, orc.build_csr(U, I, users, items), 0.1, 1e-3, 1.0, bw, 1)
+    assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL
