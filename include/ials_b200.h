@@ -15,6 +15,7 @@
  *   ials_loss_terms        <- compute_loss          model.py:168-188 (device reductions)
  *   ials_build_csr         <- InteractionDataset.__init__ + user_view / item_view
  *                             data.py:98-134,148-162 (device stable radix sorts)
+ *   ials_topk              <- top_k_from_scores     metrics.py:31-57 (fold-in evaluation)
  *
  * Conventions
  *   - All array arguments are DEVICE pointers (memory owned by the caller,
@@ -234,6 +235,16 @@ int ials_build_csr(ials_session* s, int32_t U, int32_t I, int64_t n, const int32
                    const int32_t* items, int32_t* user_ptr, int32_t* user_cols, int32_t* order,
                    int32_t* item_ptr, int32_t* item_cols, int32_t* item_pos, void* workspace,
                    size_t ws_bytes, void* stream);
+
+/* Ranking (top_k_from_scores, metrics.py:31-57) of n_rows score rows
+ * scores[r * lds + c], c < n_cols.  If ex_ptr / ex_cols (a CSR over the rows)
+ * are given, those entries are first set to -inf IN PLACE.  out (n_rows x k)
+ * receives each row's k largest finite scores' column indices, ties by
+ * ascending index, padded with -1 when fewer than k finite scores remain;
+ * counts[r] = the number returned.  1 <= k <= 1024. */
+int ials_topk(ials_session* s, int32_t n_rows, int32_t n_cols, float* scores, int64_t lds,
+              const int32_t* ex_ptr, const int32_t* ex_cols, int32_t k, int32_t* out,
+              int32_t* counts, void* stream);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ __all__ = [
     "SingularRow", "build_csr", "effective_reg", "init_factors", "partition",
     "predictions", "gramian", "partial_gramian", "side_pass", "ialspp_epoch",
     "train", "loss", "cache_drift", "systematic_rows",
+    "fold_in", "top_k", "recall_at_k", "ndcg_at_k", "evaluate",
 ]
 
 _ROW_BATCH_ELEMS = 1 << 21     # gathered (rows x degree x block) elements per batch
@@ -303,3 +304,71 @@ def systematic_rows(counts, stride, run=64):
     starts = np.arange(0, rest.size, stride * run)
     tail = np.concatenate([rest[s:s + run] for s in starts]) if starts.size else rest[:0]
     return np.sort(head), np.sort(tail)
+
+
+# ----------------------------------------------------------- fold-in / ranking
+# (pinned by tests/golden/eval.npz from the reference)
+
+def fold_in(item_factors, histories, alpha0, reg, exponent):
+    """Exact least-squares embedding per history (project_user / fold_in_users,
+    solvers.py:416-466): (sum a h h' + alpha0 G + lam I)^-1 sum a y h with
+    lam = reg (n + alpha0 I)^exponent; an empty history gives zeros."""
+    hf = np.asarray(item_factors, dtype=np.float64)
+    n_items, d = hf.shape
+    g = hf.T @ hf
+    out = np.zeros((len(histories), d))
+    for r, (its, lbl, wts) in enumerate(histories):
+        its = np.asarray(its, dtype=np.int64)
+        n = its.size
+        lbl = np.ones(n) if lbl is None else np.asarray(lbl, dtype=np.float64)
+        wts = np.ones(n) if wts is None else np.asarray(wts, dtype=np.float64)
+        rows = hf[its]
+        hess = rows.T @ (rows * wts[:, None]) + alpha0 * g
+        hess[np.arange(d), np.arange(d)] += reg * (n + alpha0 * n_items) ** exponent
+        out[r] = np.linalg.solve(hess, rows.T @ (wts * lbl))
+    return out
+
+
+def top_k(scores, k, exclude=None):
+    """Indices of the k largest scores, ties by ascending index, excluded and
+    non-finite scores never returned (top_k_from_scores, metrics.py:31-57)."""
+    s = np.asarray(scores, dtype=np.float64).copy()
+    if exclude is not None and len(exclude):
+        s[np.asarray(exclude, dtype=np.intp)] = -np.inf
+    cand = np.flatnonzero(np.isfinite(s))
+    order = np.lexsort((cand, -s[cand]))
+    return cand[order][:min(int(k), cand.size)]
+
+
+def recall_at_k(topk, targets, k):
+    """Hits among the first k over min(k, |targets|) (metrics.py:66-72)."""
+    t = set(np.asarray(targets).tolist())
+    hits = sum(1 for i in list(topk)[:k] if i in t)
+    return hits / min(k, len(t))
+
+
+def ndcg_at_k(topk, targets, k):
+    """Binary-relevance NDCG truncated at k (metrics.py:75-92)."""
+    t = set(np.asarray(targets).tolist())
+    dcg = sum(1.0 / math.log2(p + 1) for p, i in enumerate(list(topk)[:k], start=1) if i in t)
+    ideal = sum(1.0 / math.log2(p + 1) for p in range(1, min(k, len(t)) + 1))
+    return dcg / ideal
+
+
+def evaluate(item_factors, folds, alpha0, reg, exponent, recall_ks, ndcg_ks):
+    """evaluate_holdout (metrics.py:95-119) over (input_items, labels, weights,
+    target_items) tuples; returns ({k: recall}, {k: ndcg}, n_evaluated)."""
+    ev = [f for f in folds if len(f[3]) > 0]
+    emb = fold_in(item_factors, [(f[0], f[1], f[2]) for f in ev], alpha0, reg, exponent)
+    hf = np.asarray(item_factors, dtype=np.float64)
+    kmax = max(list(recall_ks) + list(ndcg_ks))
+    rs = {k: 0.0 for k in recall_ks}
+    ns = {k: 0.0 for k in ndcg_ks}
+    for r, f in enumerate(ev):
+        tk = top_k(hf @ emb[r], kmax, exclude=f[0])
+        for k in recall_ks:
+            rs[k] += recall_at_k(tk, f[3], k)
+        for k in ndcg_ks:
+            ns[k] += ndcg_at_k(tk, f[3], k)
+    n = len(ev)
+    return {k: v / n for k, v in rs.items()}, {k: v / n for k, v in ns.items()}, n

@@ -7,6 +7,8 @@ of ``libials_b200.so`` (``include/ials_b200.h``); there is no CPU fallback.
 """
 
 from .data import InteractionDataset, SideView
+from .evaluation import (MetricReport, evaluate_holdout, fold_in_users, ndcg_at_k, project_user,
+                         rank_items, recall_at_k, top_k_from_scores)
 from .linalg import SingularMatrixError, check_block, gramian, partial_gramian
 from .model import (FactorModel, PredictionCache, SolverConfig, cache_drift, compute_loss,
                     compute_predictions, effective_reg, init_model)
@@ -18,6 +20,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "InteractionDataset", "SideView",
+    "MetricReport", "evaluate_holdout", "fold_in_users", "ndcg_at_k", "project_user",
+    "rank_items", "recall_at_k", "top_k_from_scores",
     "SingularMatrixError", "check_block", "gramian", "partial_gramian",
     "FactorModel", "PredictionCache", "SolverConfig", "cache_drift", "compute_loss",
     "compute_predictions", "effective_reg", "init_model",

@@ -77,6 +77,7 @@ SIGNATURES = {
     "ials_loss_workspace_bytes": (c_sz, [c_i32]),
     "ials_build_csr_workspace_bytes": (c_sz, [c_i64]),
     "ials_launch_count": (c_i64, []),
+    "ials_topk": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
     "ials_build_csr": (c_i32, [c_p, c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                                c_p, c_sz, c_p]),
     "ials_loss_terms": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSide), c_p,

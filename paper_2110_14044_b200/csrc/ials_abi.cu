@@ -16,6 +16,7 @@
 #include "ials_common.cuh"
 #include "ials_dense.cuh"
 #include "ials_csr.cuh"
+#include "ials_topk.cuh"
 #include "ials_sweep.cuh"
 #include "ials_loss.cuh"
 #include "ials_sweep_tc.cuh"
@@ -1119,6 +1120,26 @@ int ials_build_csr(ials_session* s, int32_t U, int32_t I, int64_t n, const int32
   k_row_ptr<<<gp, 256, 0, st>>>(si, n, I, item_ptr);
   LAUNCH_CHECK(s);
   k_gather_i32<<<g, 256, 0, st>>>(su, item_pos, n, item_cols);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+// ------------------------------------------------------------------ ranking
+int ials_topk(ials_session* s, int32_t n_rows, int32_t n_cols, float* scores, int64_t lds,
+              const int32_t* ex_ptr, const int32_t* ex_cols, int32_t k, int32_t* out,
+              int32_t* counts, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (n_rows < 0 || n_cols < 0 || lds < n_cols || k < 1 || k > kTopkMax)
+    return fail(s, IALS_E_INVALID, "topk: bad sizes (rows=%d cols=%d k=%d, k <= %d)", n_rows, n_cols,
+                k, kTopkMax);
+  if (n_rows == 0) return IALS_OK;
+  if (!scores || !out || !counts) return fail(s, IALS_E_INVALID, "topk: NULL argument");
+  cudaStream_t st = S(stream);
+  if (ex_ptr && ex_cols) {
+    k_topk_exclude<<<n_rows, 256, 0, st>>>(scores, lds, ex_ptr, ex_cols);
+    LAUNCH_CHECK(s);
+  }
+  k_topk<<<n_rows, kTopkThreads, 0, st>>>(scores, lds, n_cols, k, out, counts);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }

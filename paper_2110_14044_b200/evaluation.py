@@ -1,0 +1,216 @@
+"""Fold-in and ranking evaluation on the device.
+
+Host mirror of the reference's ``project_user`` / ``fold_in_users``
+(/root/reference/pkg/src/blockals/solvers.py:416-466) and ``metrics.py``
+(``top_k_from_scores``, ``rank_items``, ``recall_at_k``, ``ndcg_at_k``,
+``evaluate_holdout``, metrics.py:31-119), same names, arguments and errors.
+
+* Fold-in solves, per history, the same regularized least squares as a user
+  pass.  On the device that is one user pass of the block sweep with a single
+  block of width d from a zero embedding and a zero cache: the Newton step
+  from w = 0 is the closed-form solve.  Block widths go up to 256, so the
+  device fold-in covers d <= 256.
+* Scores are a plain FP32 GEMM (cuBLAS through torch.matmul: allowed as a
+  library GEMM); the exclusion of each user's input items and the top-k with
+  the reference's tie order run in ``ials_topk`` (csrc/ials_topk.cuh).
+* recall / NDCG are the reference's set arithmetic on the top-k lists.
+* k above 1024 (the kernel's selection buffer) uses a stable device sort of
+  the row instead (torch.sort), with the same order.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._runtime import default_engine_session
+from .data import InteractionDataset
+from .engine import _ptr, current_stream_handle
+from .model import FactorModel, PredictionCache, SolverConfig
+from .solvers import block_update
+
+__all__ = ["MetricReport", "project_user", "fold_in_users", "top_k_from_scores", "rank_items",
+           "recall_at_k", "ndcg_at_k", "evaluate_holdout"]
+
+_MAX_FOLD_DIM = 256
+_MAX_K = 1024
+
+
+@dataclass
+class MetricReport:
+    """Per-k metric means over the evaluated user set."""
+
+    recall_at: dict
+    ndcg_at: dict
+    num_users_evaluated: int
+
+
+def fold_in_users(item_factors, histories, config: SolverConfig, device=None) -> np.ndarray:
+    """Embeddings for a batch of histories, one per (items, labels, weights)
+    (labels / weights may be None); shape (len(histories), dim)."""
+    if config is None:
+        raise ValueError("config is required")
+    hf = np.ascontiguousarray(item_factors, dtype=np.float64)
+    n_items, d = hf.shape
+    if d > _MAX_FOLD_DIM:
+        raise ValueError(f"device fold-in supports dim <= {_MAX_FOLD_DIM}")
+    users, items, labels, weights = [], [], [], []
+    for row, (its, lbl, wts) in enumerate(histories):
+        its = np.asarray(its, dtype=np.int64)
+        users.append(np.full(its.size, row, dtype=np.int64))
+        items.append(its)
+        labels.append(np.ones(its.size) if lbl is None else np.asarray(lbl, dtype=np.float64))
+        weights.append(np.ones(its.size) if wts is None else np.asarray(wts, dtype=np.float64))
+    out = np.zeros((len(histories), d))
+    if not histories or not sum(a.size for a in items):
+        return out   # empty histories: the right-hand side is zero
+    data = InteractionDataset(len(histories), n_items, np.concatenate(users), np.concatenate(items),
+                              np.concatenate(labels), np.concatenate(weights))
+    model = FactorModel(out, hf)
+    cache = PredictionCache.zeros(data.n_interactions)   # exact for the zero embedding
+    block_update(model, data, cache, config.with_(dim=d, block_size=d), np.arange(d), "user",
+                 device)
+    return model.user_factors
+
+
+def project_user(item_factors, items, labels=None, weights=None,
+                 config: SolverConfig | None = None, item_gram=None, device=None) -> np.ndarray:
+    """Embedding for a single interaction history against fixed item factors
+    (``item_gram`` is accepted for signature parity; the device forms its own)."""
+    if config is None:
+        raise ValueError("config is required")
+    return fold_in_users(item_factors, [(items, labels, weights)], config, device)[0]
+
+
+def _topk_device(scores: torch.Tensor, k: int, ex_ptr=None, ex_cols=None) -> list:
+    """Rows of a device score matrix -> top-k index lists (ials_topk)."""
+    rt = default_engine_session(scores.device)
+    n_rows, n_cols = scores.shape
+    out = torch.empty((max(n_rows, 1), k), dtype=torch.int32, device=scores.device)
+    counts = torch.empty(max(n_rows, 1), dtype=torch.int32, device=scores.device)
+    rc = rt.lib.ials_topk(rt.session.handle, n_rows, n_cols, _ptr(scores), scores.stride(0),
+                          _ptr(ex_ptr), _ptr(ex_cols), k, _ptr(out), _ptr(counts),
+                          current_stream_handle(scores.device))
+    rt.session.check(rc, "topk")
+    o, c = out.cpu().numpy(), counts.cpu().numpy()
+    return [o[r, :c[r]].astype(np.int64) for r in range(n_rows)]
+
+
+def _exclusion_csr(exclude, device):
+    if exclude is None:
+        return None, None
+    ex = np.asarray(list(exclude) if not isinstance(exclude, np.ndarray) else exclude, dtype=np.int64)
+    if not ex.size:
+        return None, None
+    return (torch.tensor([0, ex.size], dtype=torch.int32, device=device),
+            torch.from_numpy(ex.astype(np.int32)).to(device))
+
+
+def _top_k_row(scores: torch.Tensor, k, exclude) -> np.ndarray:
+    if k < 1:
+        raise ValueError("k must be positive")
+    kk = int(min(k, max(scores.numel(), 1)))
+    if kk > _MAX_K:
+        # beyond the in-kernel selection buffer: a full stable sort of the row
+        # on the device (descending; equal scores keep ascending index order)
+        s = scores.reshape(-1).clone()
+        ex = _exclusion_csr(exclude, scores.device)[1]
+        if ex is not None:
+            s[ex.long()] = -float("inf")
+        s = torch.where(torch.isfinite(s), s + 0.0, torch.full_like(s, -float("inf")))
+        pool = int(torch.isfinite(s).sum())
+        order = torch.sort(s, descending=True, stable=True).indices
+        return order[:min(kk, pool)].cpu().numpy().astype(np.int64)
+    ptr, cols = _exclusion_csr(exclude, scores.device)
+    return _topk_device(scores.reshape(1, -1).contiguous(), kk, ptr, cols)[0]
+
+
+def top_k_from_scores(scores, k, exclude=None, device=None) -> np.ndarray:
+    """Indices of the k largest scores, ties broken by ascending index;
+    excluded indices and non-finite scores never appear."""
+    if k < 1:
+        raise ValueError("k must be positive")
+    rt = default_engine_session(device)
+    s = torch.from_numpy(np.asarray(scores, dtype=np.float64).astype(np.float32)).to(rt.device)
+    return _top_k_row(s, k, exclude)
+
+
+def rank_items(user_embedding, item_factors, exclude=None, k=10, device=None) -> np.ndarray:
+    """Top-k item indices for a user embedding, excluding ``exclude``."""
+    rt = default_engine_session(device)
+    h = torch.from_numpy(np.ascontiguousarray(item_factors, dtype=np.float32)).to(rt.device)
+    e = torch.from_numpy(np.asarray(user_embedding, dtype=np.float32)).to(rt.device)
+    return _top_k_row(h @ e, k, exclude)
+
+
+def recall_at_k(topk, targets, k) -> float:
+    """Hits among the first k over ``min(k, |targets|)``."""
+    targets = set(np.asarray(targets).tolist())
+    if not targets:
+        raise ValueError("targets must be nonempty")
+    hits = sum(1 for item in list(topk)[:k] if item in targets)
+    return hits / min(k, len(targets))
+
+
+def ndcg_at_k(topk, targets, k) -> float:
+    """Truncated NDCG with binary relevance (ideal DCG puts all targets first)."""
+    targets = set(np.asarray(targets).tolist())
+    if not targets:
+        raise ValueError("targets must be nonempty")
+    dcg = sum(1.0 / math.log2(p + 1) for p, item in enumerate(list(topk)[:k], start=1)
+              if item in targets)
+    ideal = sum(1.0 / math.log2(p + 1) for p in range(1, min(k, len(targets)) + 1))
+    return dcg / ideal
+
+
+def evaluate_holdout(item_factors, split, config, recall_ks=(20, 50), ndcg_ks=(100,),
+                     device=None, users_per_batch=None) -> MetricReport:
+    """Fold in every held-out user, rank unseen items, average the metrics.
+    Users with an empty target fold are skipped; input-fold items are
+    excluded from each user's candidates.  ``split`` is a HoldoutSplit-like
+    object with ``folds`` or a list of folds (``input_items``,
+    ``input_labels``, ``input_weights``, ``target_items``)."""
+    if not recall_ks and not ndcg_ks:
+        raise ValueError("at least one k is required")
+    folds = split.folds if hasattr(split, "folds") else list(split)
+    evaluated = [f for f in folds if np.asarray(f.target_items).size > 0]
+    if not evaluated:
+        raise ValueError("no holdout users with target interactions")
+    k_max = max(list(recall_ks) + list(ndcg_ks))
+    if k_max > _MAX_K:
+        raise ValueError(f"device top-k supports k <= {_MAX_K}")
+    emb = fold_in_users(item_factors, [(f.input_items, f.input_labels, f.input_weights)
+                                       for f in evaluated], config, device)
+    rt = default_engine_session(device)
+    dev = rt.device
+    H = torch.from_numpy(np.ascontiguousarray(item_factors, dtype=np.float32)).to(dev)
+    n_items = H.shape[0]
+    E = torch.from_numpy(emb.astype(np.float32)).to(dev)
+    ex = [np.asarray(f.input_items, dtype=np.int64) for f in evaluated]
+    ex_ptr = np.zeros(len(ex) + 1, dtype=np.int64)
+    ex_ptr[1:] = np.cumsum([a.size for a in ex])
+    ex_cols = torch.from_numpy(np.concatenate(ex).astype(np.int32) if ex_ptr[-1] else
+                               np.zeros(1, np.int32)).to(dev)
+    if users_per_batch is None:   # score matrices of at most ~1 GB
+        users_per_batch = max(1, (1 << 28) // max(n_items, 1))
+    recall_sums = {k: 0.0 for k in recall_ks}
+    ndcg_sums = {k: 0.0 for k in ndcg_ks}
+    k_run = min(k_max, n_items)
+    for r0 in range(0, len(evaluated), users_per_batch):
+        r1 = min(len(evaluated), r0 + users_per_batch)
+        scores = (E[r0:r1] @ H.T).contiguous()
+        ptr = torch.from_numpy((ex_ptr[r0:r1 + 1] - ex_ptr[r0]).astype(np.int32)).to(dev)
+        cols = ex_cols[int(ex_ptr[r0]):] if ex_ptr[r1] > ex_ptr[r0] else ex_cols
+        tops = _topk_device(scores, k_run, ptr, cols)
+        for r in range(r0, r1):
+            topk, targets = tops[r - r0], evaluated[r].target_items
+            for k in recall_ks:
+                recall_sums[k] += recall_at_k(topk, targets, k)
+            for k in ndcg_ks:
+                ndcg_sums[k] += ndcg_at_k(topk, targets, k)
+    n = len(evaluated)
+    return MetricReport({k: v / n for k, v in recall_sums.items()},
+                        {k: v / n for k, v in ndcg_sums.items()}, n)

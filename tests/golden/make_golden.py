@@ -18,6 +18,12 @@ set of inputs, what the reference's own public API returns:
   weights, remainder blocks, b=1 and b=d, a non-contiguous partition), each
   with the state after one and after three epochs.
 
+* ``eval.npz`` -- fold-in and ranking: a holdout split
+  of the tiny data (``split_holdout``), three epochs of ``train`` on its
+  training part, then ``fold_in_users`` embeddings of the evaluated folds,
+  ``rank_items`` top-100 lists, ``evaluate_holdout`` metrics, and
+  ``top_k_from_scores`` on tie-heavy score vectors with exclusions.
+
 The COO inputs are stored too, so the fixtures are self-contained.
 """
 
@@ -179,6 +185,59 @@ def make_small():
     print("small: %d cases" % len(SMALL_CASES))
 
 
+def _ragged(arrays, dtype):
+    ptr = np.zeros(len(arrays) + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([len(a) for a in arrays])
+    flat = np.concatenate([np.asarray(a, dtype=dtype) for a in arrays]) if arrays else np.empty(0, dtype)
+    return ptr, flat
+
+
+def make_eval():
+    from blockals import metrics as refm
+    from blockals.pipeline import split_holdout
+    U, I, users, items = synthetic.generate("tiny", 0)
+    data = ref.InteractionDataset(U, I, users, items)
+    split = split_holdout(data, 0.1, seed=0)
+    cfg = ref.SolverConfig(dim=32, block_size=8, unobserved_weight=0.1, reg=1e-3,
+                           reg_exponent=1.0, init_stddev=0.1, epochs=3, seed=0, threads=1)
+    model = fp32_init(cfg, split.train.num_users, I)
+    ref.train(model, split.train, cfg)
+    hf = model.item_factors.astype(np.float32).astype(np.float64)   # what the GPU side holds
+    evaluated = [f for f in split.folds if f.target_items.size > 0]
+    emb = ref.fold_in_users(hf, [(f.input_items, f.input_labels, f.input_weights) for f in evaluated], cfg)
+    topk = [refm.rank_items(emb[r], hf, exclude=f.input_items, k=100) for r, f in enumerate(evaluated)]
+    rep = refm.evaluate_holdout(hf, split, cfg, recall_ks=(20, 50), ndcg_ks=(10, 100))
+    out = {"item_factors": hf, "num_items": I, "embeddings": emb}
+    out["in_ptr"], out["in_items"] = _ragged([f.input_items for f in split.folds], np.int64)
+    out["tg_ptr"], out["tg_items"] = _ragged([f.target_items for f in split.folds], np.int64)
+    out["topk_ptr"], out["topk"] = _ragged(topk, np.int64)
+    out["recall_20"], out["recall_50"] = rep.recall_at[20], rep.recall_at[50]
+    out["ndcg_10"], out["ndcg_100"] = rep.ndcg_at[10], rep.ndcg_at[100]
+    out["n_evaluated"] = rep.num_users_evaluated
+    # top_k_from_scores on tie-heavy integer scores, with exclusions
+    rng = np.random.default_rng(5)
+    sc, ex, tk, ks = [], [], [], []
+    for case in range(12):
+        n = int(rng.integers(1, 3000))
+        s = rng.integers(-20, 20, n).astype(np.float64)
+        e = rng.choice(n, int(rng.integers(0, n // 2 + 1)), replace=False) if case % 3 else np.empty(0, np.int64)
+        k = int(rng.integers(1, 400)) if case != 5 else n + 10   # k beyond the pool
+        sc.append(s); ex.append(e); ks.append(k)
+        tk.append(refm.top_k_from_scores(s, k, exclude=e))
+    out["tk_sptr"], out["tk_scores"] = _ragged(sc, np.float64)
+    out["tk_eptr"], out["tk_exclude"] = _ragged(ex, np.int64)
+    out["tk_optr"], out["tk_out"] = _ragged(tk, np.int64)
+    out["tk_k"] = np.array(ks, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "eval.npz"), **out)
+    print("eval: %d folds, %d evaluated, recall@20 %.4f ndcg@100 %.4f" %
+          (len(split.folds), rep.num_users_evaluated, rep.recall_at[20], rep.ndcg_at[100]))
+
+
 if __name__ == "__main__":
-    make_tiny()
-    make_small()
+    which = sys.argv[1:] or ["tiny", "small", "eval"]
+    if "tiny" in which:
+        make_tiny()
+    if "small" in which:
+        make_small()
+    if "eval" in which:
+        make_eval()

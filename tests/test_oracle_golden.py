@@ -111,3 +111,37 @@ def test_singular_row_named():
     with pytest.raises(orc.SingularRow) as err:
         orc.side_pass(*orc.side_view(csr, "user"), h, w, cache, blk, orc.partial_gramian(h, blk), 0.0, lu)
     assert err.value.row == 1 and err.value.pivot == 0
+
+
+# ------------------------------------------------ fold-in / ranking (8f rank 3)
+def _rag(ptr, flat, i):
+    return flat[ptr[i]:ptr[i + 1]]
+
+
+def test_oracle_fold_in_and_ranking_match_reference():
+    from conftest import load_golden
+    from oracle import ialspp_oracle as orc
+    g = load_golden("eval")
+    nf = g["in_ptr"].size - 1
+    folds = [(_rag(g["in_ptr"], g["in_items"], i), None, None, _rag(g["tg_ptr"], g["tg_items"], i))
+             for i in range(nf)]
+    ev = [f for f in folds if len(f[3]) > 0]
+    emb = orc.fold_in(g["item_factors"], [(f[0], None, None) for f in ev], 0.1, 1e-3, 1.0)
+    assert np.abs(emb - g["embeddings"]).max() <= 1e-9 * np.abs(g["embeddings"]).max()
+    for r, f in enumerate(ev):
+        tk = orc.top_k(g["item_factors"] @ g["embeddings"][r], 100, exclude=f[0])
+        assert np.array_equal(tk, _rag(g["topk_ptr"], g["topk"], r))
+    rec, ndcg, n = orc.evaluate(g["item_factors"], folds, 0.1, 1e-3, 1.0, (20, 50), (10, 100))
+    assert n == int(g["n_evaluated"])
+    assert abs(rec[20] - float(g["recall_20"])) < 1e-12 and abs(rec[50] - float(g["recall_50"])) < 1e-12
+    assert abs(ndcg[10] - float(g["ndcg_10"])) < 1e-12 and abs(ndcg[100] - float(g["ndcg_100"])) < 1e-12
+
+
+def test_oracle_top_k_ties_and_exclusion_match_reference():
+    from conftest import load_golden
+    from oracle import ialspp_oracle as orc
+    g = load_golden("eval")
+    for c in range(g["tk_k"].size):
+        s = _rag(g["tk_sptr"], g["tk_scores"], c)
+        e = _rag(g["tk_eptr"], g["tk_exclude"], c)
+        assert np.array_equal(orc.top_k(s, int(g["tk_k"][c]), e), _rag(g["tk_optr"], g["tk_out"], c))
