@@ -62,6 +62,8 @@ typedef struct ials_side {
   const float* weights;    /* [nnz] alpha, or NULL                      */
   const int32_t* pos;      /* [nnz] cache slot, or NULL                 */
   const float* lam;        /* [n_rows] effective_reg (model.py:144-150) */
+  const int32_t* rows;     /* [nnz] row of each entry, or NULL (enables the
+                              entry-parallel cache pass of the fused sweep) */
 } ials_side;
 
 /* Work schedule of one side for one block width (built once per dataset by

@@ -26,7 +26,8 @@ c_i32, c_i64, c_p, c_sz, c_f = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, 
 class IalsSide(ctypes.Structure):
     """``ials_side`` (one SideView on the device, data.py:26-52)."""
     _fields_ = [("n_rows", c_i32), ("n_fixed", c_i32), ("nnz", c_i64), ("ptr", c_p),
-                ("cols", c_p), ("labels", c_p), ("weights", c_p), ("pos", c_p), ("lam", c_p)]
+                ("cols", c_p), ("labels", c_p), ("weights", c_p), ("pos", c_p), ("lam", c_p),
+                ("rows", c_p)]
 
 
 class IalsSched(ctypes.Structure):

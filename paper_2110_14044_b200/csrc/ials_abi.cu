@@ -463,7 +463,7 @@ static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, ui
 
 // BT = 128, b > 64: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
 // heavy rows on the SIMT slice kernels.
-static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t st) {
+static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<128>;
   const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
   int rc = set_smem_attrs<128>(s);
@@ -529,7 +529,12 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, cudaStream_t 
     LAUNCH_CHECK(s);
   }
   if (p.n_light + p.n_slices > 0) {
-    k_pass_cache<<<p.n_light + p.n_slices, 256, 0, st>>>(p);
+    if (p.side.rows && nnz > 0) {   // entry-parallel: no per-row setup, full load balance
+      const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);
+      k_pass_cache_flat<<<(int)g, 256, 0, st>>>(p, nnz);
+    } else {
+      k_pass_cache<<<p.n_light + p.n_slices, 256, 0, st>>>(p);
+    }
     LAUNCH_CHECK(s);
   }
   return IALS_OK;
@@ -636,10 +641,10 @@ static int launch_tc_waves(ials_session* s, SweepParams p, const ials_sched* sch
 }
 
 template <int BT>
-static int launch_sweep(ials_session* s, const SweepParams& p, cudaStream_t st) {
+static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<BT>;
   if (BT == 128 && p.b > 32 && tc_enabled()) return launch_sweep_tc128(s, p, st);
-  if (BT == 128 && p.b > 64 && tc4_enabled()) return launch_sweep_tc4(s, p, st);
+  if (BT == 128 && p.b > 64 && tc4_enabled()) return launch_sweep_tc4(s, p, nnz, st);
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
   const int threads = L::NT * L::RPC;
@@ -685,7 +690,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     return fail(s, IALS_E_NOMEM, "side_pass: workspace %zu < %zu bytes", ws_bytes, need);
   SweepParams p{};
   p.side = SideDev{side->n_rows, side->n_fixed, side->ptr, side->cols, side->labels,
-                   side->weights, side->pos, side->lam};
+                   side->weights, side->pos, side->lam, side->rows};
   p.fixed = fixed;
   p.ldf = ldf;
   p.own = own;
@@ -802,12 +807,12 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     return IALS_OK;
   }
   switch (bt) {
-    case 8: return launch_sweep<8>(s, p, st);
-    case 16: return launch_sweep<16>(s, p, st);
-    case 32: return launch_sweep<32>(s, p, st);
-    case 64: return launch_sweep<64>(s, p, st);
-    case 128: return launch_sweep<128>(s, p, st);
-    default: return launch_sweep<256>(s, p, st);
+    case 8: return launch_sweep<8>(s, p, side->nnz, st);
+    case 16: return launch_sweep<16>(s, p, side->nnz, st);
+    case 32: return launch_sweep<32>(s, p, side->nnz, st);
+    case 64: return launch_sweep<64>(s, p, side->nnz, st);
+    case 128: return launch_sweep<128>(s, p, side->nnz, st);
+    default: return launch_sweep<256>(s, p, side->nnz, st);
   }
 }
 

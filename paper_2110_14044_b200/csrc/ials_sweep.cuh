@@ -31,6 +31,7 @@ struct SideDev {
   const float* weights;
   const int* pos;
   const float* lam;
+  const int* rows;   // [nnz] row of each entry, or null
 };
 
 struct SweepParams {
@@ -716,7 +717,10 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   if (GUARD && reinterpret_cast<const int*>(sm + L::OFF_X + BT)[0]) {
     // cancelled pivot: the FP32 SIMT sweep redoes the whole row (its own
     // cache update included), so nothing of this solve is applied
-    if (tid < p.b) p.hdelta[(size_t)h * BT + tid] = 0.f;
+    if (tid < p.b) {
+      p.hdelta[(size_t)h * BT + tid] = 0.f;
+      p.drow[(size_t)row * p.b + tid] = 0.f;
+    }
     if (tid == 0) {
       p.redo_rows[atomicAdd(p.redo_cnt, 1)] = row;
       atomicAdd(p.redo_total, 1ull);
@@ -726,6 +730,7 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   if (tid < p.b) {
     p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
     p.hdelta[(size_t)h * BT + tid] = ds[tid];
+    p.drow[(size_t)row * p.b + tid] = ds[tid];   // the entry-parallel cache pass reads d by row
   }
 }
 

@@ -809,4 +809,75 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
   }
 }
 
+// The same cache update, entry-parallel: every warp takes a contiguous run
+// of the side's entries (storage order), 4 at a time (8 lanes each), and
+// keeps the current row's d (drow[rows[e]]; heavy rows included --
+// k_heavy_solve stores theirs there too -- and d = 0 for rows the SIMT sweep
+// redid) in registers, reloading it only when its entries cross into the
+// next row.  No per-row setup and no row-length imbalance.
+__global__ void __launch_bounds__(256) k_pass_cache_flat(SweepParams p, long long nnz) {
+  const int lane = threadIdx.x & 31, g = lane & 7, sub = lane >> 3;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long per = ((nnz + nwarps - 1) / nwarps + 3) & ~3LL;
+  const long long beg = wid * per, end = min(nnz, beg + per);
+  const int b = p.b;
+  int cur = -1;
+  float dv[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) dv[j] = 0.f;
+  for (long long e0 = beg; e0 < end; e0 += 4) {   // warp-uniform trip count (shuffles below)
+    const long long e = e0 + sub;
+    const bool live = e < end;
+    const int row = live ? __ldg(p.side.rows + e) : cur;
+    const int col = live ? __ldg(p.side.cols + e) : 0;
+    if (row != cur) {
+      const float* dr = p.drow + (size_t)row * b;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 32 * q + 4 * g;
+        if (p.vec) {
+          const float4 t = (c < b) ? __ldg(reinterpret_cast<const float4*>(dr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          dv[4 * q] = t.x; dv[4 * q + 1] = t.y; dv[4 * q + 2] = t.z; dv[4 * q + 3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dv[4 * q + j] = (c + j < b) ? __ldg(dr + c + j) : 0.f;
+        }
+      }
+      cur = row;
+    }
+    const float* xr = p.fixed + (size_t)col * p.ldf + p.fb0;
+    float s = 0.f;
+    if (!live) {
+    } else if (p.vec) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 32 * q + 4 * g;
+        if (c < b) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(xr + c));
+          s = fmaf(x.x, dv[4 * q], s);
+          s = fmaf(x.y, dv[4 * q + 1], s);
+          s = fmaf(x.z, dv[4 * q + 2], s);
+          s = fmaf(x.w, dv[4 * q + 3], s);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = 32 * q + 4 * g + j;
+          if (c < b) s = fmaf(__ldg(xr + c), dv[4 * q + j], s);
+        }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (live && g == 0) {
+      const long long pos = p.side.pos ? (long long)__ldg(p.side.pos + e) : e;
+      p.cache[pos] -= s;
+    }
+  }
+}
+
 }  // namespace ials

@@ -129,11 +129,13 @@ class DeviceSide:
         self.weights = None if weights is None else to(weights, np.float32)
         self.pos = None if pos is None else to(pos, np.int32)
         self.lam = to(lam, np.float32)
+        # row of every entry (the entry-parallel cache pass)
+        self.rows = to(np.repeat(np.arange(self.n_rows, dtype=np.int32), self.counts), np.int32)
         self.device = device
         self.struct = _lib.IalsSide(self.n_rows, self.n_fixed, self.nnz, _ptr(self.ptr).value,
                                     _ptr(self.cols).value, _ptr(self.labels).value,
                                     _ptr(self.weights).value, _ptr(self.pos).value,
-                                    _ptr(self.lam).value)
+                                    _ptr(self.lam).value, _ptr(self.rows).value)
         self._sched = {}
 
     def set_lam(self, lam):
