@@ -218,6 +218,30 @@ int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* it
  * replays do not).  bench.py reads it around its timed region. */
 int64_t ials_launch_count(void);
 
+/* ---- multi-GPU host path: tensor-core GEMMs on a ROW SHARD of a factor table
+ * (one rank's contiguous rows of W or H; ials_epoch keeps its own copies).
+ * The caller workspace (ials_shard_gemm_bytes) holds the shard's K-major TF32
+ * copies -- refresh them with ials_shard_sync after the shard's rows change
+ * -- and the GEMM scratch; b is the block width the workspace is sized for. */
+size_t ials_shard_gemm_bytes(int32_t n_rows, int32_t d, int32_t b);
+int ials_shard_sync(ials_session* s, const float* F, int32_t ldf, int32_t n_rows, int32_t d,
+                    int32_t b, int32_t c0, int32_t cw, void* ws, size_t ws_bytes, void* stream);
+/* partial slab over the shard: slab[d x bb] = F_shard^T F_shard[:, b0:b0+bb]
+ * (partial_gramian, linalg.py:39-45; the caller all-reduces across ranks) */
+int ials_shard_gramian(ials_session* s, int32_t n_rows, int32_t d, int32_t b, int32_t b0, int32_t bb,
+                       float* slab, void* ws, size_t ws_bytes, void* stream);
+/* proj[n_rows x bb] = alpha0 * F_shard @ slab (the alpha0 U[r,:] @ slab term of
+ * _newton_side_pass, solvers.py:175), slab the all-reduced d x bb slab */
+int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t n_rows, int32_t d,
+                          int32_t b, int32_t bb, float* slab, float alpha0, float* proj, void* ws,
+                          size_t ws_bytes, void* stream);
+/* ials_side_pass with the projection precomputed (proj: n_rows x b). */
+int ials_side_pass_projected(ials_session* s, const ials_side* side, const ials_sched* sched,
+                             const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                             int32_t b0, int32_t b, const float* slab, const float* proj,
+                             float alpha0, float* cache, int32_t side_id, void* workspace,
+                             size_t ws_bytes, void* stream);
+
 /* Workspace bytes for ials_build_csr over n interactions. */
 size_t ials_build_csr_workspace_bytes(int64_t n);
 

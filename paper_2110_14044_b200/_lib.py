@@ -78,6 +78,14 @@ SIGNATURES = {
     "ials_loss_workspace_bytes": (c_sz, [c_i32]),
     "ials_build_csr_workspace_bytes": (c_sz, [c_i64]),
     "ials_launch_count": (c_i64, []),
+    "ials_shard_gemm_bytes": (c_sz, [c_i32, c_i32, c_i32]),
+    "ials_shard_sync": (c_i32, [c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_p, c_sz, c_p]),
+    "ials_shard_gramian": (c_i32, [c_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
+    "ials_shard_projection": (c_i32, [c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_p, c_f, c_p,
+                                      c_p, c_sz, c_p]),
+    "ials_side_pass_projected": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
+                                         c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_f,
+                                         c_p, c_i32, c_p, c_sz, c_p]),
     "ials_topk": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
     "ials_build_csr": (c_i32, [c_p, c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                                c_p, c_sz, c_p]),

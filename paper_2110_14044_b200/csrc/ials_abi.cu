@@ -675,7 +675,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
                           const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
                           int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
                           int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st,
-                          bool proj_ready = false) {
+                          bool proj_ready = false, const float* proj_in = nullptr) {
   if (!side || !sched || !fixed || !own || !slab || !cache)
     return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
   if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
@@ -747,6 +747,10 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.redo_total = s->redo;
   p.cond_max = tc_cond_max();
   p.n_light_dev = nullptr;
+  if (proj_in) {   // precomputed by the caller (ials_side_pass_projected)
+    proj = const_cast<float*>(proj_in);
+    proj_ready = true;
+  }
   p.proj = proj;
   p.tc_rows = sched->tc_rows;
   p.tc_row_slice0 = sched->tc_row_slice0;
@@ -825,6 +829,16 @@ int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sch
                         side_id, static_cast<char*>(workspace), ws_bytes, S(stream));
 }
 
+int ials_side_pass_projected(ials_session* s, const ials_side* side, const ials_sched* sched,
+                             const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                             int32_t b0, int32_t b, const float* slab, const float* proj,
+                             float alpha0, float* cache, int32_t side_id, void* workspace,
+                             size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (!proj && side && side->n_rows > 0) return fail(s, IALS_E_INVALID, "side_pass_projected: NULL proj");
+  return side_pass_impl(s, side, sched, fixed, ldf, own, ldo, d, b0, b, slab, alpha0, cache,
+                        side_id, static_cast<char*>(workspace), ws_bytes, S(stream), true, proj);
+}
 
 // ------------------------------------------------------------------ tensor-core GEMMs (epoch)
 static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
@@ -874,6 +888,7 @@ static size_t tc_gemm_bytes(int n_users, int n_items, int d, int b) {
 size_t ials_epoch_tc_bytes(int32_t n_users, int32_t n_items, int32_t d, int32_t b) {
   return tc_gemm_bytes(n_users, n_items, d, b);
 }
+
 
 static int sync_copies(ials_session* s, const float* F, int ldf, int d, int c0, int cw,
                        const TcCopies& c, cudaStream_t st) {
@@ -935,6 +950,82 @@ static int proj_tc(ials_session* s, const float* own, int ldo, const TcCopies& O
   k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), 128, GemmLay::BYTES, st>>>(ah, al, bh, bl, job);
   LAUNCH_CHECK(s);
   return IALS_OK;
+}
+
+// ---- row shards (the multi-GPU host path): one factor shard's K-major
+// copies + GEMM scratch in a caller workspace:
+//   [copies(n, d)][split partials S x d x b][slab^T hi (b x d)][slab^T lo]
+struct ShardWs {
+  TcCopies c;
+  float *P, *sth, *stl;
+  int S, span;
+};
+
+static size_t shard_bytes(int n, int d, int b) {
+  int S, span;
+  gram_plan(std::max(n, 1), d, &S, &span);
+  return copies_bytes(n, d) + al256(size_t(S) * d * b * 4) + 2 * al256(size_t(b) * d * 4) + 1024;
+}
+
+static int shard_carve(ials_session* s, void* ws, size_t ws_bytes, int n, int d, int b, ShardWs* w) {
+  if (n < 0 || d < 1 || b < 1 || b > d) return fail(s, IALS_E_INVALID, "shard: bad sizes (n=%d d=%d b=%d)", n, d, b);
+  if (!ws || ws_bytes < shard_bytes(n, d, b))
+    return fail(s, IALS_E_NOMEM, "shard: workspace %zu < %zu bytes", ws_bytes, shard_bytes(n, d, b));
+  char* t = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 1023) & ~uintptr_t(1023));
+  t = carve_copies(t, n, d, &w->c);
+  gram_plan(std::max(n, 1), d, &w->S, &w->span);
+  w->P = reinterpret_cast<float*>(t);
+  t += al256(size_t(w->S) * d * b * 4);
+  w->sth = reinterpret_cast<float*>(t);
+  t += al256(size_t(b) * d * 4);
+  w->stl = reinterpret_cast<float*>(t);
+  return IALS_OK;
+}
+
+size_t ials_shard_gemm_bytes(int32_t n_rows, int32_t d, int32_t b) { return shard_bytes(n_rows, d, b); }
+
+int ials_shard_sync(ials_session* s, const float* F, int32_t ldf, int32_t n_rows, int32_t d, int32_t b,
+                    int32_t c0, int32_t cw, void* ws, size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  ShardWs w;
+  int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
+  if (rc) return rc;
+  if (c0 < 0 || cw < 0 || c0 + cw > d || (n_rows > 0 && (!F || ldf < d)))
+    return fail(s, IALS_E_INVALID, "shard_sync: bad range");
+  return sync_copies(s, F, ldf, d, c0, cw, w.c, S(stream));
+}
+
+int ials_shard_gramian(ials_session* s, int32_t n_rows, int32_t d, int32_t b, int32_t b0, int32_t bb,
+                       float* slab, void* ws, size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  ShardWs w;
+  int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
+  if (rc) return rc;
+  if (b0 < 0 || bb < 1 || bb > b || b0 + bb > d || !slab) return fail(s, IALS_E_INVALID, "shard_gramian: bad block");
+  if (get_encode(s) != IALS_OK) return fail(s, IALS_E_CUDA, "shard_gramian: no cuTensorMapEncodeTiled");
+  if (n_rows == 0) {
+    CUDA_TRY(s, cudaMemsetAsync(slab, 0, size_t(d) * bb * 4, S(stream)));
+    return IALS_OK;
+  }
+  return gram_tc(s, w.c, d, b0, bb, w.P, slab, w.sth, w.stl, S(stream));
+}
+
+int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t n_rows, int32_t d,
+                          int32_t b, int32_t bb, float* slab, float alpha0, float* proj, void* ws,
+                          size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  ShardWs w;
+  int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
+  if (rc) return rc;
+  if (bb < 1 || bb > b || !slab || (n_rows > 0 && (!F || !proj || ldf < d)))
+    return fail(s, IALS_E_INVALID, "shard_projection: bad arguments");
+  if (n_rows == 0) return IALS_OK;
+  if (get_encode(s) != IALS_OK) return fail(s, IALS_E_CUDA, "shard_projection: no cuTensorMapEncodeTiled");
+  cudaStream_t st = S(stream);
+  // stage slab^T hi / lo from the (all-reduced) slab: the split reduction with one split
+  k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(slab, 1, (long long)d * bb, d, bb, slab, w.sth, w.stl);
+  LAUNCH_CHECK(s);
+  return proj_tc(s, F, ldf, w.c, d, bb, w.sth, w.stl, alpha0, proj, st);
 }
 
 // optional phase events: 0 start, 1 after the cache, then per block

@@ -144,10 +144,49 @@ class GpuOps:
                                               self._stream())
         self.sess.check(rc, "cache_correct")
 
+    # ---- tensor-core GEMMs on this rank's row shards (b in 65..128, like
+    # ials_epoch): K-major copies of a shard live in a per-shard workspace
+    def tc_enable(self, M_rows, b):
+        """Keep K-major copies of the shard ``M_rows`` (a row slice of W or H)
+        for block width ``b``; returns False if the tensor-core path does not
+        apply (then gram / sweep use the FP32 SIMT kernels)."""
+        d = M_rows.shape[1]
+        if not (64 < b <= 128 and d % 4 == 0 and M_rows.stride(0) % 4 == 0
+                and M_rows.data_ptr() % 16 == 0):
+            return False
+        n = M_rows.shape[0]
+        nb = int(self.sess.lib.ials_shard_gemm_bytes(n, d, b))
+        if not hasattr(self, "_shards"):
+            self._shards = {}
+        self._shards[M_rows.data_ptr()] = (torch.empty(nb, dtype=torch.uint8, device=self.device), n, b)
+        self.tc_sync(M_rows, 0, d)
+        return True
+
+    def _shard(self, M_rows):
+        return getattr(self, "_shards", {}).get(M_rows.data_ptr())
+
+    def tc_sync(self, M_rows, c0, cw):
+        from .engine import _ptr
+        sh = self._shard(M_rows)
+        if sh is None:
+            return
+        ws, n, b = sh
+        rc = self.sess.lib.ials_shard_sync(self.sess.handle, _ptr(M_rows), M_rows.stride(0), n,
+                                           M_rows.shape[1], b, c0, cw, _ptr(ws), ws.numel(),
+                                           self._stream())
+        self.sess.check(rc, "shard_sync")
+
     def gram(self, M_rows, b0, b):
         from .engine import _ptr
         d = M_rows.shape[1]
         out = torch.empty((d, b), dtype=self.dtype, device=self.device)
+        sh = self._shard(M_rows)
+        if sh is not None and b <= sh[2]:
+            ws, n, bw = sh
+            rc = self.sess.lib.ials_shard_gramian(self.sess.handle, n, d, bw, b0, b, _ptr(out),
+                                                  _ptr(ws), ws.numel(), self._stream())
+            self.sess.check(rc, "shard_gramian")
+            return out
         if M_rows.shape[0] == 0:
             return out.zero_()
         ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(1, M_rows.shape[0], d, b, 0, 0)))
@@ -166,6 +205,24 @@ class GpuOps:
         ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(
             max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)) +
             int(self.sess.lib.ials_tc_workspace_bytes(sch.tc_max_wave_rows, sch.tc_max_wave_slices)))
+        sh = self._shard(own_rows)
+        if sh is not None and b <= sh[2] and own_rows.shape[0] > 0:
+            # projection alpha0 * own @ slab on the tensor core, then the sweep
+            sws, n, bw = sh
+            proj = torch.empty((n, b), dtype=self.dtype, device=self.device)
+            rc = self.sess.lib.ials_shard_projection(self.sess.handle, _ptr(own_rows),
+                                                     own_rows.stride(0), n, d, bw, b, _ptr(slab),
+                                                     float(alpha0), _ptr(proj), _ptr(sws),
+                                                     sws.numel(), self._stream())
+            self.sess.check(rc, "shard_projection")
+            rc = self.sess.lib.ials_side_pass_projected(
+                self.sess.handle, ctypes.byref(ds.struct), ctypes.byref(sch.struct), _ptr(fixed),
+                fixed.stride(0), _ptr(own_rows), own_rows.stride(0), d, b0, b, _ptr(slab),
+                _ptr(proj), float(alpha0), _ptr(cache), side_id, _ptr(ws), ws.numel(),
+                self._stream())
+            self.sess.check(rc, "side_pass_projected")
+            self.tc_sync(own_rows, b0, b)   # the shard's block changed
+            return
         rc = self.sess.lib.ials_side_pass(self.sess.handle, ctypes.byref(ds.struct),
                                           ctypes.byref(sch.struct), _ptr(fixed), fixed.stride(0),
                                           _ptr(own_rows), own_rows.stride(0), d, b0, b,
@@ -234,6 +291,9 @@ class ShardedTrainer:
         ulo, uhi = self.user_bounds[self.rank]
         ilo, ihi = self.item_bounds[self.rank]
         Wl, Hl = W[ulo:uhi], H[ilo:ihi]
+        if hasattr(ops, "tc_enable"):   # K-major copies of both shards (no-op when b is off the TC path)
+            for M in (Wl, Hl):
+                ops.tc_enable(M, block_size)
         ops.predictions(self.us, Wl, H, self.Cu)
         ops.predictions(self.is_, Hl, W, self.Ci)
         prev = None        # (b0, b, dH) of the last item pass

@@ -233,10 +233,12 @@ def test_tensor_core_one_and_ten_epochs(ials, d):
     assert abs(reports[-1].loss - want10) / want10 < TOL
 
 
-def test_sharded_path_gpu_ops_single_rank(ials):
+@pytest.mark.parametrize("d,b", [(48, 16), (256, 128)])
+def test_sharded_path_gpu_ops_single_rank(ials, d, b):
     """The multi-GPU orchestration with the real kernels (GpuOps, fp32) at
     world size 1: local sides, the item-major cache C_i and the delta
-    corrections (k_cache_correct) against the oracle."""
+    corrections (k_cache_correct) against the oracle; b = 128 takes the
+    shard tensor-core GEMMs (ials_shard_*) and the fused sweep."""
     import torch
     from oracle import ialspp_oracle as orc
     from paper_2110_14044_b200.distributed import GpuOps, ShardedTrainer
@@ -245,7 +247,6 @@ def test_sharded_path_gpu_ops_single_rank(ials):
     data = {"num_users": U, "num_items": I, "user_ptr": csr["user_ptr"], "user_cols": csr["items"],
             "item_ptr": csr["item_ptr"], "item_cols": csr["users"][csr["item_order"]],
             "item_order": csr["item_order"], "labels": None, "weights": None}
-    d, b = 48, 16
     w, h = orc.init_factors(U, I, d, 0.1, 4)
     w, h = w.astype(np.float32).astype(np.float64), h.astype(np.float32).astype(np.float64)
     W = torch.from_numpy(w.astype(np.float32)).cuda()
