@@ -203,6 +203,21 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
                float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
                void* workspace, size_t ws_bytes, void* stream);
 
+/* ials_epoch for a model held in (pinned) HOST memory, the reference's
+ * in-place ialspp_epoch contract end to end: W_in / H_in are copied to the
+ * device buffers W / H, the epoch runs, and W_out / H_out (may alias the
+ * inputs) and cache_out (NULL to skip) receive the results.  The copies run
+ * on a second stream and overlap the epoch: H and W (in row chunks, each
+ * chunk's predictions starting as it lands) on the way in, each column block
+ * W[:, pi] / H[:, pi] as soon as its side pass has finished it on the way
+ * out.  Host leading dimensions in elements.  Stream-ordered on `stream`. */
+int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                    const ials_side* items, const ials_sched* item_sched, const float* W_in,
+                    float* W_out, int64_t ldw_host, const float* H_in, float* H_out,
+                    int64_t ldh_host, float* W, int32_t ldw, float* H, int32_t ldh, int32_t d,
+                    int32_t b, float alpha0, float* cache, float* cache_out, void* workspace,
+                    size_t ws_bytes, void* stream);
+
 /* Workspace bytes for ials_loss_terms at embedding dimension d. */
 size_t ials_loss_workspace_bytes(int32_t d);
 

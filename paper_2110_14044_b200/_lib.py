@@ -75,6 +75,10 @@ SIGNATURES = {
     "ials_epoch": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
                            ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_i32, c_p,
                            c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p]),
+    "ials_epoch_host": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
+                                ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_p, c_i64,
+                                c_p, c_p, c_i64, c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_f, c_p, c_p,
+                                c_p, c_sz, c_p]),
     "ials_loss_workspace_bytes": (c_sz, [c_i32]),
     "ials_build_csr_workspace_bytes": (c_sz, [c_i64]),
     "ials_launch_count": (c_i64, []),

@@ -29,6 +29,8 @@ using namespace ials;
 
 struct ials_session {
   int device;
+  cudaStream_t copy_st = nullptr;             // ials_epoch_host: host <-> device staging
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   unsigned long long* err;  // device error word (ULLONG_MAX = clean)
   unsigned long long* redo; // rows the fused tensor-core sweep handed to SIMT
   char msg[512];
@@ -109,6 +111,9 @@ int ials_session_destroy(ials_session* s) {
   if (!s) return IALS_OK;
   cudaFree(s->err);
   cudaFree(s->redo);
+  if (s->copy_st) cudaStreamDestroy(s->copy_st);
+  if (s->ev_a) cudaEventDestroy(s->ev_a);
+  if (s->ev_b) cudaEventDestroy(s->ev_b);
   delete s;
   return IALS_OK;
 }
@@ -1045,10 +1050,59 @@ static void rec_event(int k, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ epoch
+// host staging of ials_epoch_host (all pointers pinned host memory)
+struct EpochHost {
+  const float *W_in, *H_in;
+  float *W_out, *H_out, *cache_out;
+  int64_t ldw, ldh;
+};
+
+// st -> copy stream dependency, then a 2-D copy on the copy stream
+static int stage_copy(ials_session* s, cudaStream_t st, void* dst, size_t dpitch, const void* src,
+                      size_t spitch, size_t width, size_t rows, cudaMemcpyKind kind) {
+  if (rows == 0 || width == 0) return IALS_OK;
+  CUDA_TRY(s, cudaEventRecord(s->ev_a, st));
+  CUDA_TRY(s, cudaStreamWaitEvent(s->copy_st, s->ev_a, 0));
+  CUDA_TRY(s, cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s->copy_st));
+  return IALS_OK;
+}
+
+static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                      const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
+                      float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
+                      void* workspace, size_t ws_bytes, void* stream, const EpochHost* host);
+
 int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
                float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
                void* workspace, size_t ws_bytes, void* stream) {
+  return epoch_impl(s, users, user_sched, items, item_sched, W, ldw, H, ldh, d, b, alpha0, cache,
+                    workspace, ws_bytes, stream, nullptr);
+}
+
+int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                    const ials_side* items, const ials_sched* item_sched, const float* W_in,
+                    float* W_out, int64_t ldw_host, const float* H_in, float* H_out,
+                    int64_t ldh_host, float* W, int32_t ldw, float* H, int32_t ldh, int32_t d,
+                    int32_t b, float alpha0, float* cache, float* cache_out, void* workspace,
+                    size_t ws_bytes, void* stream) {
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (!W_in || !W_out || !H_in || !H_out || ldw_host < d || ldh_host < d)
+    return fail(s, IALS_E_INVALID, "epoch_host: bad host buffers");
+  if (!s->copy_st) {
+    CUDA_TRY(s, cudaStreamCreateWithFlags(&s->copy_st, cudaStreamNonBlocking));
+    CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_a, cudaEventDisableTiming));
+    CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_b, cudaEventDisableTiming));
+  }
+  const EpochHost h{W_in, H_in, W_out, H_out, cache_out, ldw_host, ldh_host};
+  return epoch_impl(s, users, user_sched, items, item_sched, W, ldw, H, ldh, d, b, alpha0, cache,
+                    workspace, ws_bytes, stream, &h);
+}
+
+static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                      const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
+                      float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
+                      void* workspace, size_t ws_bytes, void* stream, const EpochHost* host) {
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (!users || !items || !user_sched || !item_sched)
     return fail(s, IALS_E_INVALID, "epoch: NULL argument");
@@ -1087,14 +1141,47 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
     sth = reinterpret_cast<float*>(t);
     t += al256(size_t(b) * d * 4);
     stl = reinterpret_cast<float*>(t);
+  }
+  if (host) {
+    // H in full, then W in row chunks, host -> device on the copy stream; the
+    // predictions of each user chunk start as soon as its rows have landed
+    const size_t es = sizeof(float);
+    CUDA_TRY(s, cudaEventRecord(s->ev_a, st));   // W / H free on the device
+    CUDA_TRY(s, cudaStreamWaitEvent(s->copy_st, s->ev_a, 0));
+    CUDA_TRY(s, cudaMemcpy2DAsync(H, size_t(ldh) * es, host->H_in, size_t(host->ldh) * es, size_t(d) * es,
+                                  size_t(items->n_rows), cudaMemcpyHostToDevice, s->copy_st));
+  }
+  if (tc_gemm && !host) {
     int rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
     if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
     if (rc) return rc;
   }
   rec_event(0, st);
-  int rc = ials_predictions(s, users->n_rows, users->ptr, users->cols, W, ldw, H, ldh, d, cache,
-                            stream);
-  if (rc) return rc;
+  int rc = IALS_OK;
+  if (host) {
+    const int nch = 8, U = users->n_rows;
+    const int per = (U + nch - 1) / nch;
+    for (int c = 0; c < nch && c * per < U; ++c) {
+      const int r0 = c * per, r1 = std::min(U, r0 + per);
+      CUDA_TRY(s, cudaMemcpy2DAsync(W + size_t(r0) * ldw, size_t(ldw) * 4, host->W_in + size_t(r0) * host->ldw,
+                                    size_t(host->ldw) * 4, size_t(d) * 4, size_t(r1 - r0),
+                                    cudaMemcpyHostToDevice, s->copy_st));
+      CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));
+      CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));   // H and W rows [0, r1) are on the device
+      rc = ials_predictions(s, r1 - r0, users->ptr + r0, users->cols, W + size_t(r0) * ldw, ldw, H,
+                            ldh, d, cache, stream);
+      if (rc) return rc;
+    }
+    if (tc_gemm) {
+      rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
+      if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+      if (rc) return rc;
+    }
+  } else {
+    rc = ials_predictions(s, users->n_rows, users->ptr, users->cols, W, ldw, H, ldh, d, cache,
+                          stream);
+    if (rc) return rc;
+  }
   rec_event(1, st);
   int ek = 2;
   for (int b0 = 0; b0 < d; b0 += b) {
@@ -1110,6 +1197,11 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
                         pws, pbytes, st, tc_gemm);
     if (rc) return rc;
+    if (host) {   // W[:, b0:b0+bb] is final: back to the host beside the rest of the epoch
+      rc = stage_copy(s, st, host->W_out + b0, size_t(host->ldw) * 4, W + b0, size_t(ldw) * 4,
+                      size_t(bb) * 4, size_t(users->n_rows), cudaMemcpyDeviceToHost);
+      if (rc) return rc;
+    }
     rec_event(ek++, st);
     if (tc_gemm) {
       rc = sync_copies(s, W, ldw, d, b0, bb, cw, st);
@@ -1123,11 +1215,25 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
     rc = side_pass_impl(s, items, item_sched, W, ldw, H, ldh, d, b0, bb, slab, alpha0, cache, 1,
                         pws, pbytes, st, tc_gemm);
     if (rc) return rc;
+    if (host) {
+      rc = stage_copy(s, st, host->H_out + b0, size_t(host->ldh) * 4, H + b0, size_t(ldh) * 4,
+                      size_t(bb) * 4, size_t(items->n_rows), cudaMemcpyDeviceToHost);
+      if (rc) return rc;
+    }
     if (tc_gemm) {
       rc = sync_copies(s, H, ldh, d, b0, bb, ch, st);
       if (rc) return rc;
     }
     rec_event(ek++, st);
+  }
+  if (host) {   // the maintained cache, then the caller's stream waits for every copy
+    if (host->cache_out) {
+      const size_t cb = size_t(users->nnz) * 4;
+      rc = stage_copy(s, st, host->cache_out, cb, cache, cb, cb, 1, cudaMemcpyDeviceToHost);
+      if (rc) return rc;
+    }
+    CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));
+    CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));
   }
   return IALS_OK;
 }

@@ -370,6 +370,25 @@ class Engine:
                 self.lib.ials_epoch_events(None, 0)
         self.sess.check(rc, "epoch")
 
+    def epoch_host(self, W_host, H_host, W, H, cache, b, alpha0, W_out=None, H_out=None,
+                   cache_out=None):
+        """One epoch for a model in (pinned) host tensors: ials_epoch_host
+        stages W / H in, runs the epoch, and writes W / H (and the cache if
+        ``cache_out`` is given) back, overlapping the copies with the epoch."""
+        d = W.shape[1]
+        ws = self.workspace(d, b)
+        su, si = self.p.users.schedule(b), self.p.items.schedule(b)
+        W_out = W_host if W_out is None else W_out
+        H_out = H_host if H_out is None else H_out
+        rc = self.lib.ials_epoch_host(self.sess.handle, ctypes.byref(self.p.users.struct),
+                                      ctypes.byref(su.struct), ctypes.byref(self.p.items.struct),
+                                      ctypes.byref(si.struct), _ptr(W_host), _ptr(W_out),
+                                      W_host.stride(0), _ptr(H_host), _ptr(H_out), H_host.stride(0),
+                                      _ptr(W), W.stride(0), _ptr(H), H.stride(0), d, b,
+                                      float(alpha0), _ptr(cache), _ptr(cache_out), _ptr(ws),
+                                      ws.numel(), self.stream())
+        self.sess.check(rc, "epoch_host")
+
     def epoch_graph(self, W, H, cache, b, alpha0):
         """The same epoch captured once as a CUDA graph and replayed (one
         launch per epoch instead of ~10 per block; matters for small configs).

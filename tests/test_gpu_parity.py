@@ -285,3 +285,30 @@ def test_dedicated_solver_entry_points(ials, which):
         bw = 1
     orc.train(w, h, orc.build_csr(U, I, users, items), 0.1, 1e-3, 1.0, bw, 1)
     assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL
+
+
+def test_epoch_host_equals_device_epoch(ials):
+    """ials_epoch_host (host-staged, copies overlapped) gives bit for bit the
+    device epoch's W, H and cache, written to the host buffers."""
+    import torch
+    from paper_2110_14044_b200.engine import DeviceProblem, Engine
+    rng = np.random.default_rng(13)
+    U, I, n, d, b = 1500, 400, 30000, 256, 128
+    users = rng.integers(0, U, n)
+    items = np.minimum(rng.zipf(1.2, n) - 1, I - 1)
+    prob = DeviceProblem.from_dataset(ials.InteractionDataset(U, I, users, items), "cuda:0")
+    prob.set_regularizer(0.1, 1e-3, 1.0)
+    eng = Engine(prob)
+    g = torch.Generator().manual_seed(0)
+    W0 = torch.randn(U, d, generator=g) * 0.05
+    H0 = torch.randn(I, d, generator=g) * 0.05
+    W, H = W0.cuda(), H0.cuda()
+    cache = torch.zeros(n, device="cuda")
+    eng.epoch(W, H, cache, b, 0.1)
+    Wh, Hh = W0.clone().pin_memory(), H0.clone().pin_memory()
+    Ch = torch.zeros(n).pin_memory()
+    W2, H2 = torch.zeros_like(W), torch.zeros_like(H)
+    c2 = torch.zeros(n, device="cuda")
+    eng.epoch_host(Wh, Hh, W2, H2, c2, b, 0.1, cache_out=Ch)   # in place on the host arrays
+    torch.cuda.synchronize()
+    assert torch.equal(Wh, W.cpu()) and torch.equal(Hh, H.cpu()) and torch.equal(Ch, cache.cpu())
