@@ -8,8 +8,9 @@ Host mirror of the reference's ``project_user`` / ``fold_in_users``
 * Fold-in solves, per history, the same regularized least squares as a user
   pass.  On the device that is one user pass of the block sweep with a single
   block of width d from a zero embedding and a zero cache: the Newton step
-  from w = 0 is the closed-form solve.  Block widths go up to 256, so the
-  device fold-in covers d <= 256.
+  from w = 0 is the closed-form solve.  Block widths go up to 256; wider
+  models iterate user passes over 128-column blocks (block Gauss-Seidel on
+  the same strictly convex quadratic) to a relative change below 1e-7.
 * Scores are a plain FP32 GEMM (cuBLAS through torch.matmul: allowed as a
   library GEMM); the exclusion of each user's input items and the top-k with
   the reference's tie order run in ``ials_topk`` (csrc/ials_topk.cuh).
@@ -55,8 +56,6 @@ def fold_in_users(item_factors, histories, config: SolverConfig, device=None) ->
         raise ValueError("config is required")
     hf = np.ascontiguousarray(item_factors, dtype=np.float64)
     n_items, d = hf.shape
-    if d > _MAX_FOLD_DIM:
-        raise ValueError(f"device fold-in supports dim <= {_MAX_FOLD_DIM}")
     users, items, labels, weights = [], [], [], []
     for row, (its, lbl, wts) in enumerate(histories):
         its = np.asarray(its, dtype=np.int64)
@@ -71,8 +70,36 @@ def fold_in_users(item_factors, histories, config: SolverConfig, device=None) ->
                               np.concatenate(labels), np.concatenate(weights))
     model = FactorModel(out, hf)
     cache = PredictionCache.zeros(data.n_interactions)   # exact for the zero embedding
-    block_update(model, data, cache, config.with_(dim=d, block_size=d), np.arange(d), "user",
-                 device)
+    if d <= _MAX_FOLD_DIM:
+        block_update(model, data, cache, config.with_(dim=d, block_size=d), np.arange(d), "user",
+                     device)
+        return model.user_factors
+    return _fold_in_blocks(model, data, cache, config, device)
+
+
+def _fold_in_blocks(model, data, cache, config, device, tol=1e-7, max_sweeps=200):
+    """d > 256 (wider than one sweep block): block Gauss-Seidel on each
+    history's quadratic with the same device passes -- user passes over
+    blocks of 128 columns, the cache kept exact -- until a whole sweep changes
+    the embeddings by less than ``tol`` (relative, Frobenius).  Each pass is
+    an exact block minimisation, so the iteration converges to the reference's
+    closed-form solve (the quadratic is strictly convex: lambda > 0)."""
+    import torch
+
+    from .solvers import DeviceTrainer, partition_dims
+    d = model.dim
+    cfg = config.with_(dim=d, block_size=128)
+    tr = DeviceTrainer(model, data, cfg, partition_dims(d, 128), device, cache)
+    prev = torch.zeros_like(tr.W)
+    for _ in range(max_sweeps):
+        prev.copy_(tr.W)
+        for b0, b in tr.spans:
+            tr.block(b0, b, "user")
+        num = float(torch.linalg.vector_norm(tr.W - prev))
+        den = float(torch.linalg.vector_norm(tr.W))
+        if num <= tol * max(den, 1e-30):
+            break
+    tr.write_back()
     return model.user_factors
 
 
