@@ -866,20 +866,19 @@ struct TcCopies {   // K-major copies of one factor matrix F (n x d)
   int n, ldt;
 };
 
+// only F^T is stored: the GEMM forms the tf32 low parts on chip
 static size_t copies_bytes(int n, int d) {
   const size_t ldt = rup(std::max(n, 1), 4);
-  return 2 * al256(size_t(d) * ldt * 4) + al256(size_t(std::max(n, 1)) * d * 4);
+  return al256(size_t(d) * ldt * 4);
 }
 
 static char* carve_copies(char* w, int n, int d, TcCopies* c) {
   c->n = n;
   c->ldt = rup(std::max(n, 1), 4);
   c->FT = reinterpret_cast<float*>(w);
-  w += al256(size_t(d) * c->ldt * 4);
-  c->FT_lo = reinterpret_cast<float*>(w);
-  w += al256(size_t(d) * c->ldt * 4);
-  c->F_lo = reinterpret_cast<float*>(w);
-  return w + al256(size_t(std::max(n, 1)) * d * 4);
+  c->FT_lo = nullptr;
+  c->F_lo = nullptr;
+  return w + al256(size_t(d) * c->ldt * 4);
 }
 
 static size_t tc_gemm_bytes(int n_users, int n_items, int d, int b) {
@@ -922,17 +921,15 @@ static int gram_tc(ials_session* s, const TcCopies& F, int d, int b0, int bb, fl
   const int bn = rup(bb, 16);
   int S, span;
   gram_plan(F.n, d, &S, &span);
-  CUtensorMap ah, al, bh, bl;
+  CUtensorMap ah, bh;
   rc = make_map(s, &ah, F.FT, F.n, d, F.ldt, 128);
-  if (!rc) rc = make_map(s, &al, F.FT_lo, F.n, d, F.ldt, 128);
   if (!rc) rc = make_map(s, &bh, F.FT, F.n, d, F.ldt, bn);
-  if (!rc) rc = make_map(s, &bl, F.FT_lo, F.n, d, F.ldt, bn);
   if (rc) return rc;
   GemmJob job{d, 0, b0, bb, bn, F.n, span, P, bb, (long long)d * bb, 1.f};
-  k_gemm3_tf32<<<dim3((d + 127) / 128, S), 128, GemmLay::BYTES, st>>>(ah, al, bh, bl, job);
+  k_gemm3_tf32<<<dim3((d + 127) / 128, S), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, job);
   LAUNCH_CHECK(s);
   k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(P, S, (long long)d * bb, d, bb, slab,
-                                                      slabT_hi, slabT_lo);
+                                                      slabT_hi, nullptr);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
@@ -945,14 +942,13 @@ static int proj_tc(ials_session* s, const float* own, int ldo, const TcCopies& O
   int rc = gemm_attrs(s);
   if (rc) return rc;
   const int bn = rup(bb, 16);
-  CUtensorMap ah, al, bh, bl;
+  CUtensorMap ah, bh;
   rc = make_map(s, &ah, own, d, O.n, ldo, 128);
-  if (!rc) rc = make_map(s, &al, O.F_lo, d, O.n, d, 128);
   if (!rc) rc = make_map(s, &bh, slabT_hi, d, bb, d, bn);
-  if (!rc) rc = make_map(s, &bl, slabT_lo, d, bb, d, bn);
   if (rc) return rc;
+  (void)slabT_lo;
   GemmJob job{O.n, 0, 0, bb, bn, d, rup(d, kGemmKC), proj, bb, 0, alpha0};
-  k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), 128, GemmLay::BYTES, st>>>(ah, al, bh, bl, job);
+  k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, job);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
@@ -1028,7 +1024,7 @@ int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t 
   if (get_encode(s) != IALS_OK) return fail(s, IALS_E_CUDA, "shard_projection: no cuTensorMapEncodeTiled");
   cudaStream_t st = S(stream);
   // stage slab^T hi / lo from the (all-reduced) slab: the split reduction with one split
-  k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(slab, 1, (long long)d * bb, d, bb, slab, w.sth, w.stl);
+  k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(slab, 1, (long long)d * bb, d, bb, slab, w.sth, nullptr);
   LAUNCH_CHECK(s);
   return proj_tc(s, F, ldf, w.c, d, bb, w.sth, w.stl, alpha0, proj, st);
 }

@@ -5,14 +5,19 @@
 //   projection    proj     = alpha0 * own G[:, pi] (rows x b, K = d)
 //
 // Both operands must be K-major for kind::tf32, so the epoch keeps, per
-// factor matrix F (n x d): F^T (d x n) and the tf32 low parts F^T_lo, F_lo
-// (x - trunc_tf32(x)); k_sync_copies refreshes them for the column block a
-// side pass just changed (solvers.py:340-375 updates one block at a time).
+// factor matrix F (n x d), the transposed copy F^T (d x n); k_sync_copies
+// refreshes it for the column block a side pass just changed
+// (solvers.py:340-375 updates one block at a time).  The tf32 low parts
+// x - trunc_tf32(x) are formed on chip, and
 // D = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T accumulates in TMEM.
 //
-// One CTA = 128 threads: warp 0 / lane 0 issues TMA loads into a 3-stage
-// ring (full / empty mbarriers), warp 1 / lane 0 issues the MMAs, then all
-// four warps drain the 128 x N accumulator (thread i <-> TMEM lane i).
+// One CTA = 256 threads: warp 0 / lane 0 issues TMA loads of the raw fp32
+// operands (the hi parts: the MMA drops their low 13 bits) into a 3-stage ring,
+// warps 2..7 form the lo parts x - trunc_tf32(x) in shared memory (same
+// swizzled layout: the map is elementwise), warp 1 / lane 0 issues the MMAs
+// once both are there, and all eight warps drain the 128 x N accumulator
+// (warp w: TMEM lanes 32 (w % 4).., column half w / 4).  Only the raw
+// operands cross HBM, half of what stored lo copies would cost.
 #pragma once
 #include <cuda.h>
 #include "ials_common.cuh"
@@ -36,24 +41,29 @@ struct GemmJob {
 
 constexpr int kGemmStages = 3;
 constexpr int kGemmKC = 32;  // K per stage: one 128-byte swizzle row
+constexpr int kGemmThreads = 256, kGemmConv = kGemmThreads - 64;
 
 struct GemmLay {
   static constexpr int A_BYTES = 128 * 128;  // 128 rows x 128 B
   static constexpr int B_BYTES = 128 * 128;  // up to 128 rows
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // A hi, A lo, B hi, B lo
   static constexpr int OFF_BAR = kGemmStages * STAGE;
-  static constexpr int BYTES = OFF_BAR + 8 * (2 * kGemmStages + 1) + 16 + 1024;
+  static constexpr int BYTES = OFF_BAR + 8 * (3 * kGemmStages + 1) + 16 + 1024;
 };
 
-__global__ void __launch_bounds__(128, 1)
-    k_gemm3_tf32(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap a_lo,
-                 const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo,
+IALS_DEVI void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm3_tf32(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap b_hi,
                  GemmJob job) {
   extern __shared__ __align__(1024) char smem_g[];
   char* smem = smem_g + ((1024u - (smem_u32(smem_g) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GemmLay::OFF_BAR);
-  uint64_t* empty = full + kGemmStages;
+  uint64_t* lo_ready = full + kGemmStages;
+  uint64_t* empty = lo_ready + kGemmStages;
   uint64_t* done = empty + kGemmStages;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(done + 1);
   const int m0 = blockIdx.x * 128;
@@ -62,11 +72,10 @@ __global__ void __launch_bounds__(128, 1)
   const int nk = (ke - kb + kGemmKC - 1) / kGemmKC;
   if (tid == 0) {
     prefetch_tmap(&a_hi);
-    prefetch_tmap(&a_lo);
     prefetch_tmap(&b_hi);
-    prefetch_tmap(&b_lo);
     for (int s = 0; s < kGemmStages; ++s) {
       mbar_init(full + s, 1);
+      mbar_init(lo_ready + s, kGemmConv);
       mbar_init(empty + s, 1);
     }
     mbar_init(done, 1);
@@ -76,7 +85,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tptr;
-  const uint32_t stage_bytes = 2 * GemmLay::A_BYTES + 2 * job.bn * 128;
+  const uint32_t stage_bytes = GemmLay::A_BYTES + job.bn * 128;
   if (warp == 0 && (tid & 31) == 0) {  // TMA producer
     for (int c = 0; c < nk; ++c) {
       const int s = c % kGemmStages;
@@ -85,16 +94,14 @@ __global__ void __launch_bounds__(128, 1)
       mbar_expect_tx(full + s, stage_bytes);
       const int kc = kb + c * kGemmKC;
       tma_load_2d(smem_u32(st), &a_hi, kc, job.a_row0 + m0, full + s);
-      tma_load_2d(smem_u32(st + GemmLay::A_BYTES), &a_lo, kc, job.a_row0 + m0, full + s);
       tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, kc, job.b_row0, full + s);
-      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, kc, job.b_row0,
-                  full + s);
     }
   } else if (warp == 1 && (tid & 31) == 0) {  // MMA issuer
     const uint32_t idesc = make_idesc_tf32(128, job.bn, 0, 0, 0);
     for (int c = 0; c < nk; ++c) {
       const int s = c % kGemmStages;
       mbar_wait(full + s, (c / kGemmStages) & 1);
+      mbar_wait(lo_ready + s, (c / kGemmStages) & 1);
       tc_fence_after();
       const uint32_t base = smem_u32(smem + s * GemmLay::STAGE);
       const uint32_t ah = base, al = base + GemmLay::A_BYTES;
@@ -112,15 +119,35 @@ __global__ void __launch_bounds__(128, 1)
       umma_commit(empty + s);   // frees the stage once these MMAs have read it
     }
     umma_commit(done);
+  } else if (warp >= 2) {   // lo parts of the landed stage
+    const int ct = tid - 64;
+    const int na4 = GemmLay::A_BYTES / 16, nt4 = na4 + job.bn * 8;
+    for (int c = 0; c < nk; ++c) {
+      const int s = c % kGemmStages;
+      mbar_wait(full + s, (c / kGemmStages) & 1);
+      char* st = smem + s * GemmLay::STAGE;
+      const float4* ahi = reinterpret_cast<const float4*>(st);
+      float4* alo = reinterpret_cast<float4*>(st + GemmLay::A_BYTES);
+      const float4* bhi = reinterpret_cast<const float4*>(st + 2 * GemmLay::A_BYTES);
+      float4* blo = reinterpret_cast<float4*>(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES);
+      for (int i = ct; i < nt4; i += kGemmConv) {
+        const bool isa = i < na4;
+        const float4 v = isa ? ahi[i] : bhi[i - na4];
+        const float4 l = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+        if (isa) alo[i] = l; else blo[i - na4] = l;
+      }
+      fence_proxy_async_smem();   // generic-proxy writes -> the MMA's async-proxy reads
+      mbar_arrive(lo_ready + s);
+    }
   }
   __syncwarp();
-  // epilogue: thread i drains TMEM lane i = output row m0 + i
+  // epilogue: warp w drains TMEM lanes 32 (w % 4).. (output rows m0 + lane), column half w / 4
   mbar_wait(done, 0);
   tc_fence_after();
-  const int row = m0 + tid;
+  const int row = m0 + (warp & 3) * 32 + (tid & 31);
   float* o = job.out + (long long)blockIdx.y * job.split_stride + (long long)row * job.ldo;
-  const uint32_t raddr = tmem + ((uint32_t)(warp * 32) << 16);
-  for (int c32 = 0; c32 < job.bn; c32 += 32) {   // warp-uniform
+  const uint32_t raddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  for (int c32 = (warp >> 2) * 32; c32 < job.bn; c32 += 64) {   // warp-uniform
     float v[32];
     tmem_ld32(raddr + c32, v);
     tmem_wait_ld();
@@ -150,7 +177,7 @@ __global__ void k_gram_reduce(const float* __restrict__ P, int splits, long long
   for (int t = 0; t < splits; ++t) s += P[(long long)t * split_stride + idx];
   slab[idx] = s;
   slabT_hi[(size_t)j * d + k] = s;
-  slabT_lo[(size_t)j * d + k] = tf32_lo(s);
+  if (slabT_lo) slabT_lo[(size_t)j * d + k] = tf32_lo(s);
 }
 
 // Refresh the K-major copies of F for columns [c0, c0 + cw): F^T, F^T_lo
@@ -165,7 +192,7 @@ __global__ void k_sync_copies(const float* __restrict__ F, int n, int ldf, int c
     float x = 0.f;
     if (r < n && c < c0 + cw) {
       x = F[(size_t)r * ldf + c];
-      F_lo[(size_t)r * ldl + c] = tf32_lo(x);
+      if (F_lo) F_lo[(size_t)r * ldl + c] = tf32_lo(x);
     }
     tile[i][tx] = x;
   }
@@ -175,7 +202,7 @@ __global__ void k_sync_copies(const float* __restrict__ F, int n, int ldf, int c
     if (r < n && c < c0 + cw) {
       const float x = tile[tx][i];
       FT[(size_t)c * ldt + r] = x;
-      FT_lo[(size_t)c * ldt + r] = tf32_lo(x);
+      if (FT_lo) FT_lo[(size_t)c * ldt + r] = tf32_lo(x);
     }
   }
 }
