@@ -101,3 +101,22 @@ def test_fold_in_wide_models_converge_to_the_exact_solve():
     got = ials.fold_in_users(hf, hist, cfg)
     want = orc.fold_in(hf, hist, 0.1, 1e-3, 1.0)
     assert relf(got, want) < 1e-3
+
+
+@pytest.mark.parametrize("d", [32, 128, 200])
+def test_fold_in_with_labels_and_weights(d):
+    """Non-unit labels / weights reach the device fold-in (the sweep's
+    weighted path) exactly as the reference's rhs / Hessian use them."""
+    from oracle import ialspp_oracle as orc
+    rng = np.random.default_rng(23 + d)
+    I = 500
+    hf = (rng.standard_normal((I, d)) * 0.1).astype(np.float32).astype(np.float64)
+    hist = []
+    for _ in range(120):
+        n = int(rng.integers(0, 40))
+        its = rng.choice(I, n, replace=False)
+        hist.append((its, rng.uniform(0.5, 2.0, n), rng.uniform(0.2, 3.0, n)))
+    cfg = ials.SolverConfig(dim=d, block_size=8, unobserved_weight=0.1, reg=1e-3, reg_exponent=1.0)
+    got = ials.fold_in_users(hf, hist, cfg)
+    want = orc.fold_in(hf, hist, 0.1, 1e-3, 1.0)
+    assert relf(got, want) < 1e-3
