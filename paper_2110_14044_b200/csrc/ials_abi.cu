@@ -375,6 +375,7 @@ static int set_smem_attrs(ials_session* s) {
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_cache<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   done = true;
   return IALS_OK;
@@ -515,7 +516,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     else
       k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
     LAUNCH_CHECK(s);
-    k_heavy_solve<128, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    k_heavy_solve<128, true, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
   }
   if (p.n_light + p.n_heavy > 0) {

@@ -683,7 +683,9 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   if (tid < BT) p.gpart[(size_t)sl * BT + tid] = gacc;
 }
 
-template <int BT, bool GUARD = false>
+// SYM: the slice partials are the non-symmetric E of the tensor-core heavy
+// partials; the Hessian is their symmetric part (E + E^T) / 2.
+template <int BT, bool GUARD = false, bool SYM = false>
 __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
     k_heavy_solve(SweepParams p) {
   using L = Lay<BT>;
@@ -706,6 +708,11 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
       for (int i = 0; i < L::SR; ++i) {
         float v[L::SC];
         lds_vec<L::SC>(v, hp + (T.roff[t] + i) * BT + T.coff[t]);
+        if (SYM) {
+#pragma unroll
+          for (int j = 0; j < L::SC; ++j)
+            v[j] = 0.5f * (v[j] + hp[(size_t)(T.coff[t] + j) * BT + T.roff[t] + i]);
+        }
 #pragma unroll
         for (int j = 0; j < L::SC; ++j) T.acc[t][i][j] += v[j];
       }

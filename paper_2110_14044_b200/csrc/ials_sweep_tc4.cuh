@@ -165,7 +165,10 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, const Tc4State& st, 
 
 // UNIT: every weight and label is one (the BASELINE configurations), so the
 // residual is yhat - 1 and a h h^T = h h^T.
-template <bool UNIT>
+// SYM2 (heavy-row partials, symmetrised by their consumer): two MMAs per
+// k-step, E += hi hi^T + hi (2 lo)^T, whose symmetric part (E + E^T) / 2 is the
+// 3xTF32 sum hi hi^T + hi lo^T + lo hi^T (2 lo is exact).
+template <bool UNIT, bool SYM2 = false>
 IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, double& gacc, int ebeg,
                              int eend, int tid) {
   using L = TcLay4;
@@ -255,6 +258,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
         for (int j = 0; j < 4; ++j) {
           hi[j] = tf32_rna(x[4 * c + j]);
           lo[j] = x[4 * c + j] - hi[j];   // fed as is: the MMA drops its low 13 bits
+          if (SYM2) lo[j] *= 2.f;
         }
         const int o = rb + ((c ^ sw) << 2);
         *reinterpret_cast<float4*>(XTH + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
@@ -274,7 +278,7 @@ IALS_DEVI int tc4_accumulate(const SweepParams& p, char* smem, Tc4State& st, dou
         const uint64_t al = make_sdesc(lo + ks * 32, 16, 512, kSwizzle64B);
         umma_tf32(st.tmem, ah, ah, idesc, 1);
         umma_tf32(st.tmem, ah, al, idesc, 1);
-        umma_tf32(st.tmem, al, ah, idesc, 1);
+        if (!SYM2) umma_tf32(st.tmem, al, ah, idesc, 1);
       }
       umma_commit(bar + xb);
     }
@@ -675,9 +679,10 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
 }
 
 // Heavy-row slices on the tensor core: each slice's partial Hessian is summed
-// from zero in TMEM (same pipelined gather / 3xTF32 MMAs as the light rows)
-// and written row-major (the layout k_heavy_solve<128> reads) with its fp64
-// partial gradient; the slices of a row are combined in k_heavy_solve.
+// from zero in TMEM (same pipelined gather as the light rows, two MMAs per
+// k-step: the non-symmetric E of tc4_accumulate<., true>) and written
+// row-major with its fp64 partial gradient; k_heavy_solve<128, ., true>
+// combines the slices of a row and takes the symmetric part.
 template <bool UNIT>
 __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
                                                           const __grid_constant__ CUtensorMap fmap,
@@ -714,7 +719,7 @@ __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
       tc_fence_before();   // ordered before the MMAs by the first chunk's barrier
     }
     double gacc = 0.0;
-    tc4_accumulate<UNIT>(p, smem, st, gacc, p.slice_begin[sl], p.slice_end[sl], tid);
+    tc4_accumulate<UNIT, true>(p, smem, st, gacc, p.slice_begin[sl], p.slice_end[sl], tid);
     float* hp = p.hpart + (size_t)sl * 128 * 128 + (size_t)tid * 128;
 #pragma unroll
     for (int c32 = 0; c32 < 4; ++c32) {
