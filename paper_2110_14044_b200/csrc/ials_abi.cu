@@ -31,6 +31,8 @@ struct ials_session {
   int device;
   cudaStream_t copy_st = nullptr;             // ials_epoch_host: host <-> device staging
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  cudaStream_t aux_st = nullptr;              // heavy-row partials beside the light rows
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   unsigned long long* err;  // device error word (ULLONG_MAX = clean)
   unsigned long long* redo; // rows the fused tensor-core sweep handed to SIMT
   char msg[512];
@@ -112,6 +114,9 @@ int ials_session_destroy(ials_session* s) {
   cudaFree(s->err);
   cudaFree(s->redo);
   if (s->copy_st) cudaStreamDestroy(s->copy_st);
+  if (s->aux_st) cudaStreamDestroy(s->aux_st);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   if (s->ev_a) cudaEventDestroy(s->ev_a);
   if (s->ev_b) cudaEventDestroy(s->ev_b);
   delete s;
@@ -474,7 +479,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
-  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, sizeof(int), st));
+  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 2 * sizeof(int), st));   // redo count, heavy slice queue
   // sub-row gathers by TMA (tile::gather4) when the fixed matrix allows it
   CUtensorMap fmap;
   memset(&fmap, 0, sizeof(fmap));
@@ -482,6 +487,21 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   if (p.vec && p.side.n_fixed > 0 && get_encode(s) == IALS_OK &&
       make_gather_map(s, &fmap, p.fixed, p.d, p.side.n_fixed, p.ldf) == IALS_OK)
     use_tma = 1;
+  // heavy-row partials run on a second stream beside the light rows (they
+  // touch disjoint rows and only read the cache), so each kernel's last wave
+  // is filled by the other's CTAs; joined before the heavy solve
+  const bool fork = p.n_light > 0 && p.n_heavy > 0;
+  cudaStream_t hst = st;
+  if (fork) {
+    if (!s->aux_st) {
+      CUDA_TRY(s, cudaStreamCreateWithFlags(&s->aux_st, cudaStreamNonBlocking));
+      CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    }
+    hst = s->aux_st;
+    CUDA_TRY(s, cudaEventRecord(s->ev_fork, st));
+    CUDA_TRY(s, cudaStreamWaitEvent(hst, s->ev_fork, 0));
+  }
   if (p.n_light > 0) {
     static bool init = false;
     if (!init) {
@@ -512,10 +532,14 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     const int threads = L::NT * L::RPC;
     const int hg = std::min(p.n_slices, 4 * kNumSMs);
     if (unit)
-      k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
+      k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, hst>>>(p, fmap, use_tma);
     else
-      k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
+      k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, hst>>>(p, fmap, use_tma);
     LAUNCH_CHECK(s);
+    if (fork) {
+      CUDA_TRY(s, cudaEventRecord(s->ev_join, hst));
+      CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_join, 0));
+    }
     k_heavy_solve<128, true, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
   }

@@ -710,7 +710,16 @@ __global__ void __launch_bounds__(128, 4) k_heavy_partial_tc4(SweepParams p,
   st.gph = 0u;
   st.fmap = use_tma ? &fmap : nullptr;
   const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
-  for (int sl = blockIdx.x; sl < p.n_slices; sl += gridDim.x) {
+  // slices from a device queue (redo_cnt[1], zeroed per pass): CTAs that
+  // start late -- beside the light-row sweep on another stream -- take fewer
+  int* queue = p.redo_cnt + 1;
+  int* next = reinterpret_cast<int*>(smem + L::OFF_FLAG) + 1;
+  for (;;) {
+    if (tid == 0) *next = atomicAdd(queue, 1);
+    __syncthreads();
+    const int sl = *next;
+    __syncthreads();
+    if (sl >= p.n_slices) break;
     {
       const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
