@@ -479,7 +479,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
-  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 2 * sizeof(int), st));   // redo count, heavy slice queue
+  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 3 * sizeof(int), st));   // redo count, slice / row queues
   // sub-row gathers by TMA (tile::gather4) when the fixed matrix allows it
   CUtensorMap fmap;
   memset(&fmap, 0, sizeof(fmap));

@@ -595,7 +595,17 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
   long long tph[8];
   // profiling: phase clocks of the CTA's rec_row-th row (dbg[32767] picks it; dbg holds 32K int64)
   const int rec_row = p.dbg ? (int)p.dbg[32767] : -1;
-  for (int task = blockIdx.x; task < p.n_light; task += gridDim.x) {
+  // rows (descending degree) from a device queue (redo_cnt[2], zeroed per
+  // pass): greedy longest-first; the next index is fetched while the current
+  // row runs
+  int* queue = p.redo_cnt + 2;
+  int* next = reinterpret_cast<int*>(smem + L::OFF_FLAG) + 2;
+  if (tid == 0) *next = atomicAdd(queue, 1);
+  __syncthreads();
+  int task = *next;
+  while (task < p.n_light) {
+    int nxt = 0;
+    if (tid == 0) nxt = atomicAdd(queue, 1);   // consumed at the end of the row
     const bool rec = ndone == rec_row && tid == 0;
     if (rec) tph[0] = clock64();
     const int row = p.light_rows[task];
@@ -672,6 +682,10 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
       for (int k = 0; k < 8; ++k) p.dbg[blockIdx.x * 8 + k] = tph[k];
     }
     ++ndone;
+    if (tid == 0) *next = nxt;
+    __syncthreads();
+    task = *next;
+    __syncthreads();   // everyone has read it before the next row's fetch lands
   }
   tc_fence_before();
   __syncthreads();
