@@ -201,7 +201,7 @@ static size_t pass_ws(int32_t n_rows, int32_t n_fixed, int32_t b, int32_t n_slic
   const size_t bt = block_tile(b);
   return al256(size_t(n_rows) * b * 4) + al256(size_t(n_slices) * bt * bt * 4) +
          al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4) +
-         al256(size_t(kTcPKS) * 4) + al256(size_t(n_rows) * 4 + 16) +
+         al256(size_t(kTcPKS) * 4) + al256(size_t(n_rows) * 4 + 32) +
          al256(size_t(n_rows) * b * 4) +
          (b <= kCompactMaxB ? al256(size_t(n_fixed) * compact_ld(b) * 4) : 0);
 }
@@ -479,7 +479,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
-  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 3 * sizeof(int), st));   // redo count, slice / row queues
+  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 5 * sizeof(int), st));   // redo count, slice / row queues
   // sub-row gathers by TMA (tile::gather4) when the fixed matrix allows it
   CUtensorMap fmap;
   memset(&fmap, 0, sizeof(fmap));
@@ -555,6 +555,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     SweepParams q = p;
     q.light_rows = p.redo_rows;
     q.n_light_dev = p.redo_cnt;
+    q.queue = p.redo_cnt + 4;   // zeroed with the redo count
     k_sweep_light<128><<<simt_sm * kNumSMs, L::NT * L::RPC, L::CTA_BYTES, st>>>(q);
     LAUNCH_CHECK(s);
   }
@@ -687,7 +688,10 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     }
     const int need = (p.n_light + L::RPC - 1) / L::RPC;
     const int grid = std::min(need, per_sm * kNumSMs);
-    k_sweep_light<BT><<<grid, threads, L::CTA_BYTES, st>>>(p);
+    SweepParams q = p;
+    q.queue = p.redo_cnt + 3;   // zeroed below; the redo launch of the fused path uses [4]
+    CUDA_TRY(s, cudaMemsetAsync(q.queue, 0, sizeof(int), st));
+    k_sweep_light<BT><<<grid, threads, L::CTA_BYTES, st>>>(q);
     LAUNCH_CHECK(s);
   }
   if (p.n_heavy > 0) {
@@ -757,8 +761,8 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   float* tpl_simt = reinterpret_cast<float*>(w);
   w += al256(size_t(kTcPKS) * 4);
   p.redo_cnt = reinterpret_cast<int*>(w);
-  p.redo_rows = reinterpret_cast<int*>(w + 16);
-  w += al256(size_t(side->n_rows) * 4 + 16);
+  p.redo_rows = reinterpret_cast<int*>(w + 32);   // [0..7]: redo count, work queues
+  w += al256(size_t(side->n_rows) * 4 + 32);
   p.drow = reinterpret_cast<float*>(w);
   w += al256(size_t(side->n_rows) * b * 4);
   if (b <= kCompactMaxB && !use_tc && side->n_fixed > 0) {

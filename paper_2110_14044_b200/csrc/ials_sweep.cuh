@@ -80,6 +80,7 @@ struct SweepParams {
   unsigned long long* redo_total;
   float cond_max;
   const int* n_light_dev;  // if set, k_sweep_light reads its row count here
+  int* queue;              // if set, k_sweep_light takes its rows from this zeroed counter
   float* drow;             // [n_rows][b] per-row d of the fused sweep (k_pass_cache)
   int fb0;                 // column of the block in `fixed` (b0, or 0 for a compact copy)
 };
@@ -119,7 +120,8 @@ struct Lay {
   static constexpr int OFF_YF = OFF_Y + BT;
   static constexpr int OFF_ID = OFF_YF + BT;
   static constexpr int OFF_D = OFF_ID + BT;
-  static constexpr int FLOATS = OFF_D + BT;
+  static constexpr int OFF_Q = OFF_D + BT;   // the team's next row (device queue)
+  static constexpr int FLOATS = OFF_Q + 4;
   static constexpr int TEAM_BYTES = FLOATS * 4;
   static constexpr int CTA_BYTES = TEAM_BYTES * RPC;
 };
@@ -638,9 +640,21 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   float* sm = smem_all + team * L::FLOATS;
   zero_stage<BT>(sm, tid);
   team_sync<L::NW>(team);
-  // persistent: rows are in descending-degree order, strided over the grid
+  // persistent: rows are in descending-degree order, taken from a device
+  // queue (greedy longest-first; the next index is fetched during the row)
+  // or strided over the grid
   const int n_light = p.n_light_dev ? *p.n_light_dev : p.n_light;
-  for (int task = blockIdx.x * L::RPC + team; task < n_light; task += gridDim.x * L::RPC) {
+  int* qslot = reinterpret_cast<int*>(sm + L::OFF_Q);
+  int task = blockIdx.x * L::RPC + team;
+  if (p.queue) {
+    if (tid == 0) *qslot = atomicAdd(p.queue, 1);
+    team_sync<L::NW>(team);
+    task = *qslot;
+    team_sync<L::NW>(team);
+  }
+  for (; task < n_light;) {
+    int nxt = 0;
+    if (p.queue && tid == 0) nxt = atomicAdd(p.queue, 1);
     const int row = p.light_rows[task];
     const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
     Tiles<BT> T;
@@ -652,6 +666,14 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
     if (tid < p.b) p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
     cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);
     team_sync<L::NW>(team);
+    if (p.queue) {
+      if (tid == 0) *qslot = nxt;
+      team_sync<L::NW>(team);
+      task = *qslot;
+      team_sync<L::NW>(team);
+    } else {
+      task += gridDim.x * L::RPC;
+    }
   }
 }
 
