@@ -338,19 +338,36 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
     tmem_wait_ld();
     if (watch && pp == 8) acc[6] = clock64();
     if (warp == (c0 >> 5)) {
-      // the diagonal block's rows are lanes base..base+7 of this warp: every
-      // lane gathers the block with shuffles and factors it redundantly (a
-      // short dependent chain; a lane-parallel version is shuffle-latency
-      // bound), lane `base` publishes it
+      // the diagonal block's rows are lanes base..base+7 of this warp: they
+      // stage their panel entries and y in shared memory, every lane reads
+      // the block back (18 broadcast loads instead of 44 shuffles: this warp's
+      // instruction count is the panel's critical path) and factors it
+      // redundantly (a short dependent chain), lane `base` publishes it
       const int base = c0 & 31;
+      float* SG = reinterpret_cast<float*>(smem + L::OFF_LI);   // free until the backward solve
+      if (lane >= base && lane < base + 8) {
+        const int q = lane - base;
+        reinterpret_cast<float4*>(SG)[2 * q] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(SG)[2 * q + 1] = make_float4(v[4], v[5], v[6], v[7]);
+        SG[64 + q] = yi;
+      }
+      __syncwarp();
       float a[8][8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-#pragma unroll
-        for (int m = 0; m <= q; ++m) a[q][m] = __shfl_sync(full, v[m], base + q);
+      for (int q = 0; q < 8; ++q) {
+        const float4 x0 = reinterpret_cast<const float4*>(SG)[2 * q];
+        const float4 x1 = reinterpret_cast<const float4*>(SG)[2 * q + 1];
+        a[q][0] = x0.x; a[q][1] = x0.y; a[q][2] = x0.z; a[q][3] = x0.w;
+        a[q][4] = x1.x; a[q][5] = x1.y; a[q][6] = x1.z; a[q][7] = x1.w;
+      }
       float py[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) py[q] = __shfl_sync(full, yi, base + q);
+      {
+        const float4 y0 = reinterpret_cast<const float4*>(SG + 64)[0];
+        const float4 y1 = reinterpret_cast<const float4*>(SG + 64)[1];
+        py[0] = y0.x; py[1] = y0.y; py[2] = y0.z; py[3] = y0.w;
+        py[4] = y1.x; py[5] = y1.y; py[6] = y1.z; py[7] = y1.w;
+      }
+      __syncwarp();   // SG is rewritten by the next panel's block
       float rinv[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -358,7 +375,8 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         // 1/pivot, which the cancellation test (record_block) flags; the
         // row's own numbers are then discarded and it is redone in FP32
         const float dk = a[k][k];
-        const float r = rsqrtf(dk);
+        float r;   // MUFU.RSQ without the denormal rescale (a denormal pivot is rejected anyway)
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(dk));
         rinv[k] = r;
         a[k][k] = dk * r;
 #pragma unroll
