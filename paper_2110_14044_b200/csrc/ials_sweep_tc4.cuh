@@ -401,7 +401,8 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
 #pragma unroll
           for (int m = 0; m < 8; ++m) w[m] = (m <= q) ? a[q][m] : 0.f;
           reinterpret_cast<float4*>(DG)[2 * q] = make_float4(w[0], w[1], w[2], w[3]);
-          reinterpret_cast<float4*>(DG)[2 * q + 1] = make_float4(w[4], w[5], w[6], w[7]);
+          // readers use entries m <= q only: rows 0..3 have no upper half to store
+          if (q >= 4) reinterpret_cast<float4*>(DG)[2 * q + 1] = make_float4(w[4], w[5], w[6], w[7]);
         }
         reinterpret_cast<float4*>(RV)[0] = make_float4(rinv[0], rinv[1], rinv[2], rinv[3]);
         reinterpret_cast<float4*>(RV)[1] = make_float4(rinv[4], rinv[5], rinv[6], rinv[7]);
