@@ -152,9 +152,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tmem_ld32(raddr + c32, v);
     tmem_wait_ld();
     if (row < job.m_rows && nk > 0) {
+      if (c32 + 32 <= job.n && (job.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(job.out) & 15) == 0) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (c32 + j < job.n) o[c32 + j] = job.scale * v[j];
+        for (int j = 0; j < 32; j += 4)   // 16-byte stores: 8 per thread instead of 32
+          *reinterpret_cast<float4*>(o + c32 + j) =
+              make_float4(job.scale * v[j], job.scale * v[j + 1], job.scale * v[j + 2], job.scale * v[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c32 + j < job.n) o[c32 + j] = job.scale * v[j];
+      }
     } else if (row < job.m_rows) {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
