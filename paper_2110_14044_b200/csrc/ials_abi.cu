@@ -883,6 +883,9 @@ static void gram_plan(int n, int d, int* splits, int* span) {
   const int mt = (d + 127) / 128;
   int S = std::max((n + 2047) / 2048, (2 * kNumSMs + mt - 1) / mt);
   S = std::max(1, std::min(S, std::max(1, n / 32)));
+  // fill the last wave (one CTA per SM): as many splits as the waves hold
+  const int waves = (mt * S + kNumSMs - 1) / kNumSMs;
+  S = std::max(S, std::min(std::max(1, n / 32), waves * kNumSMs / mt));
   int sp = rup((n + S - 1) / S, kGemmKC);
   *span = std::max(sp, kGemmKC);
   *splits = std::max(1, (n + *span - 1) / *span);
