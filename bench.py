@@ -38,6 +38,8 @@ CONFIGS = {
     "sw-b64": ("mid", 256, 64, "configs[2] d=256 b=64"),
     "sw-b128": ("mid", 256, 128, "configs[2] d=256 b=128"),
     "sw-b256": ("mid", 256, 256, "configs[2] d=256 b=d (iALS case)"),
+    "d64": ("mid", 64, 64, "metric d-grid: ML20M-shaped, d=64 b=d (b=128 > d)"),
+    "d512": ("mid", 512, 128, "metric d-grid: ML20M-shaped, d=512 b=128"),
     "L1": ("mid", 1024, 128, "configs[3] ML20M-shaped 136,677x20,108 10.0M, d=1024 b=128"),
     "L2": ("mid", 2048, 128, "configs[3] ML20M-shaped, d=2048 b=128"),
     "msd": ("msd", 2048, 128, "configs[4] MSD-shaped 571,355x41,140 33.6M, d=2048 b=128"),
