@@ -91,7 +91,7 @@ struct Cfg;
 // RPC: row teams per CTA; KC: entries per staged chunk.
 template <> struct Cfg<8>   { static constexpr int ST = 8,  SR = 1, SC = 2, NW = 1,  RPC = 4, KC = 32; };
 template <> struct Cfg<16>  { static constexpr int ST = 16, SR = 2, SC = 4, NW = 1,  RPC = 4, KC = 32; };
-template <> struct Cfg<32>  { static constexpr int ST = 32, SR = 4, SC = 8, NW = 1,  RPC = 4, KC = 16; };
+template <> struct Cfg<32>  { static constexpr int ST = 16, SR = 2, SC = 4, NW = 1,  RPC = 4, KC = 16; };
 template <> struct Cfg<64>  { static constexpr int ST = 32, SR = 4, SC = 8, NW = 3,  RPC = 1, KC = 32; };
 template <> struct Cfg<128> { static constexpr int ST = 32, SR = 4, SC = 8, NW = 10, RPC = 1, KC = 32; };
 template <> struct Cfg<256> { static constexpr int ST = 32, SR = 4, SC = 8, NW = 12, RPC = 1, KC = 16; };
