@@ -266,12 +266,14 @@ def run_ours(args, cfg_key):
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         n_launch0 = int(eng.lib.ials_launch_count())
+        eng.sess.tc_redo_rows(reset=True)
         t_start.record(stream)
         for s in range(args.steps):
             eng.epoch(W, H, cache, b, ALPHA0, events=events[s])
         t_end.record(stream)
         n_launches = int(eng.lib.ials_launch_count()) - n_launch0
         torch.cuda.synchronize(dev)
+    tc_redo = eng.sess.tc_redo_rows()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -379,6 +381,9 @@ def run_ours(args, cfg_key):
             "clocks": clk.summary(),
             "gpu_launches": n_launches,
             "gpu_launches_model": launches_per_epoch * args.steps,
+            # rows the fused tensor-core sweep's cancellation guard handed to the
+            # FP32 sweep during the timed epochs (numerics transparency)
+            "tc_redo_rows": tc_redo,
         }
         print(json.dumps(line))
     if world > 1:
