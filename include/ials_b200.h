@@ -114,8 +114,9 @@ int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pi
 
 /* Sweep engine for block widths 33..128: 0 = FP32 SIMT sweep, 1 = tcgen05
  * (3xTF32) wave kernels for b in 33..128, 2 = fused tcgen05 sweep for b in
- * 65..128 (4 rows in flight per SM; rows whose Cholesky pivots cancel more
- * than IALS_TC_COND (default 256) x are re-solved by the SIMT sweep).
+ * 33..128 (4 rows in flight per SM; rows whose Cholesky pivots cancel more
+ * than IALS_TC_COND (default 256) x -- 16 x for b <= 64 -- are re-solved by
+ * the SIMT sweep).
  * Returns the previous setting.  The IALS_TC environment variable sets the
  * initial mode (default 2). */
 int ials_set_tensor_cores(int enable);
@@ -193,7 +194,7 @@ int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sch
 int ials_epoch_events(void* const* events, int32_t n);
 
 /* Extra workspace ials_epoch can use for its tensor-core GEMM path (b in
- * 65..128 with the fused sweep): K-major copies of W and H and the Gramian
+ * 33..128 with the fused sweep): K-major copies of W and H and the Gramian
  * split partials.  Pass a workspace of ials_workspace_bytes(...) plus this
  * to enable it; with less, the epoch uses the FP32 SIMT GEMMs. */
 size_t ials_epoch_tc_bytes(int32_t n_users, int32_t n_items, int32_t d, int32_t b);

@@ -75,11 +75,16 @@ static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p)
 int64_t ials_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+static bool tc4_enabled();
+// Register/shared tile width of a block of b columns.  With the fused
+// tensor-core sweep (the default) widths 33..64 also use the 128 tile (the
+// padding is idle tensor-core work; the factorisation chain is half of the
+// SIMT sweep's), under a stricter cancellation guard (tc_cond_for).
 static int block_tile(int b) {
   if (b <= 8) return 8;
   if (b <= 16) return 16;
   if (b <= 32) return 32;
-  if (b <= 64) return 64;
+  if (b <= 64) return tc4_enabled() ? 128 : 64;
   if (b <= 128) return 128;
   return 256;
 }
@@ -396,7 +401,7 @@ static int g_tc = -1;  // -1: not yet read from IALS_TC
 static bool tc_enabled() {
   if (g_tc < 0) {
     const char* e = getenv("IALS_TC");
-    // default: the fused tensor-core sweep (mode 2) for b in 65..128
+    // default: the fused tensor-core sweep (mode 2) for b in 33..128
     g_tc = (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 2;
   }
   return g_tc == 1;
@@ -472,7 +477,7 @@ static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, ui
   return IALS_OK;
 }
 
-// BT = 128, b > 64: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
+// BT = 128, b > 32: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
 // heavy rows on the SIMT slice kernels.
 static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<128>;
@@ -675,7 +680,7 @@ template <int BT>
 static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<BT>;
   if (BT == 128 && p.b > 32 && tc_enabled()) return launch_sweep_tc128(s, p, st);
-  if (BT == 128 && p.b > 64 && tc4_enabled()) return launch_sweep_tc4(s, p, nnz, st);
+  if (BT == 128 && p.b > 32 && tc4_enabled()) return launch_sweep_tc4(s, p, nnz, st);
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
   const int threads = L::NT * L::RPC;
@@ -779,7 +784,10 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.vec = (b % 4 == 0) && (reinterpret_cast<uintptr_t>(compact) % 16 == 0);
   }
   p.redo_total = s->redo;
-  p.cond_max = tc_cond_max();
+  // narrow blocks in the 128 tile: a pivot losing more than 16x of its
+  // diagonal already goes to the FP32 sweep (ill-conditioned heavy rows at
+  // b = 64 slip under the 256x limit, tests/test_gpu_parity.py heavy rows)
+  p.cond_max = b <= 64 ? std::min(tc_cond_max(), 16.f) : tc_cond_max();
   p.n_light_dev = nullptr;
   if (proj_in) {   // precomputed by the caller (ials_side_pass_projected)
     proj = const_cast<float*>(proj_in);
@@ -1144,13 +1152,13 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   float* part = reinterpret_cast<float*>(ws + slab_bytes);
   char* pws = ws + slab_bytes + gbytes;
   size_t pbytes = ws_bytes - slab_bytes - gbytes;
-  // tensor-core GEMMs (with the fused tensor-core sweep, b in 65..128): the
+  // tensor-core GEMMs (with the fused tensor-core sweep, b in 33..128): the
   // K-major copies live at the end of the workspace when it has room
   const size_t tcb = tc_gemm_bytes(users->n_rows, items->n_rows, d, b);
   const size_t pass_need =
       std::max(pass_ws(users->n_rows, users->n_fixed, b, user_sched->n_slices, user_sched->n_heavy),
                pass_ws(items->n_rows, items->n_fixed, b, item_sched->n_slices, item_sched->n_heavy));
-  const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 64 && d % 4 == 0 &&
+  const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 32 && d % 4 == 0 &&
                        ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= pass_need + tcb &&
                        get_encode(s) == IALS_OK;

@@ -1,5 +1,6 @@
 // ials_sweep_tc4.cuh -- fused tensor-core light-row sweep for block widths
-// 65..128 (BT = 128), four CTAs (rows in flight) per SM.
+// 33..128 (BT = 128; widths <= 64 are zero-padded), four CTAs (rows in
+// flight) per SM.
 //
 // Per row, one CTA of 128 threads (thread i <-> TMEM lane i <-> matrix row i):
 //   1. TMEM D := alpha0*slab[pi,pi] + lam*I   (tcgen05.st from the packed

@@ -144,14 +144,14 @@ class GpuOps:
                                               self._stream())
         self.sess.check(rc, "cache_correct")
 
-    # ---- tensor-core GEMMs on this rank's row shards (b in 65..128, like
+    # ---- tensor-core GEMMs on this rank's row shards (b in 33..128, like
     # ials_epoch): K-major copies of a shard live in a per-shard workspace
     def tc_enable(self, M_rows, b):
         """Keep K-major copies of the shard ``M_rows`` (a row slice of W or H)
         for block width ``b``; returns False if the tensor-core path does not
         apply (then gram / sweep use the FP32 SIMT kernels)."""
         d = M_rows.shape[1]
-        if not (64 < b <= 128 and d % 4 == 0 and M_rows.stride(0) % 4 == 0
+        if not (32 < b <= 128 and d % 4 == 0 and M_rows.stride(0) % 4 == 0
                 and M_rows.data_ptr() % 16 == 0):
             return False
         n = M_rows.shape[0]

@@ -149,7 +149,7 @@ class DeviceTrainer:
         marks = [ev()]
         marks[0].record()
         if self.uniform:
-            # one ials_epoch call (tensor-core GEMMs when b in 65..128), with
+            # one ials_epoch call (tensor-core GEMMs when b in 33..128), with
             # the phase events recorded inside it
             nb = len(self.spans)
             evs = [ev() for _ in range(2 + 4 * nb)]
