@@ -47,25 +47,70 @@ __global__ void __launch_bounds__(256)
       const int v = gl + m * LPN;
       w[m] = v < d4 ? __ldg(wr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int eb = e0; eb < e1; eb += GPW) {
-      const int e = eb + sub;
-      float s = 0.f;
-      if (e < e1) {
-        const float4* hr = reinterpret_cast<const float4*>(H + (size_t)__ldg(cols + e) * ldh);
+    if (NV < 4) {   // short rows (d <= 128 at LPN 8..32): one entry per step
+      for (int eb = e0; eb < e1; eb += GPW) {
+        const int e = eb + sub;
+        float s = 0.f;
+        if (e < e1) {
+          const float4* hr = reinterpret_cast<const float4*>(H + (size_t)__ldg(cols + e) * ldh);
 #pragma unroll
-        for (int m = 0; m < NV; ++m) {
-          const int v = gl + m * LPN;
-          if (v < d4) {
-            const float4 h = __ldg(hr + v);
-            s = fmaf(w[m].x, h.x, s);
-            s = fmaf(w[m].y, h.y, s);
-            s = fmaf(w[m].z, h.z, s);
-            s = fmaf(w[m].w, h.w, s);
+          for (int m = 0; m < NV; ++m) {
+            const int v = gl + m * LPN;
+            if (v < d4) {
+              const float4 h = __ldg(hr + v);
+              s = fmaf(w[m].x, h.x, s);
+              s = fmaf(w[m].y, h.y, s);
+              s = fmaf(w[m].z, h.z, s);
+              s = fmaf(w[m].w, h.w, s);
+            }
           }
         }
+        s = group_sum<LPN>(s);
+        if (e < e1 && gl == 0) out[e] = s;
       }
-      s = group_sum<LPN>(s);
-      if (e < e1 && gl == 0) out[e] = s;
+      continue;
+    }
+    // two entries per group per step: both rows' loads are in flight before
+    // the first dot product (latency-bound gathers); the next step's column
+    // ids are loaded a step ahead.  Per entry the same fixed-order sum
+    // (L1, d = 1024: 3.54 -> 2.69 ms per launch).
+    int nc0 = (e0 + sub < e1) ? __ldg(cols + e0 + sub) : -1;
+    int nc1 = (e0 + GPW + sub < e1) ? __ldg(cols + e0 + GPW + sub) : -1;
+    for (int eb = e0; eb < e1; eb += 2 * GPW) {
+      const int c0 = nc0, c1 = nc1;
+      {
+        const int f0 = eb + 2 * GPW + sub, f1 = f0 + GPW;
+        nc0 = f0 < e1 ? __ldg(cols + f0) : -1;
+        nc1 = f1 < e1 ? __ldg(cols + f1) : -1;
+      }
+      float4 h0[NV], h1[NV];
+      const float4* hr0 = reinterpret_cast<const float4*>(H + (size_t)max(c0, 0) * ldh);
+      const float4* hr1 = reinterpret_cast<const float4*>(H + (size_t)max(c1, 0) * ldh);
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        const int v = gl + m * LPN;
+        h0[m] = (c0 >= 0 && v < d4) ? __ldg(hr0 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        h1[m] = (c1 >= 0 && v < d4) ? __ldg(hr1 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        const int v = gl + m * LPN;
+        if (v < d4) {
+          s0 = fmaf(w[m].x, h0[m].x, s0);
+          s0 = fmaf(w[m].y, h0[m].y, s0);
+          s0 = fmaf(w[m].z, h0[m].z, s0);
+          s0 = fmaf(w[m].w, h0[m].w, s0);
+          s1 = fmaf(w[m].x, h1[m].x, s1);
+          s1 = fmaf(w[m].y, h1[m].y, s1);
+          s1 = fmaf(w[m].z, h1[m].z, s1);
+          s1 = fmaf(w[m].w, h1[m].w, s1);
+        }
+      }
+      s0 = group_sum<LPN>(s0);
+      s1 = group_sum<LPN>(s1);
+      if (c0 >= 0 && gl == 0) out[eb + sub] = s0;
+      if (c1 >= 0 && gl == 0) out[eb + GPW + sub] = s1;
     }
   }
 }
