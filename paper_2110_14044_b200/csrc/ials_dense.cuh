@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256)
       const int v = gl + m * LPN;
       w[m] = v < d4 ? __ldg(wr + v) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (NV < 4) {   // short rows (d <= 128 at LPN 8..32): one entry per step
+    if constexpr (NV != 8) {   // one entry per step
       for (int eb = e0; eb < e1; eb += GPW) {
         const int e = eb + sub;
         float s = 0.f;
@@ -68,12 +68,13 @@ __global__ void __launch_bounds__(256)
         s = group_sum<LPN>(s);
         if (e < e1 && gl == 0) out[e] = s;
       }
-      continue;
-    }
+    } else {
     // two entries per group per step: both rows' loads are in flight before
     // the first dot product (latency-bound gathers); the next step's column
     // ids are loaded a step ahead.  Per entry the same fixed-order sum
-    // (L1, d = 1024: 3.54 -> 2.69 ms per launch).
+    // (measured per epoch: d = 1024 (NV 8) 3.57 -> 2.70 ms; slower at NV 16,
+    // d = 2048: 8.4 -> 17.7 ms, two rows of registers halve the occupancy; and
+    // at NV 4, d = 64..512: 1.41 -> 2.04 ms at d = 512 -- NV 8 only).
     int nc0 = (e0 + sub < e1) ? __ldg(cols + e0 + sub) : -1;
     int nc1 = (e0 + GPW + sub < e1) ? __ldg(cols + e0 + GPW + sub) : -1;
     for (int eb = e0; eb < e1; eb += 2 * GPW) {
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(256)
       s1 = group_sum<LPN>(s1);
       if (c0 >= 0 && gl == 0) out[eb + sub] = s0;
       if (c1 >= 0 && gl == 0) out[eb + GPW + sub] = s1;
+    }
     }
   }
 }
