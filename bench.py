@@ -315,7 +315,7 @@ def run_ours(args, cfg_key):
         "traffic_unit": "DRAM bytes per side pass (dram__bytes_read.sum + dram__bytes_write.sum, ncu)",
         "traffic_source": traffic_src,
         "algorithmic_bytes_per_side_pass": rl["Q_sw"] / (2 * rl["B"]),
-        "kernel": "block sweep per side pass (b 65..128: k_sweep_tc4 + k_heavy_partial_tc4/solve + "
+        "kernel": "block sweep per side pass (b 33..128: k_sweep_tc4 + k_heavy_partial_tc4/solve + "
                   "k_pass_cache; else k_sweep_light + k_heavy_*)",
         "per_launch_algorithmic": (rl["F_sw"] if roof["unit"] == "TFLOP/s" else rl["Q_sw"]) / (2 * rl["B"]),
         "avg_launch_ms": round(sweep_ms / (2 * rl["B"]), 4),

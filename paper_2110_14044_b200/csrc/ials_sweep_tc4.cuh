@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
 // CTAs/SM 502 / 692 us (user / item side) against 539 / 972 us unpipelined;
 // U = 2 (80 registers, 3 CTAs/SM) 568 / 812 us; capping registers for 5 or 6
 // CTAs/SM spills (675 / 875, 1045 / 1155 us).
-template <int U>
+template <int U, bool VEC>
 __global__ void __launch_bounds__(256, 4) k_pass_cache_flat(SweepParams p, long long nnz) {
   const int lane = threadIdx.x & 31, g = lane & 7, sub = lane >> 3;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(256, 4) k_pass_cache_flat(SweepParams p, long 
         const int c = 32 * q + 4 * g;
         x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (live && c < b) {
-          if (p.vec) {
+          if (VEC) {   // b % 4 == 0: c < b covers the whole float4
             x[u][q] = __ldg(reinterpret_cast<const float4*>(xr + c));
           } else {
             x[u][q].x = __ldg(xr + c);
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(256, 4) k_pass_cache_flat(SweepParams p, long 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int c = 32 * q + 4 * g;
-          if (p.vec) {
+          if (VEC) {
             const float4 t = (c < b) ? __ldg(reinterpret_cast<const float4*>(dr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
             dv[4 * q] = t.x; dv[4 * q + 1] = t.y; dv[4 * q + 2] = t.z; dv[4 * q + 3] = t.w;
           } else {
@@ -948,11 +948,11 @@ __global__ void __launch_bounds__(256, 4) k_pass_cache_flat(SweepParams p, long 
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = 32 * q + 4 * g;
-        if (c < b) {   // zero-padded lanes add +0 terms, as the scalar path skipped them
+        if (c < b) {   // columns >= b are skipped (not added as +0 terms)
           s = fmaf(x[u][q].x, dv[4 * q], s);
-          if (c + 1 < b) s = fmaf(x[u][q].y, dv[4 * q + 1], s);
-          if (c + 2 < b) s = fmaf(x[u][q].z, dv[4 * q + 2], s);
-          if (c + 3 < b) s = fmaf(x[u][q].w, dv[4 * q + 3], s);
+          if (VEC || c + 1 < b) s = fmaf(x[u][q].y, dv[4 * q + 1], s);
+          if (VEC || c + 2 < b) s = fmaf(x[u][q].z, dv[4 * q + 2], s);
+          if (VEC || c + 3 < b) s = fmaf(x[u][q].w, dv[4 * q + 3], s);
         }
       }
       s += __shfl_xor_sync(0xffffffffu, s, 1);
