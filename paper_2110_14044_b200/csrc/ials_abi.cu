@@ -567,8 +567,8 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   if (p.n_light + p.n_slices > 0) {
     if (p.side.rows && nnz > 0) {   // entry-parallel: no per-row setup, full load balance
       const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);
-      if (p.vec) k_pass_cache_flat<1, true><<<(int)g, 256, 0, st>>>(p, nnz);
-      else k_pass_cache_flat<1, false><<<(int)g, 256, 0, st>>>(p, nnz);
+      if (p.vec) k_pass_cache_flat<true, 8><<<(int)g, 256, 0, st>>>(p, nnz);
+      else k_pass_cache_flat<false, 8><<<(int)g, 256, 0, st>>>(p, nnz);
     } else {
       k_pass_cache<<<p.n_light + p.n_slices, 256, 0, st>>>(p);
     }

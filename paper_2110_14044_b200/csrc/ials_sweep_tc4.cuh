@@ -870,96 +870,86 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
 // (bit-identical results).  Measured at L1 (ncu, per launch): U = 1 at 4
 // CTAs/SM 502 / 692 us (user / item side) against 539 / 972 us unpipelined;
 // U = 2 (80 registers, 3 CTAs/SM) 568 / 812 us; capping registers for 5 or 6
-// CTAs/SM spills (675 / 875, 1045 / 1155 us).
-template <int U, bool VEC>
-__global__ void __launch_bounds__(256, 4) k_pass_cache_flat(SweepParams p, long long nnz) {
-  const int lane = threadIdx.x & 31, g = lane & 7, sub = lane >> 3;
+// CTAs/SM spills (675 / 875, 1045 / 1155 us).  The vectorised variant (b % 4
+// == 0, no per-element width tests) cut the instruction count 428M -> 271M
+// (387 / 574 us); 4 lanes per entry executes 27% fewer instructions but needs
+// 123 registers (2 CTAs/SM): 403 / 738 us.
+template <bool VEC, int LPE>
+__global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(SweepParams p, long long nnz) {
+  constexpr int EPW = 32 / LPE, NQ = 128 / (4 * LPE);   // entries per warp step, float4 per lane
+  const int lane = threadIdx.x & 31, g = lane % LPE, sub = lane / LPE;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const long long per = ((nnz + nwarps - 1) / nwarps + 4 * U - 1) / (4 * U) * (4 * U);
+  const long long per = ((nnz + nwarps - 1) / nwarps + EPW - 1) / EPW * EPW;
   const long long beg = wid * per, end = min(nnz, beg + per);
   const int b = p.b;
   int cur = -1;
-  float dv[16];
+  float dv[4 * NQ];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) dv[j] = 0.f;
-  int nrow[U], ncol[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const long long e = beg + 4 * u + sub;
-    nrow[u] = e < end ? __ldg(p.side.rows + e) : -1;
-    ncol[u] = e < end ? __ldg(p.side.cols + e) : 0;
+  for (int j = 0; j < 4 * NQ; ++j) dv[j] = 0.f;
+  int nrow, ncol;
+  {
+    const long long e = beg + sub;
+    nrow = e < end ? __ldg(p.side.rows + e) : -1;
+    ncol = e < end ? __ldg(p.side.cols + e) : 0;
   }
-  for (long long e0 = beg; e0 < end; e0 += 4 * U) {   // warp-uniform trip count (shuffles below)
-    int row[U], col[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      row[u] = nrow[u];
-      col[u] = ncol[u];
-      const long long e = e0 + 4 * U + 4 * u + sub;
-      nrow[u] = e < end ? __ldg(p.side.rows + e) : -1;
-      ncol[u] = e < end ? __ldg(p.side.cols + e) : 0;
+  for (long long e0 = beg; e0 < end; e0 += EPW) {   // warp-uniform trip count (shuffles below)
+    const int row = nrow, col = ncol;
+    {
+      const long long e = e0 + EPW + sub;
+      nrow = e < end ? __ldg(p.side.rows + e) : -1;
+      ncol = e < end ? __ldg(p.side.cols + e) : 0;
     }
-    float4 x[U][4];
-    long long pos[U];
-    float cold[U];
+    const bool live = row >= 0;
+    float4 x[NQ];
+    const float* xr = p.fixed + (size_t)col * p.ldf + p.fb0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool live = row[u] >= 0;
-      const float* xr = p.fixed + (size_t)col[u] * p.ldf + p.fb0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 32 * q + 4 * g;
-        x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (live && c < b) {
-          if (VEC) {   // b % 4 == 0: c < b covers the whole float4
-            x[u][q] = __ldg(reinterpret_cast<const float4*>(xr + c));
-          } else {
-            x[u][q].x = __ldg(xr + c);
-            if (c + 1 < b) x[u][q].y = __ldg(xr + c + 1);
-            if (c + 2 < b) x[u][q].z = __ldg(xr + c + 2);
-            if (c + 3 < b) x[u][q].w = __ldg(xr + c + 3);
-          }
+    for (int q = 0; q < NQ; ++q) {
+      const int c = 4 * LPE * q + 4 * g;
+      x[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live && c < b) {
+        if (VEC) {   // b % 4 == 0: c < b covers the whole float4
+          x[q] = __ldg(reinterpret_cast<const float4*>(xr + c));
+        } else {
+          x[q].x = __ldg(xr + c);
+          if (c + 1 < b) x[q].y = __ldg(xr + c + 1);
+          if (c + 2 < b) x[q].z = __ldg(xr + c + 2);
+          if (c + 3 < b) x[q].w = __ldg(xr + c + 3);
         }
       }
-      const long long e = e0 + 4 * u + sub;
-      pos[u] = (live && g == 0) ? (p.side.pos ? (long long)__ldg(p.side.pos + e) : e) : 0;
-      cold[u] = (live && g == 0) ? p.cache[pos[u]] : 0.f;
     }
+    const long long e = e0 + sub;
+    const long long pos = (live && g == 0) ? (p.side.pos ? (long long)__ldg(p.side.pos + e) : e) : 0;
+    const float cold = (live && g == 0) ? p.cache[pos] : 0.f;
+    if (live && row != cur) {
+      const float* dr = p.drow + (size_t)row * b;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool live = row[u] >= 0;
-      if (live && row[u] != cur) {
-        const float* dr = p.drow + (size_t)row[u] * b;
+      for (int q = 0; q < NQ; ++q) {
+        const int c = 4 * LPE * q + 4 * g;
+        if (VEC) {
+          const float4 t = (c < b) ? __ldg(reinterpret_cast<const float4*>(dr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          dv[4 * q] = t.x; dv[4 * q + 1] = t.y; dv[4 * q + 2] = t.z; dv[4 * q + 3] = t.w;
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = 32 * q + 4 * g;
-          if (VEC) {
-            const float4 t = (c < b) ? __ldg(reinterpret_cast<const float4*>(dr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            dv[4 * q] = t.x; dv[4 * q + 1] = t.y; dv[4 * q + 2] = t.z; dv[4 * q + 3] = t.w;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dv[4 * q + j] = (c + j < b) ? __ldg(dr + c + j) : 0.f;
-          }
-        }
-        cur = row[u];
-      }
-      float s = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 32 * q + 4 * g;
-        if (c < b) {   // columns >= b are skipped (not added as +0 terms)
-          s = fmaf(x[u][q].x, dv[4 * q], s);
-          if (VEC || c + 1 < b) s = fmaf(x[u][q].y, dv[4 * q + 1], s);
-          if (VEC || c + 2 < b) s = fmaf(x[u][q].z, dv[4 * q + 2], s);
-          if (VEC || c + 3 < b) s = fmaf(x[u][q].w, dv[4 * q + 3], s);
+          for (int j = 0; j < 4; ++j) dv[4 * q + j] = (c + j < b) ? __ldg(dr + c + j) : 0.f;
         }
       }
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      if (live && g == 0) p.cache[pos[u]] = cold[u] - s;
+      cur = row;
     }
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = 4 * LPE * q + 4 * g;
+      if (c < b) {   // columns >= b are skipped (not added as +0 terms)
+        s = fmaf(x[q].x, dv[4 * q], s);
+        if (VEC || c + 1 < b) s = fmaf(x[q].y, dv[4 * q + 1], s);
+        if (VEC || c + 2 < b) s = fmaf(x[q].z, dv[4 * q + 2], s);
+        if (VEC || c + 3 < b) s = fmaf(x[q].w, dv[4 * q + 3], s);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < LPE; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (live && g == 0) p.cache[pos] = cold - s;
   }
 }
 
