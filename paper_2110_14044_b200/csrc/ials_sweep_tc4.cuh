@@ -864,9 +864,9 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
 // redid) in registers, reloading it only when its entries cross into the
 // next row.  No per-row setup and no row-length imbalance.  Latency-bound
 // (a dependent ids -> sub-row -> cache chain per entry): the loop is software
-// pipelined -- the next batch's ids are loaded one batch ahead, and a batch
-// of U x 4 entries issues all its sub-row and cache loads before the first
-// dot product.  Per entry the sum is the same fixed-order chain as before
+// pipelined -- the next step's ids are loaded one step ahead, and a step's
+// 32 / LPE entries issue all their sub-row and cache loads before the dot
+// product.  Per entry the sum is the same fixed-order chain as before
 // (bit-identical results).  Measured at L1 (ncu, per launch): U = 1 at 4
 // CTAs/SM 502 / 692 us (user / item side) against 539 / 972 us unpipelined;
 // U = 2 (80 registers, 3 CTAs/SM) 568 / 812 us; capping registers for 5 or 6
