@@ -211,7 +211,10 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
  * on a second stream and overlap the epoch: H and W (in row chunks, each
  * chunk's predictions starting as it lands) on the way in, each column block
  * W[:, pi] / H[:, pi] as soon as its side pass has finished it on the way
- * out.  Host leading dimensions in elements.  Stream-ordered on `stream`. */
+ * out.  With the tensor-core path the first user pass also runs by row chunk
+ * (IALS_HOST_CHUNKS, default 4): each chunk's projection and sweep start once
+ * its rows of W have landed.  Results are bit-identical to ials_epoch.  Host
+ * leading dimensions in elements.  Stream-ordered on `stream`. */
 int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                     const ials_side* items, const ials_sched* item_sched, const float* W_in,
                     float* W_out, int64_t ldw_host, const float* H_in, float* H_out,

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <functional>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -35,7 +36,18 @@ struct ials_session {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   unsigned long long* err;  // device error word (ULLONG_MAX = clean)
   unsigned long long* redo; // rows the fused tensor-core sweep handed to SIMT
+  const struct ChunkPlan* chunk = nullptr;   // set by ials_epoch_host around its first user pass
   char msg[512];
+};
+
+// ials_epoch_host's first user pass: the light rows grouped by row chunk
+// (stable, so each chunk keeps the longest-first order), and a prologue that
+// queues chunk c's W copy, predictions and projection before its sweep
+struct ChunkPlan {
+  int nch;
+  const int* rows;   // grouped light rows (device)
+  const int* tot;    // rows per chunk (device)
+  std::function<int(int)> prologue;
 };
 
 static thread_local char g_msg[512];
@@ -495,8 +507,8 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   // heavy-row partials run on a second stream beside the light rows (they
   // touch disjoint rows and only read the cache), so each kernel's last wave
   // is filled by the other's CTAs; joined before the heavy solve
-  const bool fork = p.n_light > 0 && p.n_heavy > 0;
-  cudaStream_t hst = st;
+  const bool fork = p.n_light > 0 && p.n_heavy > 0 && !s->chunk;   // chunked: heavy rows after
+  cudaStream_t hst = st;                                          // the last chunk's data lands
   if (fork) {
     if (!s->aux_st) {
       CUDA_TRY(s, cudaStreamCreateWithFlags(&s->aux_st, cudaStreamNonBlocking));
@@ -519,11 +531,23 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
     const int grid = std::min(p.n_light, 4 * kNumSMs);   // TMEM: 4 x 128 columns per SM
-    if (unit)
-      k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
-    else
-      k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(p, fmap, use_tma);
-    LAUNCH_CHECK(s);
+    const ChunkPlan* cp = s->chunk;
+    for (int c = 0; c < (cp ? cp->nch : 1); ++c) {
+      SweepParams q = p;
+      if (cp) {
+        rc = cp->prologue(c);
+        if (rc) return rc;
+        q.light_rows = cp->rows;
+        q.chunk_tot = cp->tot;
+        q.chunk = c;
+        if (c > 0) CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt + 2, 0, sizeof(int), st));   // row queue
+      }
+      if (unit)
+        k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
+      else
+        k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
+      LAUNCH_CHECK(s);
+    }
   }
   if (p.n_heavy > 0) {
     static bool hinit = false;
@@ -1108,6 +1132,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                       const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
                       float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
                       void* workspace, size_t ws_bytes, void* stream, const EpochHost* host);
+static int radix_sort_index(ials_session* s, const int* keys, int64_t n, int K, int* keys_out,
+                            int* vals_out, int* tk, int* tv, int* hist, int* tot, cudaStream_t st);
 
 int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
@@ -1195,8 +1221,72 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   }
   rec_event(0, st);
   int rc = IALS_OK;
-  if (host) {
-    const int nch = 8, U = users->n_rows;
+  // Host staging with the fused sweep: the first user pass runs chunk by
+  // chunk of user rows, each chunk's sweep starting once its rows of W have
+  // landed (with its predictions and projection), instead of after all of W.
+  // Its light rows are grouped by chunk (stable: longest-first inside each)
+  // in the split-partial scratch P, idle between the two Gramians of block 0.
+  // (L1 e2e: 117.6 ms unchunked; 4 / 8 / 16 / 32 chunks 112.8 / 113.1 / 115.2 / 119.9 ms --
+  // each chunk's sweep ends with its own tail; IALS_HOST_CHUNKS overrides, 0 or 1 = off)
+  static const int kChunks = getenv("IALS_HOST_CHUNKS") ? std::max(1, std::min(64, atoi(getenv("IALS_HOST_CHUNKS")))) : 4;
+  const int U = users->n_rows, per_chunk = (U + kChunks - 1) / kChunks;
+  const int nl = user_sched->n_light;
+  const size_t part_need = 4 * al256(size_t(std::max(nl, 1)) * 4) +
+                           al256(size_t((nl + kRadixTile - 1) / kRadixTile + 1) * 256 * 4) + al256(256 * 4);
+  bool chunked = host && tc_gemm && nl > 0 && kChunks > 1 && U >= kChunks;
+  if (chunked) {
+    int su, spu, si, spi;
+    gram_plan(std::max(users->n_rows, 1), d, &su, &spu);
+    gram_plan(std::max(items->n_rows, 1), d, &si, &spi);
+    chunked = al256(size_t(std::max(su, si)) * d * b * 4) >= part_need;
+  }
+  ChunkPlan plan{};
+  if (chunked) {
+    CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));   // H is on the device
+    CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));
+    rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+    if (rc) return rc;
+    char* t = reinterpret_cast<char*>(P);
+    int* keys = reinterpret_cast<int*>(t);
+    t += al256(size_t(nl) * 4);
+    int* skeys = reinterpret_cast<int*>(t);
+    t += al256(size_t(nl) * 4);
+    int* idx = reinterpret_cast<int*>(t);
+    t += al256(size_t(nl) * 4);
+    int* grouped = reinterpret_cast<int*>(t);
+    t += al256(size_t(nl) * 4);
+    int* tot = reinterpret_cast<int*>(t);
+    t += al256(256 * 4);
+    int* hist = reinterpret_cast<int*>(t);
+    plan.nch = kChunks;
+    plan.rows = grouped;
+    plan.tot = tot;
+    plan.prologue = [&, st, keys, skeys, idx, grouped, tot, hist](int c) -> int {
+      if (c == 0) {   // after block 0's H Gramian, the last user of P before the sweep
+        k_chunk_keys<<<(nl + 255) / 256, 256, 0, st>>>(user_sched->light_rows, nl, per_chunk, keys);
+        LAUNCH_CHECK(s);
+        int r = radix_sort_index(s, keys, nl, kChunks, skeys, idx, skeys, idx, hist, tot, st);
+        if (r) return r;
+        k_gather_i32<<<(nl + 255) / 256, 256, 0, st>>>(user_sched->light_rows, idx, nl, grouped);
+        LAUNCH_CHECK(s);
+      }
+      const int r0 = c * per_chunk, r1 = std::min(U, r0 + per_chunk);
+      if (r1 <= r0) return IALS_OK;
+      CUDA_TRY(s, cudaMemcpy2DAsync(W + size_t(r0) * ldw, size_t(ldw) * 4, host->W_in + size_t(r0) * host->ldw,
+                                    size_t(host->ldw) * 4, size_t(d) * 4, size_t(r1 - r0),
+                                    cudaMemcpyHostToDevice, s->copy_st));
+      CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));
+      CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));   // W rows [r0, r1) are on the device
+      int r = ials_predictions(s, r1 - r0, users->ptr + r0, users->cols, W + size_t(r0) * ldw, ldw, H,
+                               ldh, d, cache, stream);
+      if (r) return r;
+      TcCopies part = cw;
+      part.n = r1 - r0;
+      return proj_tc(s, W + size_t(r0) * ldw, ldw, part, d, std::min(b, d), sth, stl, alpha0,
+                     reinterpret_cast<float*>(pws) + size_t(r0) * std::min(b, d), st);
+    };
+  } else if (host) {
+    const int nch = 8;
     const int per = (U + nch - 1) / nch;
     for (int c = 0; c < nch && c * per < U; ++c) {
       const int r0 = c * per, r1 = std::min(U, r0 + per);
@@ -1223,16 +1313,20 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   int ek = 2;
   for (int b0 = 0; b0 < d; b0 += b) {
     const int bb = std::min(b, d - b0);
+    const bool first_chunked = chunked && b0 == 0;
     if (tc_gemm) {
       rc = gram_tc(s, ch, d, b0, bb, P, slab, sth, stl, st);
-      if (!rc) rc = proj_tc(s, W, ldw, cw, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
+      if (!rc && !first_chunked)
+        rc = proj_tc(s, W, ldw, cw, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
     } else {
       rc = gramian_impl(s, H, items->n_rows, ldh, d, b0, bb, slab, part, gbytes, st);
     }
     if (rc) return rc;
     rec_event(ek++, st);
+    if (first_chunked) s->chunk = &plan;
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
                         pws, pbytes, st, tc_gemm);
+    s->chunk = nullptr;
     if (rc) return rc;
     if (host) {   // W[:, b0:b0+bb] is final: back to the host beside the rest of the epoch
       rc = stage_copy(s, st, host->W_out + b0, size_t(host->ldw) * 4, W + b0, size_t(ldw) * 4,
@@ -1240,8 +1334,9 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       if (rc) return rc;
     }
     rec_event(ek++, st);
-    if (tc_gemm) {
-      rc = sync_copies(s, W, ldw, d, b0, bb, cw, st);
+    if (tc_gemm) {   // (chunked: W's copies are built here, after its first block)
+      rc = first_chunked ? sync_copies(s, W, ldw, d, 0, d, cw, st)
+                         : sync_copies(s, W, ldw, d, b0, bb, cw, st);
       if (!rc) rc = gram_tc(s, cw, d, b0, bb, P, slab, sth, stl, st);
       if (!rc) rc = proj_tc(s, H, ldh, ch, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
     } else {

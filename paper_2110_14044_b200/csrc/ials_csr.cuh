@@ -152,6 +152,12 @@ __global__ void k_gather_i32(const int* __restrict__ src, const int* __restrict_
   if (k < n) dst[k] = __ldg(src + __ldg(idx + k));
 }
 
+// chunk of each row id (rows [c * per, (c + 1) * per) form chunk c)
+__global__ void k_chunk_keys(const int* __restrict__ rows, int n, int per, int* __restrict__ keys) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) keys[k] = __ldg(rows + k) / per;
+}
+
 __global__ void k_iota_i32(int64_t n, int* __restrict__ dst) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) dst[k] = (int)k;

@@ -83,6 +83,8 @@ struct SweepParams {
   int* queue;              // if set, k_sweep_light takes its rows from this zeroed counter
   float* drow;             // [n_rows][b] per-row d of the fused sweep (k_pass_cache)
   int fb0;                 // column of the block in `fixed` (b0, or 0 for a compact copy)
+  const int* chunk_tot;    // if set (k_sweep_tc4): light rows grouped by row chunk, chunk_tot[k]
+  int chunk;               //   rows in chunk k; this launch sweeps chunk `chunk` only
 };
 
 template <int BT>

@@ -623,12 +623,22 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
   if (tid == 0) *next = atomicAdd(queue, 1);
   __syncthreads();
   int task = *next;
-  while (task < p.n_light) {
+  // the first user pass of ials_epoch_host sweeps the light rows chunk by
+  // chunk as their rows of W arrive: this launch's slice of the grouped list
+  const int* lrows = p.light_rows;
+  int n_light = p.n_light;
+  if (p.chunk_tot) {
+    int off = 0;
+    for (int k = 0; k < p.chunk; ++k) off += p.chunk_tot[k];
+    lrows += off;
+    n_light = p.chunk_tot[p.chunk];
+  }
+  while (task < n_light) {
     int nxt = 0;
     if (tid == 0) nxt = atomicAdd(queue, 1);   // consumed at the end of the row
     const bool rec = ndone == rec_row && tid == 0;
     if (rec) tph[0] = clock64();
-    const int row = p.light_rows[task];
+    const int row = lrows[task];
     const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
     const float lam = p.side.lam[row];
     tc4_init(p, row_addr, tid);
