@@ -288,15 +288,27 @@ def test_dedicated_solver_entry_points(ials, which):
     assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL
 
 
-def test_epoch_host_equals_device_epoch(ials):
-    """ials_epoch_host (host-staged, copies overlapped) gives bit for bit the
-    device epoch's W, H and cache, written to the host buffers."""
+@pytest.mark.parametrize("case", ["tc", "tc_b64", "heavy_users", "simt", "tiny"])
+def test_epoch_host_equals_device_epoch(ials, case):
+    """ials_epoch_host (host-staged, copies overlapped; with the tensor-core
+    path the first user pass runs by row chunk as W lands) gives bit for bit
+    the device epoch's W, H and cache, written to the host buffers: the
+    default tensor-core shape, b = 64 (padded tile), users above the heavy
+    threshold (their slices run after the last chunk), a SIMT block width and
+    fewer users than chunks."""
     import torch
     from paper_2110_14044_b200.engine import DeviceProblem, Engine
     rng = np.random.default_rng(13)
-    U, I, n, d, b = 1500, 400, 30000, 256, 128
+    U, I, n, d, b = {"tc": (1500, 400, 30000, 256, 128), "tc_b64": (1500, 400, 30000, 128, 64),
+                     "heavy_users": (1200, 6000, 40000, 128, 128), "simt": (1500, 400, 30000, 64, 16),
+                     "tiny": (3, 50, 60, 128, 128)}[case]
     users = rng.integers(0, U, n)
     items = np.minimum(rng.zipf(1.2, n) - 1, I - 1)
+    if case == "heavy_users":   # three users with 5,000 distinct items each
+        extra_u = np.repeat(np.arange(3), 5000)
+        extra_i = np.concatenate([rng.choice(I, 5000, replace=False) for _ in range(3)])
+        users, items = np.concatenate([users, extra_u]), np.concatenate([items, extra_i])
+        n = users.size
     prob = DeviceProblem.from_dataset(ials.InteractionDataset(U, I, users, items), "cuda:0")
     prob.set_regularizer(0.1, 1e-3, 1.0)
     eng = Engine(prob)
