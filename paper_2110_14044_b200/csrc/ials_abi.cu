@@ -591,8 +591,15 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   if (p.n_light + p.n_slices > 0) {
     if (p.side.rows && nnz > 0) {   // entry-parallel: no per-row setup, full load balance
       const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);
-      if (p.vec) k_pass_cache_flat<true, 8><<<(int)g, 256, 0, st>>>(p, nnz);
-      else k_pass_cache_flat<false, 8><<<(int)g, 256, 0, st>>>(p, nnz);
+      // walk the other side's order when this side's d is the smaller gather
+      const bool swap = p.x_rows && p.x_cols && p.side.n_rows < p.side.n_fixed;
+      if (swap) {
+        if (p.vec) k_pass_cache_flat<true, 8, true><<<(int)g, 256, 0, st>>>(p, nnz);
+        else k_pass_cache_flat<false, 8, true><<<(int)g, 256, 0, st>>>(p, nnz);
+      } else {
+        if (p.vec) k_pass_cache_flat<true, 8, false><<<(int)g, 256, 0, st>>>(p, nnz);
+        else k_pass_cache_flat<false, 8, false><<<(int)g, 256, 0, st>>>(p, nnz);
+      }
     } else {
       k_pass_cache<<<p.n_light + p.n_slices, 256, 0, st>>>(p);
     }
@@ -739,7 +746,8 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
                           const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
                           int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
                           int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st,
-                          bool proj_ready = false, const float* proj_in = nullptr) {
+                          bool proj_ready = false, const float* proj_in = nullptr,
+                          const ials_side* other = nullptr) {
   if (!side || !sched || !fixed || !own || !slab || !cache)
     return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
   if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
@@ -809,6 +817,11 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.vec = (b % 4 == 0) && (reinterpret_cast<uintptr_t>(compact) % 16 == 0);
   }
   p.redo_total = s->redo;
+  if (other && other->rows && other->cols && other->nnz == side->nnz) {   // same entries, other order
+    p.x_rows = other->rows;
+    p.x_cols = other->cols;
+    p.x_pos = other->pos;
+  }
   // narrow blocks in the 128 tile: a pivot losing more than 16x of its
   // diagonal already goes to the FP32 sweep (ill-conditioned heavy rows at
   // b = 64 slip under the 256x limit, tests/test_gpu_parity.py heavy rows)
@@ -1325,7 +1338,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     rec_event(ek++, st);
     if (first_chunked) s->chunk = &plan;
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
-                        pws, pbytes, st, tc_gemm);
+                        pws, pbytes, st, tc_gemm, nullptr, items);
     s->chunk = nullptr;
     if (rc) return rc;
     if (host) {   // W[:, b0:b0+bb] is final: back to the host beside the rest of the epoch
@@ -1345,7 +1358,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     if (rc) return rc;
     rec_event(ek++, st);
     rc = side_pass_impl(s, items, item_sched, W, ldw, H, ldh, d, b0, bb, slab, alpha0, cache, 1,
-                        pws, pbytes, st, tc_gemm);
+                        pws, pbytes, st, tc_gemm, nullptr, users);
     if (rc) return rc;
     if (host) {
       rc = stage_copy(s, st, host->H_out + b0, size_t(host->ldh) * 4, H + b0, size_t(ldh) * 4,

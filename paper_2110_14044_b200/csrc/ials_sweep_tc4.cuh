@@ -884,7 +884,13 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
 // == 0, no per-element width tests) cut the instruction count 428M -> 271M
 // (387 / 574 us); 4 lanes per entry executes 27% fewer instructions but needs
 // 123 registers (2 CTAs/SM): 403 / 738 us.
-template <bool VEC, int LPE>
+// SWAP: walk the other side's view of the entries instead (x_rows / x_cols /
+// x_pos): the vector held across a run is then the fixed side's sub-row and
+// the gathered one this side's d (drow, n_rows x b: L2-resident when this
+// side is the smaller one -- the item pass, whose fixed W[:, pi] is 70 MB at
+// L1 and 292 MB at msd).  Each entry's sum is the same fixed-order chain of
+// the same products (fma is commutative in its factors): bit-identical.
+template <bool VEC, int LPE, bool SWAP>
 __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(SweepParams p, long long nnz) {
   constexpr int EPW = 32 / LPE, NQ = 128 / (4 * LPE);   // entries per warp step, float4 per lane
   const int lane = threadIdx.x & 31, g = lane % LPE, sub = lane / LPE;
@@ -893,6 +899,9 @@ __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(Sweep
   const long long per = ((nnz + nwarps - 1) / nwarps + EPW - 1) / EPW * EPW;
   const long long beg = wid * per, end = min(nnz, beg + per);
   const int b = p.b;
+  const int* __restrict__ R = SWAP ? p.x_rows : p.side.rows;   // the run's (held) vector
+  const int* __restrict__ C = SWAP ? p.x_cols : p.side.cols;   // the gathered vector
+  const int* __restrict__ PS = SWAP ? p.x_pos : p.side.pos;
   int cur = -1;
   float dv[4 * NQ];
 #pragma unroll
@@ -900,19 +909,19 @@ __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(Sweep
   int nrow, ncol;
   {
     const long long e = beg + sub;
-    nrow = e < end ? __ldg(p.side.rows + e) : -1;
-    ncol = e < end ? __ldg(p.side.cols + e) : 0;
+    nrow = e < end ? __ldg(R + e) : -1;
+    ncol = e < end ? __ldg(C + e) : 0;
   }
   for (long long e0 = beg; e0 < end; e0 += EPW) {   // warp-uniform trip count (shuffles below)
     const int row = nrow, col = ncol;
     {
       const long long e = e0 + EPW + sub;
-      nrow = e < end ? __ldg(p.side.rows + e) : -1;
-      ncol = e < end ? __ldg(p.side.cols + e) : 0;
+      nrow = e < end ? __ldg(R + e) : -1;
+      ncol = e < end ? __ldg(C + e) : 0;
     }
     const bool live = row >= 0;
     float4 x[NQ];
-    const float* xr = p.fixed + (size_t)col * p.ldf + p.fb0;
+    const float* xr = SWAP ? p.drow + (size_t)col * b : p.fixed + (size_t)col * p.ldf + p.fb0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int c = 4 * LPE * q + 4 * g;
@@ -929,10 +938,10 @@ __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(Sweep
       }
     }
     const long long e = e0 + sub;
-    const long long pos = (live && g == 0) ? (p.side.pos ? (long long)__ldg(p.side.pos + e) : e) : 0;
+    const long long pos = (live && g == 0) ? (PS ? (long long)__ldg(PS + e) : e) : 0;
     const float cold = (live && g == 0) ? p.cache[pos] : 0.f;
     if (live && row != cur) {
-      const float* dr = p.drow + (size_t)row * b;
+      const float* dr = SWAP ? p.fixed + (size_t)row * p.ldf + p.fb0 : p.drow + (size_t)row * b;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int c = 4 * LPE * q + 4 * g;
