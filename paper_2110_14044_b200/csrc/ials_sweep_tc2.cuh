@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(128) k_tc_factor(SweepParams p) {
   const float* ds = reinterpret_cast<const float*>(smem + L::OFF_D);
   const int b = p.b, i = tid;
   const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
-  const float a0 = p.alpha0;
   int nrow_done = 0;
   long long tphase[8];
   for (int r = p.w_r0 + blockIdx.x; r < p.w_r1; r += gridDim.x) {

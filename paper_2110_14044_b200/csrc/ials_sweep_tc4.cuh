@@ -326,7 +326,6 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
   float* lrow = reinterpret_cast<float*>(smem + L::OFF_L) + tid * (tid + 1) / 2;   // packed row
   const int b = p.b, i = tid, lane = tid & 31, warp = tid >> 5;
   const int np = (b + 7) >> 3;
-  const unsigned full = 0xffffffffu;
   (void)row;
   float yi = ys[i];
   for (int pp = 0; pp < np; ++pp) {
