@@ -167,7 +167,7 @@ def test_heavy_rows_vs_oracle(ials, d, b, I):
 
 
 @pytest.mark.parametrize("d,b", [(128, 128), (200, 100), (96, 72), (128, 40), (120, 60),
-                                 (100, 98)])
+                                 (100, 98), (66, 33), (130, 65)])
 def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
     """b in (32, 128] runs the tcgen05 3xTF32 sweep (mode 1: wave kernels;
     mode 2, the default: fused 4-CTA/SM kernel); compare with the oracle and
