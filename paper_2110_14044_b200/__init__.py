@@ -7,6 +7,7 @@ of ``libials_b200.so`` (``include/ials_b200.h``); there is no CPU fallback.
 """
 
 from .data import InteractionDataset, SideView
+from .estimator import ImplicitALS
 from .evaluation import (MetricReport, evaluate_holdout, fold_in_users, ndcg_at_k, project_user,
                          rank_items, recall_at_k, top_k_from_scores)
 from .linalg import SingularMatrixError, check_block, gramian, partial_gramian
@@ -19,7 +20,7 @@ from .solvers import (BlockPartition, DeviceTrainer, EpochReport, block_update,
 __version__ = "0.1.0"
 
 __all__ = [
-    "InteractionDataset", "SideView",
+    "InteractionDataset", "SideView", "ImplicitALS",
     "MetricReport", "evaluate_holdout", "fold_in_users", "ndcg_at_k", "project_user",
     "rank_items", "recall_at_k", "top_k_from_scores",
     "SingularMatrixError", "check_block", "gramian", "partial_gramian",
