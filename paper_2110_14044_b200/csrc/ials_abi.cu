@@ -312,8 +312,14 @@ int ials_cache_correct(ials_session* s, int32_t n_seg, const int32_t* seg_row,
     return fail(s, IALS_E_INVALID, "cache_correct: bad shape (b0=%d b=%d)", b0, b);
   if (n_seg == 0) return IALS_OK;
   const int blocks = std::min((n_seg + 7) / 8, kNumSMs * 16);
-  k_cache_correct<<<blocks, 256, 0, S(stream)>>>(n_seg, Items{nullptr, seg_row, seg_beg, seg_end},
-                                                 cols, A, lda, b0, D, ldd, b, out);
+  const bool vec = b <= 128 && b % 4 == 0 && b0 % 4 == 0 && lda % 4 == 0 && ldd % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(D) % 16 == 0;
+  if (vec)
+    k_cache_correct_v<<<blocks, 256, 0, S(stream)>>>(n_seg, Items{nullptr, seg_row, seg_beg, seg_end},
+                                                     cols, A, lda, b0, D, ldd, b, out);
+  else
+    k_cache_correct<<<blocks, 256, 0, S(stream)>>>(n_seg, Items{nullptr, seg_row, seg_beg, seg_end},
+                                                   cols, A, lda, b0, D, ldd, b, out);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }

@@ -142,6 +142,57 @@ __global__ void __launch_bounds__(256)
 // Dual-cache delta correction of the sharded path:
 // out[e] += <A[row, b0:b0+b], D[cols[e], 0:b]> over a (local) CSR, where D is
 // the change of the other side's column block in the previous half-epoch.
+// The same correction for b <= 128 with 16-byte rows (b0, lda, ldd, b multiples
+// of 4): a warp keeps its segment's A[row, b0:b0+b] in registers (16 floats
+// per lane) and takes 4 entries per step (8 lanes each), the next step's
+// column ids loaded a step ahead, so the D-row gathers of a step are all in
+// flight together instead of one warp-wide dot product and reduction per entry.
+__global__ void __launch_bounds__(256)
+    k_cache_correct_v(int n_items, Items it, const int* __restrict__ cols,
+                      const float* __restrict__ A, int lda, int b0, const float* __restrict__ D,
+                      int ldd, int b, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, g = lane & 7, sub = lane >> 3;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < n_items; t += nw) {
+    int row, e0, e1;
+    it.get(t, row, e0, e1);
+    const float* ar = A + (size_t)row * lda + b0;
+    float4 av[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = 32 * q + 4 * g;
+      av[q] = c < b ? __ldg(reinterpret_cast<const float4*>(ar + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    int ncol = e0 + sub < e1 ? __ldg(cols + e0 + sub) : -1;
+    for (int eb = e0; eb < e1; eb += 4) {
+      const int col = ncol;
+      ncol = eb + 4 + sub < e1 ? __ldg(cols + eb + 4 + sub) : -1;
+      float s = 0.f;
+      if (col >= 0) {
+        const float* dr = D + (size_t)col * ldd;
+        float4 x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = 32 * q + 4 * g;
+          x[q] = c < b ? __ldg(reinterpret_cast<const float4*>(dr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s = fmaf(av[q].x, x[q].x, s);
+          s = fmaf(av[q].y, x[q].y, s);
+          s = fmaf(av[q].z, x[q].z, s);
+          s = fmaf(av[q].w, x[q].w, s);
+        }
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (col >= 0 && g == 0) out[eb + sub] += s;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256)
     k_cache_correct(int n_items, Items it, const int* __restrict__ cols,
                     const float* __restrict__ A, int lda, int b0, const float* __restrict__ D,
