@@ -393,11 +393,20 @@ int ials_partial_gramian(ials_session* s, const float* M, int32_t n, int32_t ldm
                       S(stream));
 }
 
+// Kernel attributes (dynamic shared memory, carveout) are per device: the
+// one-time setups below are tracked per device so that sessions of one
+// process on several GPUs each get them.
+static unsigned dev_bit() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return 1u << (d & 31);
+}
+
 // ------------------------------------------------------------------ side pass
 template <int BT>
 static int set_smem_attrs(ials_session* s) {
-  static bool done = false;
-  if (done) return IALS_OK;
+  static unsigned done = 0;
+  if (done & dev_bit()) return IALS_OK;
   const int bytes = Lay<BT>::CTA_BYTES;
   CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_light<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -405,7 +414,7 @@ static int set_smem_attrs(ials_session* s) {
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_solve<BT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_cache<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done = true;
+  done |= dev_bit();
   return IALS_OK;
 }
 
@@ -526,13 +535,13 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     CUDA_TRY(s, cudaStreamWaitEvent(hst, s->ev_fork, 0));
   }
   if (p.n_light > 0) {
-    static bool init = false;
-    if (!init) {
+    static unsigned init = 0;
+    if (!(init & dev_bit())) {
       for (auto k : {k_sweep_tc4<false>, k_sweep_tc4<true>}) {
         CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
         CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       }
-      init = true;
+      init |= dev_bit();
     }
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
@@ -556,13 +565,13 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     }
   }
   if (p.n_heavy > 0) {
-    static bool hinit = false;
-    if (!hinit) {
+    static unsigned hinit = 0;
+    if (!(hinit & dev_bit())) {
       for (auto k : {k_heavy_partial_tc4<false>, k_heavy_partial_tc4<true>}) {
         CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
         CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       }
-      hinit = true;
+      hinit |= dev_bit();
     }
     const int threads = L::NT * L::RPC;
     const int hg = std::min(p.n_slices, 4 * kNumSMs);
@@ -621,7 +630,8 @@ static int launch_sweep_tc128(ials_session* s, const SweepParams& p, cudaStream_
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
   static int per_sm = 0;
-  if (per_sm == 0) {
+  static unsigned per_dev = 0;
+  if (!(per_dev & dev_bit())) {
     CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc128, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      TcLay::BYTES));
     CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc128,
@@ -642,6 +652,7 @@ static int launch_sweep_tc128(ials_session* s, const SweepParams& p, cudaStream_
     const int by_smem = smem_sm / (TcLay::BYTES + 1024);
     const int by_regs = regs_sm / (((fa.numRegs + 7) / 8) * 8 * 128);
     per_sm = std::max(1, std::min(std::min(by_smem, by_regs), 4));
+    per_dev |= dev_bit();
   }
   if (p.n_light > 0) {
     const int grid = std::min(p.n_light, per_sm * kNumSMs);
@@ -681,7 +692,8 @@ static int tc_per_sm(ials_session* s, K kernel, int bytes, int* out) {
 static int launch_tc_waves(ials_session* s, SweepParams p, const ials_sched* sched,
                            cudaStream_t st) {
   static int h_sm = 0, f_sm = 0, c_sm = 0;
-  if (h_sm == 0) {
+  static unsigned per_dev = 0;
+  if (!(per_dev & dev_bit())) {
     int rc = tc_per_sm(s, k_tc_hess, TcLayH::BYTES, &h_sm);
     if (!rc) rc = tc_per_sm(s, k_tc_factor, TcLayF::BYTES, &f_sm);
     if (!rc) rc = tc_per_sm(s, k_tc_cache, TcLayC::BYTES, &c_sm);
@@ -690,6 +702,7 @@ static int launch_tc_waves(ials_session* s, SweepParams p, const ials_sched* sch
     f_sm = std::min(f_sm, 4);
     if (const char* e = getenv("IALS_TC_FSM")) f_sm = std::max(1, std::min(f_sm, atoi(e)));
     if (const char* e = getenv("IALS_TC_HSM")) h_sm = std::max(1, std::min(h_sm, atoi(e)));
+    per_dev |= dev_bit();
   }
   k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
   LAUNCH_CHECK(s);
@@ -988,11 +1001,11 @@ static int sync_copies(ials_session* s, const float* F, int ldf, int d, int c0, 
 }
 
 static int gemm_attrs(ials_session* s) {
-  static bool init = false;
-  if (!init) {
+  static unsigned init = 0;
+  if (!(init & dev_bit())) {
     CUDA_TRY(s, cudaFuncSetAttribute(k_gemm3_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      GemmLay::BYTES));
-    init = true;
+    init |= dev_bit();
   }
   return IALS_OK;
 }
