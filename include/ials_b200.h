@@ -4,7 +4,7 @@
  * The reference (blockals 0.1.0, /root/reference/pkg/src/blockals) is a pure
  * Python/NumPy package and has no FFI.  Its drop-in boundary is its Python
  * API; every entry point below replaces the numerical core of one reference
- * function, and the host mirror (paper_2110_14044_b200/*.py, bound with
+ * function, and the host mirror (paper_2110_14044_b200/ Python modules, bound with
  * ctypes) keeps the reference names, argument meaning and error behaviour:
  *
  *   ials_predictions       <- compute_predictions   model.py:153-165
