@@ -57,3 +57,20 @@ def test_library_is_sm100a():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_header_compiles_as_c_and_cpp(tmp_path):
+    """include/ials_b200.h is a plain C header: it compiles warning-free as
+    C99 and C++17 (the binding a C / cgo / JNI consumer would include)."""
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "hdr.c"
+    src.write_text('#include "ials_b200.h"\nint main(void) { return 0; }\n')
+    for cc, flags in (("gcc", ["-std=c99"]), ("g++", ["-std=c++17", "-x", "c++"])):
+        if shutil.which(cc) is None:
+            pytest.skip(f"{cc} not available")
+        r = subprocess.run([cc, *flags, "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
+                            "-I", os.path.join(root, "include"), str(src)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
