@@ -99,6 +99,11 @@ def _fold_in_blocks(model, data, cache, config, device, tol=1e-7, max_sweeps=200
         den = float(torch.linalg.vector_norm(tr.W))
         if num <= tol * max(den, 1e-30):
             break
+    else:   # strongly coupled blocks converge slowly: say so instead of returning silently
+        import warnings
+        warnings.warn(f"fold_in_users: block Gauss-Seidel for d = {d} stopped after {max_sweeps} "
+                      f"sweeps at a relative change of {num / max(den, 1e-30):.2e} (> {tol:.0e})",
+                      RuntimeWarning, stacklevel=3)
     tr.write_back()
     return model.user_factors
 
