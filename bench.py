@@ -491,7 +491,22 @@ def cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
     threads) on a bounded systematic sample: predictions for a sample of user
     rows, one block's two slabs in full, the user pass for every s_u-th user and
     the item pass for every s_i-th item (degree-sorted), scaled by the stride;
-    epoch = t_pred + B * t_block ("extrapolated from 1 of B blocks")."""
+    epoch = t_pred + B * t_block ("extrapolated from 1 of B blocks").  The BLAS
+    pool is opened to every host core for the measurement (torchrun exports
+    OMP_NUM_THREADS=1 to its ranks)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        limits = threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:  # pragma: no cover - threadpoolctl is a reference dependency
+        limits = None
+    try:
+        return _cpu_baseline(ds, d, b, budget_s, seed)
+    finally:
+        if limits is not None:
+            limits.restore_original_limits()
+
+
+def _cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
     from oracle import ialspp_oracle as orc
     U, I = int(ds["U"]), int(ds["I"])
     uptr, iptr = ds["user_ptr"].astype(np.int64), ds["item_ptr"].astype(np.int64)
