@@ -1023,10 +1023,11 @@ static int gram_tc(ials_session* s, const TcCopies& F, int d, int b0, int bb, fl
   if (!rc) rc = make_map(s, &bh, F.FT, F.n, d, F.ldt, bn);
   if (rc) return rc;
   GemmJob job{d, 0, b0, bb, bn, F.n, span, P, bb, (long long)d * bb, 1.f};
-  k_gemm3_tf32<<<dim3((d + 127) / 128, S), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, job);
+  k_gemm3_tf32<<<dim3((d + 127) / 128, S), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, bh, job);
   LAUNCH_CHECK(s);
+  // slab^T hi and its tf32 lo part (the projection TMA-loads both)
   k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(P, S, (long long)d * bb, d, bb, slab,
-                                                      slabT_hi, nullptr);
+                                                      slabT_hi, slabT_lo);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
@@ -1039,13 +1040,16 @@ static int proj_tc(ials_session* s, const float* own, int ldo, const TcCopies& O
   int rc = gemm_attrs(s);
   if (rc) return rc;
   const int bn = rup(bb, 16);
-  CUtensorMap ah, bh;
+  CUtensorMap ah, bh, bl;
   rc = make_map(s, &ah, own, d, O.n, ldo, 128);
   if (!rc) rc = make_map(s, &bh, slabT_hi, d, bb, d, bn);
+  if (!rc && slabT_lo) rc = make_map(s, &bl, slabT_lo, d, bb, d, bn);
   if (rc) return rc;
-  (void)slabT_lo;
   GemmJob job{O.n, 0, 0, bb, bn, d, rup(d, kGemmKC), proj, bb, 0, alpha0};
-  k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, job);
+  // B = slab^T is the same for every CTA: its lo part comes precomputed
+  // (k_gram_reduce) instead of being re-formed on chip by each CTA
+  job.b_lo_tma = slabT_lo ? 1 : 0;
+  k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, slabT_lo ? bl : bh, job);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
@@ -1121,7 +1125,7 @@ int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t 
   if (get_encode(s) != IALS_OK) return fail(s, IALS_E_CUDA, "shard_projection: no cuTensorMapEncodeTiled");
   cudaStream_t st = S(stream);
   // stage slab^T hi / lo from the (all-reduced) slab: the split reduction with one split
-  k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(slab, 1, (long long)d * bb, d, bb, slab, w.sth, nullptr);
+  k_gram_reduce<<<(d * bb + 255) / 256, 256, 0, st>>>(slab, 1, (long long)d * bb, d, bb, slab, w.sth, w.stl);
   LAUNCH_CHECK(s);
   return proj_tc(s, F, ldf, w.c, d, bb, w.sth, w.stl, alpha0, proj, st);
 }

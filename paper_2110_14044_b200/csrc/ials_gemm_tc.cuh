@@ -37,6 +37,7 @@ struct GemmJob {
   int ldo;
   long long split_stride;  // floats between splits
   float scale;
+  int b_lo_tma = 0;        // B's lo part is precomputed in memory (b_lo map): TMA-load it
 };
 
 constexpr int kGemmStages = 3;
@@ -57,7 +58,7 @@ IALS_DEVI void mbar_arrive(uint64_t* bar) {
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm3_tf32(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap b_hi,
-                 GemmJob job) {
+                 const __grid_constant__ CUtensorMap b_lo, GemmJob job) {
   extern __shared__ __align__(1024) char smem_g[];
   char* smem = smem_g + ((1024u - (smem_u32(smem_g) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (tid == 0) {
     prefetch_tmap(&a_hi);
     prefetch_tmap(&b_hi);
+    if (job.b_lo_tma) prefetch_tmap(&b_lo);
     for (int s = 0; s < kGemmStages; ++s) {
       mbar_init(full + s, 1);
       mbar_init(lo_ready + s, kGemmConv);
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tptr;
-  const uint32_t stage_bytes = GemmLay::A_BYTES + job.bn * 128;
+  const uint32_t stage_bytes = GemmLay::A_BYTES + job.bn * 128 * (job.b_lo_tma ? 2 : 1);
   if (warp == 0 && (tid & 31) == 0) {  // TMA producer
     for (int c = 0; c < nk; ++c) {
       const int s = c % kGemmStages;
@@ -95,6 +97,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int kc = kb + c * kGemmKC;
       tma_load_2d(smem_u32(st), &a_hi, kc, job.a_row0 + m0, full + s);
       tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, kc, job.b_row0, full + s);
+      if (job.b_lo_tma)
+        tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, kc, job.b_row0, full + s);
     }
   } else if (warp == 1 && (tid & 31) == 0) {  // MMA issuer
     const uint32_t idesc = make_idesc_tf32(128, job.bn, 0, 0, 0);
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     umma_commit(done);
   } else if (warp >= 2) {   // lo parts of the landed stage
     const int ct = tid - 64;
-    const int na4 = GemmLay::A_BYTES / 16, nt4 = na4 + job.bn * 8;
+    const int na4 = GemmLay::A_BYTES / 16, nt4 = na4 + (job.b_lo_tma ? 0 : job.bn * 8);
     for (int c = 0; c < nk; ++c) {
       const int s = c % kGemmStages;
       mbar_wait(full + s, (c / kGemmStages) & 1);
