@@ -50,6 +50,19 @@ struct ChunkPlan {
   std::function<int(int)> prologue;
 };
 
+
+// Every entry point that takes a session runs on the session's device and
+// restores the caller's current device on return (torch keeps its own notion
+// of the current device; a session created for GPU 1 must not leave the
+// thread on GPU 1, nor launch on GPU 0 when the caller's current device is 0).
+struct DevGuard {
+  int prev = -1, want = -1;
+  explicit DevGuard(const ials_session* s);
+  ~DevGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
 static thread_local char g_msg[512];
 
 static int fail(ials_session* s, int code, const char* fmt, ...) {
@@ -82,6 +95,14 @@ static std::atomic<long long> g_launches{0};
                   __FILE__, __LINE__);                                                \
   } while (0)
 
+
+DevGuard::DevGuard(const ials_session* s) {
+  if (!s) return;
+  want = s->device;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != want) cudaSetDevice(want);
+}
+
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
 int64_t ials_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
@@ -112,6 +133,8 @@ int ials_session_create(int device, ials_session** out) {
   ials_session* s = new ials_session();
   s->device = device;
   s->msg[0] = 0;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMalloc(&s->err, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(s->err, 0xFF, sizeof(unsigned long long));
@@ -120,14 +143,17 @@ int ials_session_create(int device, ials_session** out) {
   if (e != cudaSuccess) {
     fail(nullptr, IALS_E_CUDA, "session create: %s", cudaGetErrorString(e));
     delete s;
+    if (prev >= 0) cudaSetDevice(prev);
     return IALS_E_CUDA;
   }
+  if (prev >= 0 && prev != device) cudaSetDevice(prev);
   *out = s;
   return IALS_OK;
 }
 
 int ials_session_destroy(ials_session* s) {
   if (!s) return IALS_OK;
+  DevGuard _dg(s);
   cudaFree(s->err);
   cudaFree(s->redo);
   if (s->copy_st) cudaStreamDestroy(s->copy_st);
@@ -149,12 +175,14 @@ int ials_last_error(ials_session* s, char* buf, size_t len) {
 }
 
 int ials_reset_singular(ials_session* s, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   CUDA_TRY(s, cudaMemsetAsync(s->err, 0xFF, sizeof(unsigned long long), S(stream)));
   return IALS_OK;
 }
 
 int ials_tc_redo_rows(ials_session* s, void* stream, int64_t* total, int32_t reset) {
+  DevGuard _dg(s);
   if (!s || !total) return fail(s, IALS_E_INVALID, "tc_redo_rows: NULL argument");
   unsigned long long v = 0;
   CUDA_TRY(s, cudaMemcpyAsync(&v, s->redo, sizeof(v), cudaMemcpyDeviceToHost, S(stream)));
@@ -166,6 +194,7 @@ int ials_tc_redo_rows(ials_session* s, void* stream, int64_t* total, int32_t res
 
 int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pivot,
                         int32_t* side) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   unsigned long long key = 0;
   CUDA_TRY(s, cudaMemcpyAsync(&key, s->err, sizeof(key), cudaMemcpyDeviceToHost, S(stream)));
@@ -253,6 +282,7 @@ static int predictions_impl(ials_session* s, int32_t n_items, Items it, const in
 int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,
                      const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                      float* out, void* stream) {
+  DevGuard _dg(s);
   if (n_rows < 0) return fail(s, IALS_E_INVALID, "predictions: n_rows < 0");
   return predictions_impl(s, n_rows, Items{ptr, nullptr, nullptr, nullptr}, cols, W, ldw, H, ldh,
                           d, out, stream);
@@ -262,6 +292,7 @@ int ials_predictions_segments(ials_session* s, int32_t n_seg, const int32_t* seg
                               const int32_t* seg_beg, const int32_t* seg_end, const int32_t* cols,
                               const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                               float* out, void* stream) {
+  DevGuard _dg(s);
   if (n_seg < 0 || (n_seg > 0 && (!seg_row || !seg_beg || !seg_end)))
     return fail(s, IALS_E_INVALID, "predictions_segments: bad segment list");
   return predictions_impl(s, n_seg, Items{nullptr, seg_row, seg_beg, seg_end}, cols, W, ldw, H,
@@ -308,6 +339,7 @@ int ials_cache_correct(ials_session* s, int32_t n_seg, const int32_t* seg_row,
                        const int32_t* seg_beg, const int32_t* seg_end, const int32_t* cols,
                        const float* A, int32_t lda, int32_t b0, const float* D, int32_t ldd,
                        int32_t b, float* out, void* stream) {
+  DevGuard _dg(s);
   if (n_seg < 0 || b < 1 || b > 256 || b0 < 0 || lda < b0 + b || ldd < b)
     return fail(s, IALS_E_INVALID, "cache_correct: bad shape (b0=%d b=%d)", b0, b);
   if (n_seg == 0) return IALS_OK;
@@ -386,6 +418,7 @@ static int gramian_impl(ials_session* s, const float* M, int32_t n, int32_t ldm,
 int ials_partial_gramian(ials_session* s, const float* M, int32_t n, int32_t ldm, int32_t d,
                          int32_t b0, int32_t b, float* slab, void* workspace, size_t ws_bytes,
                          void* stream) {
+  DevGuard _dg(s);
   if (n < 0 || d < 1 || ldm < d || b < 1 || b0 < 0 || b0 + b > d)
     return fail(s, IALS_E_INVALID, "partial_gramian: bad shape (n=%d d=%d b0=%d b=%d)", n, d,
                 b0, b);
@@ -923,6 +956,7 @@ int ials_side_pass(ials_session* s, const ials_side* side, const ials_sched* sch
                    const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
                    int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
                    int32_t side_id, void* workspace, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   return side_pass_impl(s, side, sched, fixed, ldf, own, ldo, d, b0, b, slab, alpha0, cache,
                         side_id, static_cast<char*>(workspace), ws_bytes, S(stream));
@@ -933,6 +967,7 @@ int ials_side_pass_projected(ials_session* s, const ials_side* side, const ials_
                              int32_t b0, int32_t b, const float* slab, const float* proj,
                              float alpha0, float* cache, int32_t side_id, void* workspace,
                              size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (!proj && side && side->n_rows > 0) return fail(s, IALS_E_INVALID, "side_pass_projected: NULL proj");
   return side_pass_impl(s, side, sched, fixed, ldf, own, ldo, d, b0, b, slab, alpha0, cache,
@@ -1088,6 +1123,7 @@ size_t ials_shard_gemm_bytes(int32_t n_rows, int32_t d, int32_t b) { return shar
 
 int ials_shard_sync(ials_session* s, const float* F, int32_t ldf, int32_t n_rows, int32_t d, int32_t b,
                     int32_t c0, int32_t cw, void* ws, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   ShardWs w;
   int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
@@ -1099,6 +1135,7 @@ int ials_shard_sync(ials_session* s, const float* F, int32_t ldf, int32_t n_rows
 
 int ials_shard_gramian(ials_session* s, int32_t n_rows, int32_t d, int32_t b, int32_t b0, int32_t bb,
                        float* slab, void* ws, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   ShardWs w;
   int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
@@ -1115,6 +1152,7 @@ int ials_shard_gramian(ials_session* s, int32_t n_rows, int32_t d, int32_t b, in
 int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t n_rows, int32_t d,
                           int32_t b, int32_t bb, float* slab, float alpha0, float* proj, void* ws,
                           size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   ShardWs w;
   int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
@@ -1132,8 +1170,11 @@ int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t 
 
 // optional phase events: 0 start, 1 after the cache, then per block
 // (user Gramian, user pass, item Gramian, item pass) -> 2 + 4 * blocks
-static cudaEvent_t g_ev[2 + 4 * 1024];
-static int g_nev = 0;
+// (per host thread: the Python mirror sets them around one ials_epoch call
+// and clears them after it, so concurrent epochs on other threads -- or other
+// devices -- never record each other's events)
+static thread_local cudaEvent_t g_ev[2 + 4 * 1024];
+static thread_local int g_nev = 0;
 
 int ials_epoch_events(void* const* events, int32_t n) {
   if (n < 0 || n > 2 + 4 * 1024 || (n > 0 && !events)) return IALS_E_INVALID;
@@ -1142,8 +1183,9 @@ int ials_epoch_events(void* const* events, int32_t n) {
   return IALS_OK;
 }
 
-static void rec_event(int k, cudaStream_t st) {
-  if (k < g_nev && g_ev[k]) cudaEventRecord(g_ev[k], st);
+static cudaError_t rec_event(int k, cudaStream_t st) {
+  if (k < g_nev && g_ev[k]) return cudaEventRecord(g_ev[k], st);
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ epoch
@@ -1175,6 +1217,7 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
                const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
                float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
                void* workspace, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   return epoch_impl(s, users, user_sched, items, item_sched, W, ldw, H, ldh, d, b, alpha0, cache,
                     workspace, ws_bytes, stream, nullptr);
 }
@@ -1185,6 +1228,7 @@ int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* u
                     int64_t ldh_host, float* W, int32_t ldw, float* H, int32_t ldh, int32_t d,
                     int32_t b, float alpha0, float* cache, float* cache_out, void* workspace,
                     size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (!W_in || !W_out || !H_in || !H_out || ldw_host < d || ldh_host < d)
     return fail(s, IALS_E_INVALID, "epoch_host: bad host buffers");
@@ -1223,7 +1267,10 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                pass_ws(items->n_rows, items->n_fixed, b, item_sched->n_slices, item_sched->n_heavy));
   const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 32 && d % 4 == 0 &&
                        ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
-                       reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= pass_need + tcb &&
+                       reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= tcb &&
+                       // the pass scratch left below the 1 KB-aligned carve start
+                       (long long)(((ws_bytes - tcb) & ~size_t(1023)) - (slab_bytes + gbytes)) >=
+                           (long long)pass_need &&
                        get_encode(s) == IALS_OK;
   TcCopies cw{}, ch{};
   float *P = nullptr, *sth = nullptr, *stl = nullptr;
@@ -1255,7 +1302,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
     if (rc) return rc;
   }
-  rec_event(0, st);
+  CUDA_TRY(s, rec_event(0, st));
   int rc = IALS_OK;
   // Host staging with the fused sweep: the first user pass runs chunk by
   // chunk of user rows, each chunk's sweep starting once its rows of W have
@@ -1345,7 +1392,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                           stream);
     if (rc) return rc;
   }
-  rec_event(1, st);
+  CUDA_TRY(s, rec_event(1, st));
   int ek = 2;
   for (int b0 = 0; b0 < d; b0 += b) {
     const int bb = std::min(b, d - b0);
@@ -1358,7 +1405,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       rc = gramian_impl(s, H, items->n_rows, ldh, d, b0, bb, slab, part, gbytes, st);
     }
     if (rc) return rc;
-    rec_event(ek++, st);
+    CUDA_TRY(s, rec_event(ek++, st));
     if (first_chunked) s->chunk = &plan;
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
                         pws, pbytes, st, tc_gemm, nullptr, items);
@@ -1369,7 +1416,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                       size_t(bb) * 4, size_t(users->n_rows), cudaMemcpyDeviceToHost);
       if (rc) return rc;
     }
-    rec_event(ek++, st);
+    CUDA_TRY(s, rec_event(ek++, st));
     if (tc_gemm) {   // (chunked: W's copies are built here, after its first block)
       rc = first_chunked ? sync_copies(s, W, ldw, d, 0, d, cw, st)
                          : sync_copies(s, W, ldw, d, b0, bb, cw, st);
@@ -1379,7 +1426,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       rc = gramian_impl(s, W, users->n_rows, ldw, d, b0, bb, slab, part, gbytes, st);
     }
     if (rc) return rc;
-    rec_event(ek++, st);
+    CUDA_TRY(s, rec_event(ek++, st));
     rc = side_pass_impl(s, items, item_sched, W, ldw, H, ldh, d, b0, bb, slab, alpha0, cache, 1,
                         pws, pbytes, st, tc_gemm, nullptr, users);
     if (rc) return rc;
@@ -1392,7 +1439,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       rc = sync_copies(s, H, ldh, d, b0, bb, ch, st);
       if (rc) return rc;
     }
-    rec_event(ek++, st);
+    CUDA_TRY(s, rec_event(ek++, st));
   }
   if (host) {   // the maintained cache, then the caller's stream waits for every copy
     if (host->cache_out) {
@@ -1454,6 +1501,7 @@ int ials_build_csr(ials_session* s, int32_t U, int32_t I, int64_t n, const int32
                    const int32_t* items, int32_t* user_ptr, int32_t* user_cols, int32_t* order,
                    int32_t* item_ptr, int32_t* item_cols, int32_t* item_pos, void* workspace,
                    size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (U < 1 || I < 1 || n < 0 || n >= (int64_t(1) << 31))
     return fail(s, IALS_E_INVALID, "build_csr: bad sizes (U=%d I=%d n=%lld)", U, I, (long long)n);
@@ -1498,6 +1546,7 @@ int ials_build_csr(ials_session* s, int32_t U, int32_t I, int64_t n, const int32
 int ials_topk(ials_session* s, int32_t n_rows, int32_t n_cols, float* scores, int64_t lds,
               const int32_t* ex_ptr, const int32_t* ex_cols, int32_t k, int32_t* out,
               int32_t* counts, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (n_rows < 0 || n_cols < 0 || lds < n_cols || k < 1 || k > kTopkMax)
     return fail(s, IALS_E_INVALID, "topk: bad sizes (rows=%d cols=%d k=%d, k <= %d)", n_rows, n_cols,
@@ -1523,6 +1572,7 @@ size_t ials_loss_workspace_bytes(int32_t d) {
 int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* items,
                     const float* W, int32_t ldw, const float* H, int32_t ldh, int32_t d,
                     double* out, void* workspace, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (!users || !items || !W || !H || !out) return fail(s, IALS_E_INVALID, "loss: NULL argument");
   cudaStream_t st = S(stream);

@@ -395,15 +395,18 @@ class Engine:
         The graph is keyed on the buffers, so W / H / cache must stay the same
         tensors between calls."""
         key = (W.data_ptr(), H.data_ptr(), cache.data_ptr(), int(b), float(alpha0))
-        g = getattr(self, "_graphs", {}).get(key)
-        if g is None:
+        entry = getattr(self, "_graphs", {}).get(key)
+        if entry is None or entry[1] is not self._ws:
+            # (re)captured when the workspace the graph baked in was replaced;
+            # each graph keeps its own workspace tensor alive
             self.epoch(W, H, cache, b, alpha0)          # attributes / workspace set up
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 self.epoch(W, H, cache, b, alpha0)
-            self.__dict__.setdefault("_graphs", {})[key] = g
-        g.replay()
+            entry = (g, self._ws)
+            self.__dict__.setdefault("_graphs", {})[key] = entry
+        entry[0].replay()
 
     def loss_terms(self, W, H):
         """Device fp64 loss pieces; returns a (4,) float64 CUDA tensor."""

@@ -86,6 +86,14 @@ def _layout(partition: BlockPartition):
     return perm, spans, identity
 
 
+def _uniform_spans(spans, dim: int) -> bool:
+    """True when the spans are exactly partition_dims(dim, b)'s blocks -- every
+    span (b0, min(b, dim - b0)) for b0 = 0, b, 2b, ... -- which is what one
+    ials_epoch call sweeps.  A wider (or narrower) last block is not."""
+    b = spans[0][1]
+    return list(spans) == [(s, min(b, dim - s)) for s in range(0, dim, b)]
+
+
 class DeviceTrainer:
     """W, H and the cache resident on one device for a dataset + config."""
 
@@ -113,7 +121,7 @@ class DeviceTrainer:
             self.cache.copy_(torch.from_numpy(np.asarray(cache.scores, dtype=np.float32)))
         bmax = max(b for _, b in self.spans)
         self.slab = torch.empty((model.dim, bmax), dtype=torch.float32, device=self.rt.device)
-        self.uniform = self.identity and all(b == self.spans[0][1] for _, b in self.spans[:-1])
+        self.uniform = self.identity and _uniform_spans(self.spans, model.dim)
 
     # ---------------------------------------------------------------- passes
     def pass_(self, side, b0, b):

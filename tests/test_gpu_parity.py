@@ -352,3 +352,29 @@ def test_tensor_core_sweep_labels_and_weights(ials, d, b):
     assert relmax(m.user_factors, w) < TOL and relmax(m.item_factors, h) < TOL
     want = orc.loss(w, h, csr, 0.1, 1e-3, 1.0)
     assert abs(reports[-1].loss - want) / want < TOL
+
+
+def test_wider_last_block_matches_oracle(ials):
+    """A contiguous partition with a wider last block: the epoch
+    must run the partition's own blocks (a 10-wide then a 20-wide Newton step),
+    not three 10-wide blocks."""
+    from oracle import ialspp_oracle as orc
+    rng = np.random.default_rng(11)
+    U, I, nnz, d = 400, 150, 5000, 30
+    users = rng.integers(0, U, nnz)
+    items = np.minimum(rng.zipf(1.3, nnz) - 1, I - 1)
+    data = ials.InteractionDataset(U, I, users, items)
+    cfg = ials.SolverConfig(dim=d, block_size=10, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=1, seed=3)
+    part = ials.BlockPartition((np.arange(0, 10), np.arange(10, 30)), d)
+    model = ials.init_model(cfg, U, I)
+    model.user_factors[:] = model.user_factors.astype(np.float32)
+    model.item_factors[:] = model.item_factors.astype(np.float32)
+    w, h = model.user_factors.copy(), model.item_factors.copy()
+    cache = ials.PredictionCache.zeros(data.n_interactions)
+    ials.ialspp_epoch(model, data, cache, cfg, part)
+    csr = orc.build_csr(U, I, users, items)
+    orc.ialspp_epoch(w, h, csr, np.zeros(nnz), 0.1, 1e-3, 1.0,
+                     [np.arange(0, 10), np.arange(10, 30)])
+    for got, want in ((model.user_factors, w), (model.item_factors, h)):
+        assert relf(got, want) < TOL and relmax(got, want) < TOL

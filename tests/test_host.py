@@ -157,3 +157,17 @@ def test_no_cpu_fallback_without_device(monkeypatch):
         ials.train(model, data, cfg)
     with pytest.raises(RuntimeError):
         ials.compute_predictions(model, data)
+
+
+def test_uniform_spans_only_for_partition_dims():
+    """a contiguous partition whose last block is wider than the
+    first is not partition_dims(d, b) and must not go to one ials_epoch call."""
+    from paper_2110_14044_b200.solvers import _layout, _uniform_spans
+    for d, b in ((30, 10), (30, 7), (8, 8), (13, 1)):
+        _, spans, ident = _layout(ials.partition_dims(d, b))
+        assert ident and _uniform_spans(spans, d)
+    wide_last = ials.BlockPartition((np.arange(0, 10), np.arange(10, 30)), 30)
+    _, spans, ident = _layout(wide_last)
+    assert ident and not _uniform_spans(spans, 30)
+    narrow_mid = ials.BlockPartition((np.arange(0, 10), np.arange(10, 15), np.arange(15, 30)), 30)
+    assert not _uniform_spans(_layout(narrow_mid)[1], 30)
