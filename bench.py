@@ -118,6 +118,16 @@ def roofline_model(U, I, S, d, b, p_fp32_tflops, bw_gbs):
             "t_P": t_p, "t_epoch": t_sw + t_g + t_p, "sweep_bound": bound, "B": B}
 
 
+def config_dict(cfg_key, U, I, S, world):
+    """The workload description both arms print (same dict: same config)."""
+    shape, d, b, desc = CONFIGS[cfg_key]
+    return {"workload": cfg_key, "desc": desc, "users": U, "items": I, "nnz": S,
+            "d": d, "b": b, "alpha0": ALPHA0, "reg": REG, "reg_exponent": NU,
+            "parallelism": f"replicas x{world}" if world > 1 else "single",
+            "l2": ("inputs larger than L2 (W,H,cache,CSR > 126 MB)" if (U + I) * d * 4 + 12 * S > 126e6
+                   else "inputs fit in L2 (launch-bound config)")}
+
+
 # --------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -358,6 +368,37 @@ def run_ours(args, cfg_key):
                "d2h_bytes_per_step": 4 * (U + I) * d + 4 * S,
                "path": "ials_epoch_host C-ABI call: W/H from pinned host, W/H/cache back, copies overlapped with the epoch"}
 
+    # ---- e2e through the reference's own public API: ialspp_epoch(model, data,
+    # cache, config) on the caller's float64 NumPy model (solvers.py:340-375),
+    # results written back in place every step (wall clock around the calls;
+    # each call returns with the host arrays final)
+    e2e_api = None
+    if not args.no_e2e and world == 1:
+        import paper_2110_14044_b200 as ials
+        data = ials.InteractionDataset(U, I, ds["users"], ds["user_cols"])
+        mcfg = ials.SolverConfig(dim=d, block_size=b, unobserved_weight=ALPHA0, reg=REG,
+                                 reg_exponent=NU, init_stddev=SIGMA, seed=0)
+        model = ials.FactorModel(W0.cpu().double().numpy(), H0.cpu().double().numpy())
+        pcache = ials.PredictionCache.zeros(S)
+        for e in range(max(1, args.warmup)):
+            ials.ialspp_epoch(model, data, pcache, mcfg, epoch_index=e)
+        torch.cuda.synchronize(dev)
+        n0 = int(eng.lib.ials_launch_count())
+        t0 = time.perf_counter()
+        for e in range(args.steps):
+            ials.ialspp_epoch(model, data, pcache, mcfg, epoch_index=e)
+        api_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        e2e_api = {"value": updates / (api_ms / 1e3), "unit": "nnz*d/s",
+                   "ms_per_step": round(api_ms, 3),
+                   "h2d_bytes_per_step": 8 * (U + I) * d,
+                   "d2h_bytes_per_step": 8 * (U + I) * d + 8 * S,
+                   "gpu_launches_per_step": (int(eng.lib.ials_launch_count()) - n0) / args.steps,
+                   "path": ("paper_2110_14044_b200.ialspp_epoch(model, data, cache, config): the "
+                            "reference's drop-in call on its float64 NumPy model and cache, updated "
+                            "in place (wall clock; host arrays page-locked once, f64 copies and "
+                            "casts on the GPU overlapped with the epoch)")}
+        del model, pcache, data
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(ds, d, b, budget_s=args.cpu_budget)
@@ -370,13 +411,13 @@ def run_ours(args, cfg_key):
             "epoch_seconds": round(ms_step / 1e3, 6),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded Zipf/lognormal stand-in for ML20M/MSD shapes)",
-            "config": {"workload": cfg_key, "desc": desc, "users": U, "items": I, "nnz": S,
-                       "d": d, "b": b, "alpha0": ALPHA0, "reg": REG, "reg_exponent": NU,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (W,H,cache,CSR > 126 MB)" if (U + I) * d * 4 + 12 * S > 126e6 else "inputs fit in L2 (launch-bound config)"},
+            "config": config_dict(cfg_key, U, I, S, world),
             "phases_ms": {k: round(v / args.steps, 4) for k, v in ph.items()},
             "roofline": roof,
-            "e2e": e2e,
+            # headline end to end: the reference-facing call; the fp32 pinned
+            # C-ABI call (ials_epoch_host) beside it
+            "e2e": e2e_api if e2e_api is not None else e2e,
+            "e2e_cabi": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": n_launches,
@@ -486,14 +527,31 @@ def run_sharded(args, cfg_key, ds, dev, rank, world):
 
 
 # ------------------------------------------------------------------ CPU arm
+def reference_module():
+    """The unmodified reference (``blockals``) installed under baseline/_ref
+    (``pip install --no-deps --target baseline/_ref``; git-ignored, shipped to
+    the GPU box), or None when it is not there."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "blockals")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import blockals
+        from blockals import solvers as ref_solvers
+    except Exception:   # pragma: no cover - broken install
+        return None
+    return blockals, ref_solvers
+
+
 def cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
-    """Oracle port (oracle/ialspp_oracle.py, NumPy f64 + OpenBLAS, all host
-    threads) on a bounded systematic sample: predictions for a sample of user
-    rows, one block's two slabs in full, the user pass for every s_u-th user and
-    the item pass for every s_i-th item (degree-sorted), scaled by the stride;
-    epoch = t_pred + B * t_block ("extrapolated from 1 of B blocks").  The BLAS
-    pool is opened to every host core for the measurement (torchrun exports
-    OMP_NUM_THREADS=1 to its ranks)."""
+    """The reference CPU solver on this host's cores, on a bounded systematic
+    sample of one epoch: the UNMODIFIED reference from baseline/_ref when it is
+    installed (``kind`` "reference": its own ``compute_predictions``,
+    ``partial_gramian`` and ``_newton_side_pass``, solvers.py:152-186, over
+    sub-views of the sampled rows), else the oracle port (``kind`` "port",
+    oracle/ialspp_oracle.py).  The BLAS pool is opened to every host core for
+    the measurement (torchrun exports OMP_NUM_THREADS=1 to its ranks)."""
     try:
         from threadpoolctl import threadpool_limits
         limits = threadpool_limits(limits=os.cpu_count() or 1)
@@ -506,12 +564,19 @@ def cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
             limits.restore_original_limits()
 
 
+def _entries(rows, ptr):
+    counts = ptr[rows + 1] - ptr[rows]
+    starts = np.repeat(ptr[rows], counts)
+    return starts + np.arange(counts.sum()) - np.repeat(np.cumsum(counts) - counts, counts)
+
+
 def _cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
-    from oracle import ialspp_oracle as orc
+    from oracle import ialspp_oracle as orc   # the row sampler; the port itself if no reference
+    refm = reference_module()
     U, I = int(ds["U"]), int(ds["I"])
     uptr, iptr = ds["user_ptr"].astype(np.int64), ds["item_ptr"].astype(np.int64)
     S = int(uptr[-1])
-    rng = np.random.default_rng(0)
+    rng = np.random.default_rng(seed)
     scale = SIGMA / np.sqrt(d)
     w = rng.normal(0.0, scale, size=(U, d))
     h = rng.normal(0.0, scale, size=(I, d))
@@ -524,35 +589,72 @@ def _cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
     li = orc.effective_reg(np.diff(iptr), U, REG, ALPHA0, NU)
     B = -(-d // b)
     blk = np.arange(min(b, d))
-    # size the strides from a quick calibration of the per-entry cost
+    # size the strides from a rough per-unit cost so one step is ~budget_s
     work_u = (S * b * b + U * (d * b + b ** 3 / 3))
-    per_unit = 2.0e-10 * max(1.0, b / 32)    # rough s per (flop-ish unit) on the host
+    per_unit = 2.0e-10 * max(1.0, b / 32)
     s_u = max(1, int(work_u * per_unit * B / (0.35 * budget_s)))
     s_i = max(1, s_u // 8)
     s_p = max(1, int(S * d * 2e-9 / (0.15 * budget_s)))
-    t0 = time.perf_counter()
     prows = np.arange(0, U, s_p)
-    idx = np.concatenate([np.arange(uptr[r], uptr[r + 1]) for r in prows])
-    _ = orc.predictions(w, h, users[idx], ucols[idx])
-    t_pred = (time.perf_counter() - t0) * (S / max(idx.size, 1))
-    cache = np.zeros(S)
-    t0 = time.perf_counter()
-    slab_h = orc.partial_gramian(h, blk)
-    t_gh = time.perf_counter() - t0
+    pidx = _entries(prows, uptr)
+    if refm is not None:
+        ref, rs = refm
+        from blockals import data as ref_data
+        # predictions over the sampled users' interactions (model.py:153-165)
+        pdata = ref.InteractionDataset(prows.size, I, np.repeat(np.arange(prows.size),
+                                       uptr[prows + 1] - uptr[prows]), ucols[pidx])
+        pmodel = ref.FactorModel(np.ascontiguousarray(w[prows]), h)
+        t0 = time.perf_counter()
+        ref.compute_predictions(pmodel, pdata)
+        t_pred = (time.perf_counter() - t0) * (S / max(pidx.size, 1))
+        gram = lambda m: ref.partial_gramian(m, blk)
+
+        def run_rows(ptr, cols, pos, fixed, own, slab, lam, rows):
+            # the reference's own side pass over a SideView of just these rows
+            # (their entries, a compact cache); view buckets are built once per
+            # dataset in the reference, so outside the timed region
+            ent = _entries(rows, ptr)
+            sub_ptr = np.zeros(rows.size + 1, dtype=np.int64)
+            np.cumsum(ptr[rows + 1] - ptr[rows], out=sub_ptr[1:])
+            ones = np.ones(ent.size)
+            view = ref_data.SideView(rows.size, fixed.shape[0], sub_ptr, cols[ent], ones, ones,
+                                np.arange(ent.size))
+            view.buckets()
+            upd = np.ascontiguousarray(own[rows])
+            cache_ext = np.zeros(ent.size + 1)
+            t0 = time.perf_counter()
+            rs._newton_side_pass(view, fixed, upd, cache_ext, blk, slab, ALPHA0, lam[rows])
+            return time.perf_counter() - t0
+        kind, what = "reference", ("the unmodified reference (baseline/_ref blockals 0.1.0): "
+                                   "compute_predictions, partial_gramian, _newton_side_pass")
+    else:
+        t0 = time.perf_counter()
+        orc.predictions(w, h, users[pidx], ucols[pidx])
+        t_pred = (time.perf_counter() - t0) * (S / max(pidx.size, 1))
+        gram = lambda m: orc.partial_gramian(m, blk)
+        cache = np.zeros(S)
+
+        def run_rows(ptr, cols, pos, fixed, own, slab, lam, rows):
+            t0 = time.perf_counter()
+            orc.side_pass(ptr, cols, lab, lab, pos, fixed, own, cache, blk, slab, ALPHA0, lam,
+                          rows=rows)
+            return time.perf_counter() - t0
+        kind, what = "port", "oracle/ialspp_oracle.py (f64 NumPy restatement)"
+
     def timed_pass(ptr, cols, pos, fixed, own, slab, lam, stride):
         head, tail = orc.systematic_rows(np.diff(ptr), stride)
         t = 0.0
         for rows, weight in ((head, 1.0), (tail, float(stride))):
             if rows.size:
-                t0 = time.perf_counter()
-                orc.side_pass(ptr, cols, lab, lab, pos, fixed, own, cache, blk, slab, ALPHA0,
-                              lam, rows=rows)
-                t += (time.perf_counter() - t0) * weight
+                t += run_rows(ptr, cols, pos, fixed, own, slab, lam, rows) * weight
         return t
 
+    t0 = time.perf_counter()
+    slab_h = gram(h)
+    t_gh = time.perf_counter() - t0
     t_user = timed_pass(uptr, ucols, np.arange(S), h, w, slab_h, lu, s_u)
     t0 = time.perf_counter()
-    slab_w = orc.partial_gramian(w, blk)
+    slab_w = gram(w)
     t_gw = time.perf_counter() - t0
     t_item = timed_pass(iptr, icols, ipos, w, h, slab_w, li, s_i)
     t_epoch = t_pred + B * (t_gh + t_user + t_gw + t_item)
@@ -563,10 +665,10 @@ def _cpu_baseline(ds, d, b, budget_s=15.0, seed=0):
     except Exception:
         blas, threads = [], os.cpu_count()
     return {"value": 2.0 * S * d / t_epoch, "unit": "nnz*d/s", "cores": int(threads),
-            "kind": "port", "epoch_seconds_est": round(t_epoch, 2),
-            "sample": (f"oracle/ialspp_oracle.py f64 on this host: predictions for every {s_p}th "
-                       f"user, block-0 slabs in full, user / item pass on the 64 heaviest rows "
-                       f"in full plus every {s_u}th / {s_i}th run of 64 degree-sorted rows "
+            "kind": kind, "epoch_seconds_est": round(t_epoch, 2),
+            "sample": (f"{what}, f64 on this host ({os.cpu_count()} cores): predictions for every "
+                       f"{s_p}th user, block-0 slabs in full, user / item pass on the 64 heaviest "
+                       f"rows in full plus every {s_u}th / {s_i}th run of 64 degree-sorted rows "
                        f"(scaled by the stride); epoch = t_pred + {B} x t_block "
                        f"(extrapolated from 1 of {B} blocks)"),
             "phase_seconds_est": {"pred": round(t_pred, 3), "gram": round(t_gh + t_gw, 3),
@@ -581,7 +683,7 @@ def run_reference(args, cfg_key):
         return
     shape, d, b, desc = CONFIGS[cfg_key]
     ds = dataset(shape)
-    S = int(ds["user_ptr"][-1])
+    U, I, S = int(ds["U"]), int(ds["I"]), int(ds["user_ptr"][-1])
     vals = []
     for _ in range(args.warmup):
         cpu_baseline(ds, d, b, budget_s=args.cpu_budget)
@@ -594,9 +696,10 @@ def run_reference(args, cfg_key):
             "ms_per_step": round(2.0 * S * d / value * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Zipf/lognormal stand-in for ML20M/MSD shapes)",
-            "config": {"workload": cfg_key, "desc": desc, "nnz": S, "d": d, "b": b},
+            "config": config_dict(cfg_key, U, I, S, world),
             "cpu_baseline": {"value": value, "unit": "nnz*d/s", "cores": last["cores"],
-                             "kind": "port", "sample": last["sample"]},
+                             "kind": last["kind"], "sample": last["sample"],
+                             "epoch_seconds_est": last["epoch_seconds_est"]},
             "e2e": {"value": value, "unit": "nnz*d/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -204,6 +204,18 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
                float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
                void* workspace, size_t ws_bytes, void* stream);
 
+/* The passes [pass0, pass0 + npass) of ials_epoch, pass p = 2 * block + side
+ * (0 user, 1 item), with the prediction cache recomputed first when
+ * recompute_cache != 0: exactly the code ials_epoch runs for those passes
+ * (same GEMMs, sweep kernels and schedules), so a caller (the parity tests)
+ * can inspect the state between passes.  ials_epoch == ials_epoch_range(...,
+ * 0, 2 * ceil(d / b), 1). */
+int ials_epoch_range(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                     const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
+                     float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
+                     void* workspace, size_t ws_bytes, void* stream, int32_t pass0, int32_t npass,
+                     int32_t recompute_cache);
+
 /* ials_epoch for a model held in (pinned) HOST memory, the reference's
  * in-place ialspp_epoch contract end to end: W_in / H_in are copied to the
  * device buffers W / H, the epoch runs, and W_out / H_out (may alias the
@@ -221,6 +233,27 @@ int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* u
                     int64_t ldh_host, float* W, int32_t ldw, float* H, int32_t ldh, int32_t d,
                     int32_t b, float alpha0, float* cache, float* cache_out, void* workspace,
                     size_t ws_bytes, void* stream);
+
+/* ials_epoch_host for the reference's own float64 model (FactorModel's
+ * C-contiguous f64 W / H, PredictionCache's f64 scores): the same overlapped
+ * epoch, with every host copy going through device float64 staging and a cast
+ * kernel on the copy stream (f64 -> fp32 round-to-nearest on the way in, exact
+ * fp32 -> f64 on the way out), so the host does no conversion and no extra
+ * pass over the model.  `staging` (device) holds ials_host64_staging_bytes.
+ * Host buffers should be page-locked (cudaHostRegister) for the copies to
+ * overlap; pageable buffers work but serialise. */
+/* Page-lock (cudaHostRegister, portable) / release a caller's host range in
+ * place, so ials_epoch_host64 copies overlap the epoch without a host-side
+ * staging copy.  Registering an already registered range is not an error. */
+int ials_host_register(void* ptr, size_t bytes);
+int ials_host_unregister(void* ptr);
+size_t ials_host64_staging_bytes(int32_t n_users, int32_t n_items, int32_t d, int64_t nnz);
+int ials_epoch_host64(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                      const ials_side* items, const ials_sched* item_sched, const double* W_in,
+                      double* W_out, int64_t ldw_host, const double* H_in, double* H_out,
+                      int64_t ldh_host, float* W, int32_t ldw, float* H, int32_t ldh, int32_t d,
+                      int32_t b, float alpha0, float* cache, double* cache_out, void* staging,
+                      size_t staging_bytes, void* workspace, size_t ws_bytes, void* stream);
 
 /* Workspace bytes for ials_loss_terms at embedding dimension d. */
 size_t ials_loss_workspace_bytes(int32_t d);

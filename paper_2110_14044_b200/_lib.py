@@ -75,6 +75,17 @@ SIGNATURES = {
     "ials_epoch": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
                            ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_i32, c_p,
                            c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p]),
+    "ials_host_register": (c_i32, [c_p, c_sz]),
+    "ials_host_unregister": (c_i32, [c_p]),
+    "ials_host64_staging_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64]),
+    "ials_epoch_host64": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
+                                  ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_p,
+                                  c_i64, c_p, c_p, c_i64, c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_f,
+                                  c_p, c_p, c_p, c_sz, c_p, c_sz, c_p]),
+    "ials_epoch_range": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
+                                 ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_i32,
+                                 c_p, c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p, c_i32, c_i32,
+                                 c_i32]),
     "ials_epoch_host": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
                                 ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_p, c_i64,
                                 c_p, c_p, c_i64, c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_f, c_p, c_p,

@@ -70,3 +70,37 @@ def default_engine_session(device=None) -> Runtime:
 def to_device_f32(arr, device) -> torch.Tensor:
     a = np.ascontiguousarray(arr, dtype=np.float32)
     return torch.from_numpy(a).to(device, non_blocking=False)
+
+
+# ------------------------------------------------------------ page-locked host arrays
+_PINNED = {}
+
+
+def pin_host_array(arr: np.ndarray) -> bool:
+    """Page-lock ``arr``'s memory in place (ials_host_register) once, so the
+    epoch's host copies run asynchronously beside the kernels.  The range is
+    released when ``arr`` itself is garbage-collected (it keeps its buffer
+    alive until then).  Returns False if the driver refused (the copies then
+    still work, from pageable memory)."""
+    if arr.nbytes == 0:
+        return False
+    key = (arr.ctypes.data, arr.nbytes)
+    if key in _PINNED:
+        return True
+    lib = _lib.load()
+    if lib.ials_host_register(ctypes.c_void_p(key[0]), ctypes.c_size_t(key[1])) != 0:
+        return False
+
+    def _release(k=key):
+        if _PINNED.pop(k, None) is not None:
+            try:
+                _lib.load().ials_host_unregister(ctypes.c_void_p(k[0]))
+            except Exception:
+                pass
+    try:
+        _PINNED[key] = weakref.finalize(arr, _release)
+    except TypeError:      # not weak-referenceable: release right away (pageable copies)
+        _PINNED[key] = True
+        _release()
+        return False
+    return True

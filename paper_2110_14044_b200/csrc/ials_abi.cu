@@ -23,6 +23,7 @@
 #include "ials_sweep_tc.cuh"
 #include "ials_sweep_tc2.cuh"
 #include "ials_sweep_tc4.cuh"
+#include "ials_sweep_pk.cuh"
 #include "ials_gemm_tc.cuh"
 #include "ials_sweep_b1.cuh"
 
@@ -116,8 +117,8 @@ static bool tc4_enabled();
 static int block_tile(int b) {
   if (b <= 8) return 8;
   if (b <= 16) return 16;
-  if (b <= 32) return 32;
-  if (b <= 64) return tc4_enabled() ? 128 : 64;
+  if (b <= 32) return tc4_enabled() ? 128 : 32;   // packed tensor-core sweep, 4 rows per tile
+  if (b <= 64) return tc4_enabled() ? 128 : 64;   // packed tensor-core sweep, 2 rows per tile
   if (b <= 128) return 128;
   return 256;
 }
@@ -525,10 +526,10 @@ static int make_map(ials_session* s, CUtensorMap* m, const float* ptr, uint64_t 
 // rows of `fixed` (n_fixed x d, ld ldf) in boxes of 128 columns x 1 row: the
 // tile::gather4 source of the fused sweep (out-of-range columns read as 0)
 static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, uint64_t d, uint64_t rows,
-                           uint64_t ld_floats) {
+                           uint64_t ld_floats, uint32_t box_w = 128) {
   cuuint64_t gdim[2] = {d, rows};
   cuuint64_t gstr[1] = {ld_floats * 4};
-  cuuint32_t box[2] = {128, 1};
+  cuuint32_t box[2] = {box_w, 1};
   cuuint32_t es[2] = {1, 1};
   const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim,
                               gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -549,9 +550,22 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   CUtensorMap fmap;
   memset(&fmap, 0, sizeof(fmap));
   int use_tma = 0;
+  // light rows: the fused sweep (b 65..128) or the packed one (b 17..64: G
+  // rows per 128-lane tile, slot width 128 / G), boxes of the slot width
+  const int G = p.b > 64 ? 1 : (p.b > 32 ? 2 : 4);
+  // (the map's extent is the fixed matrix's own width: p.ldf columns when the
+  // pass gathers from a compact column copy, d otherwise)
+  const uint64_t fcols = (uint64_t)p.fixed_cols;
   if (p.vec && p.side.n_fixed > 0 && get_encode(s) == IALS_OK &&
-      make_gather_map(s, &fmap, p.fixed, p.d, p.side.n_fixed, p.ldf) == IALS_OK)
+      make_gather_map(s, &fmap, p.fixed, fcols, p.side.n_fixed, p.ldf, 128 / G) == IALS_OK)
     use_tma = 1;
+  CUtensorMap hmap;   // heavy-row partials: the 128-wide tile
+  memset(&hmap, 0, sizeof(hmap));
+  int use_tma_h = use_tma;
+  if (use_tma && G > 1)
+    use_tma_h = make_gather_map(s, &hmap, p.fixed, fcols, p.side.n_fixed, p.ldf, 128) == IALS_OK;
+  else
+    hmap = fmap;
   // heavy-row partials run on a second stream beside the light rows (they
   // touch disjoint rows and only read the cache), so each kernel's last wave
   // is filled by the other's CTAs; joined before the heavy solve
@@ -574,11 +588,20 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay4::BYTES));
         CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       }
+      for (auto k : {k_sweep_pk<2, false>, k_sweep_pk<2, true>}) {
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PkLay<2>::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
+      for (auto k : {k_sweep_pk<4, false>, k_sweep_pk<4, true>}) {
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PkLay<4>::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
       init |= dev_bit();
     }
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
-    const int grid = std::min(p.n_light, 4 * kNumSMs);   // TMEM: 4 x 128 columns per SM
+    // TMEM: 4 x 128 columns per SM; the packed sweep takes G rows per task
+    const int grid = std::min((p.n_light + G - 1) / G, 4 * kNumSMs);
     const ChunkPlan* cp = s->chunk;
     for (int c = 0; c < (cp ? cp->nch : 1); ++c) {
       SweepParams q = p;
@@ -590,10 +613,22 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         q.chunk = c;
         if (c > 0) CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt + 2, 0, sizeof(int), st));   // row queue
       }
-      if (unit)
-        k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
-      else
-        k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
+      if (G == 1) {
+        if (unit)
+          k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
+        else
+          k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
+      } else if (G == 2) {
+        if (unit)
+          k_sweep_pk<2, true><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
+        else
+          k_sweep_pk<2, false><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
+      } else {
+        if (unit)
+          k_sweep_pk<4, true><<<grid, 128, PkLay<4>::BYTES, st>>>(q, fmap, use_tma);
+        else
+          k_sweep_pk<4, false><<<grid, 128, PkLay<4>::BYTES, st>>>(q, fmap, use_tma);
+      }
       LAUNCH_CHECK(s);
     }
   }
@@ -609,9 +644,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     const int threads = L::NT * L::RPC;
     const int hg = std::min(p.n_slices, 4 * kNumSMs);
     if (unit)
-      k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, hst>>>(p, fmap, use_tma);
+      k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, hst>>>(p, hmap, use_tma_h);
     else
-      k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, hst>>>(p, fmap, use_tma);
+      k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, hst>>>(p, hmap, use_tma_h);
     LAUNCH_CHECK(s);
     if (fork) {
       CUDA_TRY(s, cudaEventRecord(s->ev_join, hst));
@@ -764,7 +799,7 @@ template <int BT>
 static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<BT>;
   if (BT == 128 && p.b > 32 && tc_enabled()) return launch_sweep_tc128(s, p, st);
-  if (BT == 128 && p.b > 32 && tc4_enabled()) return launch_sweep_tc4(s, p, nnz, st);
+  if (BT == 128 && p.b > 16 && tc4_enabled()) return launch_sweep_tc4(s, p, nnz, st);
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
   const int threads = L::NT * L::RPC;
@@ -822,6 +857,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.d = d;
   p.b0 = b0;
   p.fb0 = b0;
+  p.fixed_cols = d;
   p.b = b;
   p.slab = slab;
   p.alpha0 = alpha0;
@@ -866,6 +902,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.fixed = compact;
     p.ldf = ldc;
     p.fb0 = 0;
+    p.fixed_cols = ldc;
     p.vec = (b % 4 == 0) && (reinterpret_cast<uintptr_t>(compact) % 16 == 0);
   }
   p.redo_total = s->redo;
@@ -1191,25 +1228,74 @@ static cudaError_t rec_event(int k, cudaStream_t st) {
 // ------------------------------------------------------------------ epoch
 // host staging of ials_epoch_host (all pointers pinned host memory)
 struct EpochHost {
-  const float *W_in, *H_in;
-  float *W_out, *H_out, *cache_out;
+  const void *W_in, *H_in;
+  void *W_out, *H_out, *cache_out;
   int64_t ldw, ldh;
+  // float64 host model (ials_epoch_host64): the copies go through device f64
+  // staging (dense, ld = d) and cast kernels on the copy stream
+  bool f64 = false;
+  double *sW = nullptr, *sH = nullptr, *sC = nullptr;
 };
 
-// st -> copy stream dependency, then a 2-D copy on the copy stream
-static int stage_copy(ials_session* s, cudaStream_t st, void* dst, size_t dpitch, const void* src,
-                      size_t spitch, size_t width, size_t rows, cudaMemcpyKind kind) {
-  if (rows == 0 || width == 0) return IALS_OK;
-  CUDA_TRY(s, cudaEventRecord(s->ev_a, st));
-  CUDA_TRY(s, cudaStreamWaitEvent(s->copy_st, s->ev_a, 0));
-  CUDA_TRY(s, cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s->copy_st));
+static inline int cast_grid(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8LL * kNumSMs));
+}
+
+// rows [r0, r1) of a host matrix (host ld in elements) -> device fp32 rows,
+// on the copy stream (the caller orders it after / before the epoch's work)
+static int host_rows_in(ials_session* s, const EpochHost* h, const void* src, int64_t lds, float* dst,
+                        int ldd, int d, int r0, int r1, double* stage) {
+  if (r1 <= r0 || d <= 0) return IALS_OK;
+  const size_t rows = size_t(r1 - r0);
+  if (!h->f64) {
+    CUDA_TRY(s, cudaMemcpy2DAsync(dst + size_t(r0) * ldd, size_t(ldd) * 4,
+                                  static_cast<const float*>(src) + size_t(r0) * lds, size_t(lds) * 4,
+                                  size_t(d) * 4, rows, cudaMemcpyHostToDevice, s->copy_st));
+    return IALS_OK;
+  }
+  double* sg = stage + size_t(r0) * d;
+  CUDA_TRY(s, cudaMemcpy2DAsync(sg, size_t(d) * 8, static_cast<const double*>(src) + size_t(r0) * lds,
+                                size_t(lds) * 8, size_t(d) * 8, rows, cudaMemcpyHostToDevice,
+                                s->copy_st));
+  k_f64_to_f32_2d<<<cast_grid(int64_t(rows) * d), 256, 0, s->copy_st>>>(sg, d, dst + size_t(r0) * ldd,
+                                                                         ldd, d, int64_t(rows));
+  LAUNCH_CHECK(s);
   return IALS_OK;
 }
 
+// columns [c0, c0 + cw) of a device fp32 matrix (n rows) -> the host matrix,
+// on the copy stream once the work queued on `st` so far has finished
+static int host_cols_out(ials_session* s, cudaStream_t st, const EpochHost* h, void* dst, int64_t ldh_,
+                         const float* src, int lds, int n, int d, int c0, int cw, double* stage) {
+  if (n <= 0 || cw <= 0) return IALS_OK;
+  CUDA_TRY(s, cudaEventRecord(s->ev_a, st));
+  CUDA_TRY(s, cudaStreamWaitEvent(s->copy_st, s->ev_a, 0));
+  if (!h->f64) {
+    CUDA_TRY(s, cudaMemcpy2DAsync(static_cast<float*>(dst) + c0, size_t(ldh_) * 4, src + c0,
+                                  size_t(lds) * 4, size_t(cw) * 4, size_t(n),
+                                  cudaMemcpyDeviceToHost, s->copy_st));
+    return IALS_OK;
+  }
+  k_f32_to_f64_2d<<<cast_grid(int64_t(n) * cw), 256, 0, s->copy_st>>>(src + c0, lds, stage + c0, d, cw, n);
+  LAUNCH_CHECK(s);
+  CUDA_TRY(s, cudaMemcpy2DAsync(static_cast<double*>(dst) + c0, size_t(ldh_) * 8, stage + c0,
+                                size_t(d) * 8, size_t(cw) * 8, size_t(n), cudaMemcpyDeviceToHost,
+                                s->copy_st));
+  return IALS_OK;
+}
+
+
+// the passes of one epoch: p = 2 * block + side (0 user, 1 item); a range
+// [pass0, pass0 + npass) runs exactly the code ials_epoch runs for them
+struct PassRange {
+  int pass0, npass;
+  bool recompute;   // the prediction cache first (ials_epoch: yes)
+};
 static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                       const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
                       float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
-                      void* workspace, size_t ws_bytes, void* stream, const EpochHost* host);
+                      void* workspace, size_t ws_bytes, void* stream, const EpochHost* host,
+                      PassRange range = PassRange{0, 1 << 30, true});
 static int radix_sort_index(ials_session* s, const int* keys, int64_t n, int K, int* keys_out,
                             int* vals_out, int* tk, int* tv, int* hist, int* tot, cudaStream_t st);
 
@@ -1220,6 +1306,22 @@ int ials_epoch(ials_session* s, const ials_side* users, const ials_sched* user_s
   DevGuard _dg(s);
   return epoch_impl(s, users, user_sched, items, item_sched, W, ldw, H, ldh, d, b, alpha0, cache,
                     workspace, ws_bytes, stream, nullptr);
+}
+
+int ials_epoch_range(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                     const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
+                     float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
+                     void* workspace, size_t ws_bytes, void* stream, int32_t pass0, int32_t npass,
+                     int32_t recompute_cache) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  const int nb = (b >= 1 && d >= 1) ? (d + b - 1) / b : 0;
+  if (pass0 < 0 || npass < 0 || pass0 + npass > 2 * nb)
+    return fail(s, IALS_E_INVALID, "epoch_range: passes [%d, %d) outside [0, %d)", pass0,
+                pass0 + npass, 2 * nb);
+  return epoch_impl(s, users, user_sched, items, item_sched, W, ldw, H, ldh, d, b, alpha0, cache,
+                    workspace, ws_bytes, stream, nullptr,
+                    PassRange{pass0, npass, recompute_cache != 0});
 }
 
 int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* user_sched,
@@ -1242,10 +1344,70 @@ int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* u
                     workspace, ws_bytes, stream, &h);
 }
 
+int ials_host_register(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) return fail(nullptr, IALS_E_INVALID, "host_register: empty range");
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return IALS_OK;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, IALS_E_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+  }
+  return IALS_OK;
+}
+
+int ials_host_unregister(void* ptr) {
+  if (!ptr) return IALS_OK;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(nullptr, IALS_E_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+  }
+  return IALS_OK;
+}
+
+size_t ials_host64_staging_bytes(int32_t n_users, int32_t n_items, int32_t d, int64_t nnz) {
+  return al256(size_t(std::max(n_users, 0)) * std::max(d, 0) * 8) +
+         al256(size_t(std::max(n_items, 0)) * std::max(d, 0) * 8) + al256(size_t(std::max<int64_t>(nnz, 0)) * 8);
+}
+
+int ials_epoch_host64(ials_session* s, const ials_side* users, const ials_sched* user_sched,
+                      const ials_side* items, const ials_sched* item_sched, const double* W_in,
+                      double* W_out, int64_t ldw_host, const double* H_in, double* H_out,
+                      int64_t ldh_host, float* W, int32_t ldw, float* H, int32_t ldh, int32_t d,
+                      int32_t b, float alpha0, float* cache, double* cache_out, void* staging,
+                      size_t staging_bytes, void* workspace, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (!W_in || !W_out || !H_in || !H_out || ldw_host < d || ldh_host < d || !users || !items)
+    return fail(s, IALS_E_INVALID, "epoch_host64: bad host buffers");
+  if (!staging || staging_bytes < ials_host64_staging_bytes(users->n_rows, items->n_rows, d, users->nnz))
+    return fail(s, IALS_E_NOMEM, "epoch_host64: staging %zu < %zu bytes", staging_bytes,
+                ials_host64_staging_bytes(users->n_rows, items->n_rows, d, users->nnz));
+  if (!s->copy_st) {
+    CUDA_TRY(s, cudaStreamCreateWithFlags(&s->copy_st, cudaStreamNonBlocking));
+    CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_a, cudaEventDisableTiming));
+    CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_b, cudaEventDisableTiming));
+  }
+  EpochHost h{W_in, H_in, W_out, H_out, cache_out, ldw_host, ldh_host};
+  char* t = static_cast<char*>(staging);
+  h.f64 = true;
+  h.sW = reinterpret_cast<double*>(t);
+  t += al256(size_t(users->n_rows) * d * 8);
+  h.sH = reinterpret_cast<double*>(t);
+  t += al256(size_t(items->n_rows) * d * 8);
+  h.sC = reinterpret_cast<double*>(t);
+  return epoch_impl(s, users, user_sched, items, item_sched, W, ldw, H, ldh, d, b, alpha0, cache,
+                    workspace, ws_bytes, stream, &h);
+}
+
 static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched* user_sched,
                       const ials_side* items, const ials_sched* item_sched, float* W, int32_t ldw,
                       float* H, int32_t ldh, int32_t d, int32_t b, float alpha0, float* cache,
-                      void* workspace, size_t ws_bytes, void* stream, const EpochHost* host) {
+                      void* workspace, size_t ws_bytes, void* stream, const EpochHost* host,
+                      PassRange range) {
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (!users || !items || !user_sched || !item_sched)
     return fail(s, IALS_E_INVALID, "epoch: NULL argument");
@@ -1265,7 +1427,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   const size_t pass_need =
       std::max(pass_ws(users->n_rows, users->n_fixed, b, user_sched->n_slices, user_sched->n_heavy),
                pass_ws(items->n_rows, items->n_fixed, b, item_sched->n_slices, item_sched->n_heavy));
-  const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 32 && d % 4 == 0 &&
+  const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 16 && d % 4 == 0 &&
                        ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= tcb &&
                        // the pass scratch left below the 1 KB-aligned carve start
@@ -1291,11 +1453,10 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   if (host) {
     // H in full, then W in row chunks, host -> device on the copy stream; the
     // predictions of each user chunk start as soon as its rows have landed
-    const size_t es = sizeof(float);
     CUDA_TRY(s, cudaEventRecord(s->ev_a, st));   // W / H free on the device
     CUDA_TRY(s, cudaStreamWaitEvent(s->copy_st, s->ev_a, 0));
-    CUDA_TRY(s, cudaMemcpy2DAsync(H, size_t(ldh) * es, host->H_in, size_t(host->ldh) * es, size_t(d) * es,
-                                  size_t(items->n_rows), cudaMemcpyHostToDevice, s->copy_st));
+    int hr = host_rows_in(s, host, host->H_in, host->ldh, H, ldh, d, 0, items->n_rows, host->sH);
+    if (hr) return hr;
   }
   if (tc_gemm && !host) {
     int rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
@@ -1355,9 +1516,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       }
       const int r0 = c * per_chunk, r1 = std::min(U, r0 + per_chunk);
       if (r1 <= r0) return IALS_OK;
-      CUDA_TRY(s, cudaMemcpy2DAsync(W + size_t(r0) * ldw, size_t(ldw) * 4, host->W_in + size_t(r0) * host->ldw,
-                                    size_t(host->ldw) * 4, size_t(d) * 4, size_t(r1 - r0),
-                                    cudaMemcpyHostToDevice, s->copy_st));
+      int hr = host_rows_in(s, host, host->W_in, host->ldw, W, ldw, d, r0, r1, host->sW);
+      if (hr) return hr;
       CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));
       CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));   // W rows [r0, r1) are on the device
       int r = ials_predictions(s, r1 - r0, users->ptr + r0, users->cols, W + size_t(r0) * ldw, ldw, H,
@@ -1373,9 +1533,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     const int per = (U + nch - 1) / nch;
     for (int c = 0; c < nch && c * per < U; ++c) {
       const int r0 = c * per, r1 = std::min(U, r0 + per);
-      CUDA_TRY(s, cudaMemcpy2DAsync(W + size_t(r0) * ldw, size_t(ldw) * 4, host->W_in + size_t(r0) * host->ldw,
-                                    size_t(host->ldw) * 4, size_t(d) * 4, size_t(r1 - r0),
-                                    cudaMemcpyHostToDevice, s->copy_st));
+      rc = host_rows_in(s, host, host->W_in, host->ldw, W, ldw, d, r0, r1, host->sW);
+      if (rc) return rc;
       CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));
       CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));   // H and W rows [0, r1) are on the device
       rc = ials_predictions(s, r1 - r0, users->ptr + r0, users->cols, W + size_t(r0) * ldw, ldw, H,
@@ -1387,7 +1546,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
       if (rc) return rc;
     }
-  } else {
+  } else if (range.recompute) {
     rc = ials_predictions(s, users->n_rows, users->ptr, users->cols, W, ldw, H, ldh, d, cache,
                           stream);
     if (rc) return rc;
@@ -1397,6 +1556,10 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   for (int b0 = 0; b0 < d; b0 += b) {
     const int bb = std::min(b, d - b0);
     const bool first_chunked = chunked && b0 == 0;
+    const int pu = 2 * (b0 / b);
+    const bool do_u = pu >= range.pass0 && pu < range.pass0 + range.npass;
+    const bool do_i = pu + 1 >= range.pass0 && pu + 1 < range.pass0 + range.npass;
+    if (do_u) {
     if (tc_gemm) {
       rc = gram_tc(s, ch, d, b0, bb, P, slab, sth, stl, st);
       if (!rc && !first_chunked)
@@ -1412,11 +1575,13 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     s->chunk = nullptr;
     if (rc) return rc;
     if (host) {   // W[:, b0:b0+bb] is final: back to the host beside the rest of the epoch
-      rc = stage_copy(s, st, host->W_out + b0, size_t(host->ldw) * 4, W + b0, size_t(ldw) * 4,
-                      size_t(bb) * 4, size_t(users->n_rows), cudaMemcpyDeviceToHost);
+      rc = host_cols_out(s, st, host, host->W_out, host->ldw, W, ldw, users->n_rows, d, b0, bb,
+                         host->sW);
       if (rc) return rc;
     }
     CUDA_TRY(s, rec_event(ek++, st));
+    }   // do_u
+    if (!do_i) continue;
     if (tc_gemm) {   // (chunked: W's copies are built here, after its first block)
       rc = first_chunked ? sync_copies(s, W, ldw, d, 0, d, cw, st)
                          : sync_copies(s, W, ldw, d, b0, bb, cw, st);
@@ -1431,8 +1596,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                         pws, pbytes, st, tc_gemm, nullptr, users);
     if (rc) return rc;
     if (host) {
-      rc = stage_copy(s, st, host->H_out + b0, size_t(host->ldh) * 4, H + b0, size_t(ldh) * 4,
-                      size_t(bb) * 4, size_t(items->n_rows), cudaMemcpyDeviceToHost);
+      rc = host_cols_out(s, st, host, host->H_out, host->ldh, H, ldh, items->n_rows, d, b0, bb,
+                         host->sH);
       if (rc) return rc;
     }
     if (tc_gemm) {
@@ -1443,8 +1608,9 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   }
   if (host) {   // the maintained cache, then the caller's stream waits for every copy
     if (host->cache_out) {
-      const size_t cb = size_t(users->nnz) * 4;
-      rc = stage_copy(s, st, host->cache_out, cb, cache, cb, cb, 1, cudaMemcpyDeviceToHost);
+      // one "row" of nnz entries (nnz < 2^31)
+      rc = host_cols_out(s, st, host, host->cache_out, users->nnz, cache, (int)users->nnz, 1,
+                         (int)users->nnz, 0, (int)users->nnz, host->sC);
       if (rc) return rc;
     }
     CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));

@@ -58,3 +58,29 @@ IALS_DEVI void report_singular(unsigned long long* err, int side, int row, int p
 }
 
 }  // namespace ials
+
+namespace ials {
+// Host f64 <-> device fp32 staging of ials_epoch_host64 (the reference's
+// float64 model in place): 2-D strided casts, grid-stride over rows x cols.
+// f64 -> fp32 rounds to nearest (what torch / NumPy .astype(float32) do).
+__global__ void __launch_bounds__(256) k_f64_to_f32_2d(const double* __restrict__ src, int64_t lds,
+                                                        float* __restrict__ dst, int64_t ldd,
+                                                        int cols, int64_t rows) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    dst[r * ldd + c] = __double2float_rn(src[r * lds + c]);
+  }
+}
+__global__ void __launch_bounds__(256) k_f32_to_f64_2d(const float* __restrict__ src, int64_t lds,
+                                                        double* __restrict__ dst, int64_t ldd,
+                                                        int cols, int64_t rows) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    dst[r * ldd + c] = (double)src[r * lds + c];
+  }
+}
+}  // namespace ials

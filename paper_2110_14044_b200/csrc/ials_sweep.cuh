@@ -83,6 +83,7 @@ struct SweepParams {
   int* queue;              // if set, k_sweep_light takes its rows from this zeroed counter
   float* drow;             // [n_rows][b] per-row d of the fused sweep (k_pass_cache)
   int fb0;                 // column of the block in `fixed` (b0, or 0 for a compact copy)
+  int fixed_cols;          // columns of `fixed` (d, or the compact copy's width)
   const int* x_rows;       // the other side's view of the same entries (rows = fixed-side ids,
   const int* x_cols;       //   cols = this side's ids, x_pos = cache positions or NULL): the
   const int* x_pos;        //   cache pass may walk it instead (k_pass_cache_flat<., ., true>)

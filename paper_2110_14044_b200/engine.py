@@ -370,6 +370,20 @@ class Engine:
                 self.lib.ials_epoch_events(None, 0)
         self.sess.check(rc, "epoch")
 
+    def epoch_passes(self, W, H, cache, b, alpha0, pass0, npass, recompute_cache=False):
+        """Passes [pass0, pass0 + npass) of ``epoch`` (pass 2k = user pass of
+        block k, 2k + 1 = its item pass), through the same C code path."""
+        d = W.shape[1]
+        ws = self.workspace(d, b)
+        su, si = self.p.users.schedule(b), self.p.items.schedule(b)
+        rc = self.lib.ials_epoch_range(self.sess.handle, ctypes.byref(self.p.users.struct),
+                                       ctypes.byref(su.struct), ctypes.byref(self.p.items.struct),
+                                       ctypes.byref(si.struct), _ptr(W), W.stride(0), _ptr(H),
+                                       H.stride(0), d, b, float(alpha0), _ptr(cache), _ptr(ws),
+                                       ws.numel(), self.stream(), int(pass0), int(npass),
+                                       int(bool(recompute_cache)))
+        self.sess.check(rc, "epoch_range")
+
     def epoch_host(self, W_host, H_host, W, H, cache, b, alpha0, W_out=None, H_out=None,
                    cache_out=None):
         """One epoch for a model in (pinned) host tensors: ials_epoch_host
@@ -388,6 +402,36 @@ class Engine:
                                       float(alpha0), _ptr(cache), _ptr(cache_out), _ptr(ws),
                                       ws.numel(), self.stream())
         self.sess.check(rc, "epoch_host")
+
+    def epoch_host64(self, W_host, H_host, W, H, cache, b, alpha0, staging, cache_out=None,
+                     events=None):
+        """One epoch for the reference's float64 model in host memory (NumPy
+        arrays, C-contiguous): ials_epoch_host64 copies W / H in through device
+        f64 staging, runs the epoch, and writes W / H (and the maintained
+        cache, if ``cache_out`` is given) back in place, the copies and casts
+        overlapped with the epoch on a second stream.  Stream-ordered: the
+        host arrays are final once the current stream has synchronised."""
+        d = W.shape[1]
+        ws = self.workspace(d, b)
+        su, si = self.p.users.schedule(b), self.p.items.schedule(b)
+        hp = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
+        if events:
+            for e in events:
+                if not e.cuda_event:
+                    e.record(torch.cuda.current_stream(self.device))
+            arr = (c_void_p * len(events))(*[c_void_p(e.cuda_event) for e in events])
+            self.sess.check(self.lib.ials_epoch_events(arr, len(events)), "epoch events")
+        try:
+            rc = self.lib.ials_epoch_host64(
+                self.sess.handle, ctypes.byref(self.p.users.struct), ctypes.byref(su.struct),
+                ctypes.byref(self.p.items.struct), ctypes.byref(si.struct), hp(W_host), hp(W_host),
+                W_host.strides[0] // 8, hp(H_host), hp(H_host), H_host.strides[0] // 8, _ptr(W),
+                W.stride(0), _ptr(H), H.stride(0), d, b, float(alpha0), _ptr(cache), hp(cache_out),
+                _ptr(staging), staging.numel(), _ptr(ws), ws.numel(), self.stream())
+        finally:
+            if events:
+                self.lib.ials_epoch_events(None, 0)
+        self.sess.check(rc, "epoch_host64")
 
     def epoch_graph(self, W, H, cache, b, alpha0):
         """The same epoch captured once as a CUDA graph and replayed (one

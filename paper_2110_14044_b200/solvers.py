@@ -247,12 +247,100 @@ def block_update(model: FactorModel, data, cache: PredictionCache, config: Solve
     tr.write_back(cache)
 
 
+class _HostEpochRunner:
+    """Device buffers for the float64 drop-in epoch of one dataset at one
+    width on one device (cached across calls): fp32 W / H / cache, the f64
+    staging of ials_epoch_host64, the row schedules and the workspace of the
+    dataset's engine."""
+
+    def __init__(self, data, dim, device):
+        import torch
+
+        from ._runtime import default_engine_session
+
+        self.rt = default_engine_session(device)
+        self.eng = self.rt.engine_for(data)
+        dev = self.rt.device
+        U, I, S = data.num_users, data.num_items, data.n_interactions
+        self.W = torch.empty((U, dim), dtype=torch.float32, device=dev)
+        self.H = torch.empty((I, dim), dtype=torch.float32, device=dev)
+        self.cache = torch.empty(max(S, 1), dtype=torch.float32, device=dev)[:S]
+        nbytes = int(self.eng.lib.ials_host64_staging_bytes(U, I, dim, S))
+        self.staging = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+
+    def epoch(self, model, cache, config, b, index):
+        import torch
+
+        from ._runtime import pin_host_array
+
+        e = self.eng
+        e.p.set_regularizer(config.unobserved_weight, config.reg, config.reg_exponent)
+        for a in (model.user_factors, model.item_factors, cache.scores):
+            pin_host_array(a)
+        nb = -(-model.dim // b)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 + 4 * nb)]
+        self.rt.session.reset_singular()
+        e.epoch_host64(model.user_factors, model.item_factors, self.W, self.H, self.cache, b,
+                       config.unobserved_weight, self.staging, cache_out=cache.scores, events=ev)
+        torch.cuda.current_stream(self.rt.device).synchronize()
+        rep = EpochReport(index)
+        names = ["cache"] + [n for _ in range(nb) for n in ("gramian", "user", "gramian", "item")]
+        prev = ev[0]
+        for name, m in zip(names, ev[1:]):
+            setattr(rep, f"{name}_seconds", getattr(rep, f"{name}_seconds") + prev.elapsed_time(m) / 1e3)
+            prev = m
+        return rep
+
+
+_RUNNERS = None
+
+
+def _host_runner(data, dim, device):
+    global _RUNNERS
+    import weakref
+
+    import torch
+    if _RUNNERS is None:
+        _RUNNERS = weakref.WeakKeyDictionary()
+    idx = torch.cuda.current_device() if device is None else (torch.device(device).index or 0)
+    try:
+        per = _RUNNERS.setdefault(data, {})
+    except TypeError:
+        per = {}
+    run = per.get((dim, idx))
+    if run is None:
+        run = per[(dim, idx)] = _HostEpochRunner(data, dim, device)
+    return run
+
+
+def _f64_c(a) -> bool:
+    return isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and \
+        a.flags.writeable
+
+
 def ialspp_epoch(model: FactorModel, data, cache: PredictionCache, config: SolverConfig,
                  partition: BlockPartition | None = None, epoch_index: int = 0,
                  device=None) -> EpochReport:
-    """Block epoch: recompute the cache, then per block a user and an item pass."""
-    if partition is not None and partition.dim != model.dim:
+    """Block epoch: recompute the cache, then per block a user and an item pass.
+
+    The caller's float64 model and cache are updated in place.  With the
+    default contiguous partition (or ``partition_dims``' own blocks) the epoch
+    is one ``ials_epoch_host64`` call: the f64 arrays are page-locked in place
+    once and copied through device staging with the casts on the GPU,
+    overlapped with the epoch, and the device buffers are kept across calls
+    for the same dataset.  Other partitions permute columns on the host."""
+    part = partition if partition is not None else partition_dims(model.dim, config.block_size)
+    if part.dim != model.dim:
         raise ValueError("partition does not match the model dimension")
+    from .model import _check_pair
+    _check_pair(model, data)                 # compute_predictions' checks (model.py:153-165)
+    if cache.scores.shape != (data.n_interactions,):
+        raise ValueError("cache length does not match the dataset")
+    perm, spans, identity = _layout(part)
+    if (identity and _uniform_spans(spans, model.dim) and data.n_interactions > 0
+            and all(_f64_c(a) for a in (model.user_factors, model.item_factors, cache.scores))):
+        return _host_runner(data, model.dim, device).epoch(model, cache, config, spans[0][1],
+                                                           epoch_index)
     tr = DeviceTrainer(model, data, config, partition, device, cache)
     rep = tr.epoch(epoch_index)
     tr.write_back(cache)

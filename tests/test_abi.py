@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "ials_b200.h")
 def declared_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(ials_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(ials_[a-z0-9_]+)\s*\(", text)))
 
 
 @pytest.fixture(scope="module")
@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol(lib):
     from paper_2110_14044_b200 import _lib
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
-    exported = set(re.findall(r"\bT (ials_[a-z_]+)\b", out))
+    exported = set(re.findall(r"\bT (ials_[a-z0-9_]+)\b", out))
     missing = set(declared_functions()) - exported
     assert not missing, missing
     for name in declared_functions():

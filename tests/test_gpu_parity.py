@@ -378,3 +378,41 @@ def test_wider_last_block_matches_oracle(ials):
                      [np.arange(0, 10), np.arange(10, 30)])
     for got, want in ((model.user_factors, w), (model.item_factors, h)):
         assert relf(got, want) < TOL and relmax(got, want) < TOL
+
+
+@pytest.mark.parametrize("d,b", [(16, 8), (128, 128), (96, 48)])
+def test_dropin_host64_bit_identical_to_device_epoch(ials, d, b):
+    """ialspp_epoch on the caller's float64 NumPy model (ials_epoch_host64:
+    f64 copies + casts on the GPU, overlapped with the epoch) equals the
+    device-resident ials_epoch on fp32 copies of the same model, bit for bit,
+    over two consecutive calls; the maintained cache comes back too."""
+    from paper_2110_14044_b200.solvers import DeviceTrainer
+    rng = np.random.default_rng(5)
+    U, I, nnz = 700, 260, 14000
+    users = rng.integers(0, U, nnz)
+    items = np.minimum(rng.zipf(1.3, nnz) - 1, I - 1)
+    data = ials.InteractionDataset(U, I, users, items)
+    cfg = ials.SolverConfig(dim=d, block_size=b, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=1, seed=2)
+    m1 = ials.init_model(cfg, U, I)          # float64, not pre-rounded: the cast runs on the GPU
+    m2 = m1.copy()
+    c1 = ials.PredictionCache.zeros(nnz)
+    for e in range(2):
+        ials.ialspp_epoch(m1, data, c1, cfg, epoch_index=e)
+        tr = DeviceTrainer(m2, data, cfg)
+        tr.epoch(e, timed=False)
+        c2 = ials.PredictionCache.zeros(nnz)
+        tr.write_back(c2)
+        assert np.array_equal(m1.user_factors, m2.user_factors)
+        assert np.array_equal(m1.item_factors, m2.item_factors)
+        assert np.array_equal(c1.scores, c2.scores)
+    # a Fortran-ordered model takes the host-permuting path: same numbers
+    m3 = ials.init_model(cfg, U, I)
+    m3.user_factors = np.asfortranarray(m3.user_factors)     # (set after __post_init__)
+    m3.item_factors = np.asfortranarray(m3.item_factors)
+    m4 = ials.init_model(cfg, U, I)
+    c3, c4 = ials.PredictionCache.zeros(nnz), ials.PredictionCache.zeros(nnz)
+    ials.ialspp_epoch(m3, data, c3, cfg)
+    ials.ialspp_epoch(m4, data, c4, cfg)
+    assert np.array_equal(m3.user_factors, m4.user_factors)
+    assert np.array_equal(c3.scores, c4.scores)
