@@ -324,6 +324,20 @@ int ials_topk(ials_session* s, int32_t n_rows, int32_t n_cols, float* scores, in
               const int32_t* ex_ptr, const int32_t* ex_cols, int32_t k, int32_t* out,
               int32_t* counts, void* stream);
 
+/* ials_topk on float64 score rows (top_k_from_scores on the caller's f64
+ * scores, metrics.py:31-57): the same order -- score descending, ties by
+ * ascending index -- over 64-bit order-preserving keys, so no precision is
+ * lost before ranking. */
+int ials_topk64(ials_session* s, int32_t n_rows, int32_t n_cols, double* scores, int64_t lds,
+                const int32_t* ex_ptr, const int32_t* ex_cols, int32_t k, int32_t* out,
+                int32_t* counts, void* stream);
+
+/* out[u][i] = <E[u], H[i]> (n_users x n_items, ld ldo) on the tensor core
+ * (3xTF32, FP32-accurate; rank_items / evaluate_holdout / recommend,
+ * metrics.py:57-119).  E, H 16-byte aligned with lde, ldh multiples of 4. */
+int ials_scores(ials_session* s, const float* E, int32_t lde, int32_t n_users, const float* H,
+                int32_t ldh, int32_t n_items, int32_t d, float* out, int32_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

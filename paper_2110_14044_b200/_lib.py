@@ -75,6 +75,8 @@ SIGNATURES = {
     "ials_epoch": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
                            ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched), c_p, c_i32, c_p,
                            c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p]),
+    "ials_topk64": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
+    "ials_scores": (c_i32, [c_p, c_p, c_i32, c_i32, c_p, c_i32, c_i32, c_i32, c_p, c_i32, c_p]),
     "ials_host_register": (c_i32, [c_p, c_sz]),
     "ials_host_unregister": (c_i32, [c_p]),
     "ials_host64_staging_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64]),

@@ -1729,6 +1729,54 @@ int ials_topk(ials_session* s, int32_t n_rows, int32_t n_cols, float* scores, in
   return IALS_OK;
 }
 
+int ials_topk64(ials_session* s, int32_t n_rows, int32_t n_cols, double* scores, int64_t lds,
+                const int32_t* ex_ptr, const int32_t* ex_cols, int32_t k, int32_t* out,
+                int32_t* counts, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (n_rows < 0 || n_cols < 0 || lds < n_cols || k < 1 || k > kTopkMax)
+    return fail(s, IALS_E_INVALID, "topk64: bad sizes (rows=%d cols=%d k=%d, k <= %d)", n_rows,
+                n_cols, k, kTopkMax);
+  if (n_rows == 0) return IALS_OK;
+  if (!scores || !out || !counts) return fail(s, IALS_E_INVALID, "topk64: NULL argument");
+  cudaStream_t st = S(stream);
+  if (ex_ptr && ex_cols) {
+    k_topk_exclude64<<<n_rows, 256, 0, st>>>(scores, lds, ex_ptr, ex_cols);
+    LAUNCH_CHECK(s);
+  }
+  k_topk64<<<n_rows, kTopkThreads, 0, st>>>(scores, lds, n_cols, k, out, counts);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+// scores = E @ H^T (n_users x n_items) on the tensor core: the 3xTF32 TMA
+// GEMM with blockIdx.y over 128-item tiles (FP32-accurate scores for
+// rank_items / evaluate_holdout / ImplicitALS.recommend, metrics.py:57-119)
+int ials_scores(ials_session* s, const float* E, int32_t lde, int32_t n_users, const float* H,
+                int32_t ldh, int32_t n_items, int32_t d, float* out, int32_t ldo, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (n_users < 0 || n_items < 0 || d < 1 || lde < d || ldh < d || ldo < n_items)
+    return fail(s, IALS_E_INVALID, "scores: bad shape (users=%d items=%d d=%d)", n_users, n_items, d);
+  if (n_users == 0 || n_items == 0) return IALS_OK;
+  if (!E || !H || !out || lde % 4 || ldh % 4 || reinterpret_cast<uintptr_t>(E) % 16 ||
+      reinterpret_cast<uintptr_t>(H) % 16)
+    return fail(s, IALS_E_INVALID, "scores: E / H must be 16-byte aligned with ld %% 4 == 0");
+  int rc = gemm_attrs(s);
+  if (!rc) rc = get_encode(s);
+  if (rc) return rc;
+  CUtensorMap am, bm;
+  rc = make_map(s, &am, E, d, n_users, lde, 128);
+  if (!rc) rc = make_map(s, &bm, H, d, n_items, ldh, 128);
+  if (rc) return rc;
+  const int nt = (n_items + 127) / 128;
+  GemmJob job{n_users, 0, 0, n_items, 128, d, rup(d, kGemmKC), out, ldo, 0, 1.f};
+  job.n_tiles = nt;
+  k_gemm3_tf32<<<dim3((n_users + 127) / 128, nt), kGemmThreads, GemmLay::BYTES, S(stream)>>>(am, bm, bm, job);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
 // ------------------------------------------------------------------ loss
 size_t ials_loss_workspace_bytes(int32_t d) {
   return 2 * al256(size_t(d) * d * 4) + gram_ws(0, d, d) +

@@ -38,6 +38,8 @@ struct GemmJob {
   long long split_stride;  // floats between splits
   float scale;
   int b_lo_tma = 0;        // B's lo part is precomputed in memory (b_lo map): TMA-load it
+  int n_tiles = 0;         // > 0: blockIdx.y walks N tiles of 128 output columns (B rows
+                           // b_row0 + 128 y, out columns 128 y..), no K split (score GEMM)
 };
 
 constexpr int kGemmStages = 3;
@@ -68,7 +70,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* done = empty + kGemmStages;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(done + 1);
   const int m0 = blockIdx.x * 128;
-  const int kb = blockIdx.y * job.k_span;
+  const int ny = job.n_tiles ? (int)blockIdx.y : 0;   // N tile
+  const int ks = job.n_tiles ? 0 : (int)blockIdx.y;   // K split
+  const int b_row = job.b_row0 + 128 * ny;
+  const int n_here = job.n_tiles ? min(128, job.n - 128 * ny) : job.n;
+  const int kb = ks * job.k_span;
   const int ke = min(kb + job.k_span, job.k_total);
   const int nk = (ke - kb + kGemmKC - 1) / kGemmKC;
   if (tid == 0) {
@@ -96,9 +102,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_expect_tx(full + s, stage_bytes);
       const int kc = kb + c * kGemmKC;
       tma_load_2d(smem_u32(st), &a_hi, kc, job.a_row0 + m0, full + s);
-      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, kc, job.b_row0, full + s);
+      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, kc, b_row, full + s);
       if (job.b_lo_tma)
-        tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, kc, job.b_row0, full + s);
+        tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, kc, b_row, full + s);
     }
   } else if (warp == 1 && (tid & 31) == 0) {  // MMA issuer
     const uint32_t idesc = make_idesc_tf32(128, job.bn, 0, 0, 0);
@@ -149,14 +155,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   mbar_wait(done, 0);
   tc_fence_after();
   const int row = m0 + (warp & 3) * 32 + (tid & 31);
-  float* o = job.out + (long long)blockIdx.y * job.split_stride + (long long)row * job.ldo;
+  float* o = job.out + (long long)ks * job.split_stride + (long long)row * job.ldo + 128 * ny;
   const uint32_t raddr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   for (int c32 = (warp >> 2) * 32; c32 < job.bn; c32 += 64) {   // warp-uniform
     float v[32];
     tmem_ld32(raddr + c32, v);
     tmem_wait_ld();
     if (row < job.m_rows && nk > 0) {
-      if (c32 + 32 <= job.n && (job.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(job.out) & 15) == 0) {
+      if (c32 + 32 <= n_here && (job.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(job.out) & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4)   // 16-byte stores: 8 per thread instead of 32
           *reinterpret_cast<float4*>(o + c32 + j) =
@@ -164,12 +170,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-          if (c32 + j < job.n) o[c32 + j] = job.scale * v[j];
+          if (c32 + j < n_here) o[c32 + j] = job.scale * v[j];
       }
     } else if (row < job.m_rows) {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (c32 + j < job.n) o[c32 + j] = 0.f;
+        if (c32 + j < n_here) o[c32 + j] = 0.f;
     }
   }
   tc_fence_before();

@@ -61,12 +61,16 @@ struct PkLay {
   static constexpr int OFF_ID = OFF_YF + 512;
   static constexpr int OFF_D = OFF_ID + 512;
   static constexpr int OFF_DIAG = OFF_D + 512;
-  static constexpr int OFF_TILE = OFF_DIAG + 512;              // rows[G], beg[G], end[G], lam[G]
-  static constexpr int OFF_FLAG = OFF_TILE + 64;               // flags[G], next task
+  static constexpr int OFF_TILE = OFF_DIAG + 512;              // [2][rows[4], beg[4], end[4], lam[4]]
+  static constexpr int OFF_FLAG = OFF_TILE + 128;              // flags[G], next task
+  // G = 4: the 32 x 32 packed template alpha0 * slab[pi, pi] in shared memory
+  // (loaded once per launch; G = 2's 8.7 KB one is read through L1)
+  static constexpr int TPL_FLOATS = G == 4 ? 576 : 0;
   static constexpr int OFF_BAR = OFF_FLAG + 32;                // MMA bars [NXT], gather bars [NB], TMEM base
   static constexpr int BAR_GATHER = NXT;
   static constexpr int OFF_TPTR = OFF_BAR + 8 * (NXT + NB);
-  static constexpr int BYTES = OFF_TPTR + 16 + 1024;
+  static constexpr int OFF_TPL = OFF_TPTR + 16;
+  static constexpr int BYTES = OFF_TPL + TPL_FLOATS * 4 + 1024;
 };
 
 struct PkState {
@@ -114,20 +118,19 @@ IALS_DEVI void pk_gather(const SweepParams& p, char* smem, const PkState& st, co
   const int* mp = reinterpret_cast<const int*>(smem + L::OFF_MP) + (c & (L::MR - 1)) * L::EPC;
   float* X = reinterpret_cast<float*>(smem + L::OFF_X) + (c % L::NB) * G * L::KC * L::SW;
   if (st.fmap) {
-    if (tid == 32) {
-      uint32_t bytes = 0;
-#pragma unroll
-      for (int g = 0; g < G; ++g) bytes += (uint32_t)((pk_nk<G>(beg, end, g, c) + 3) >> 2) * 4 * L::SW * 4;
+    // each slot's gathers are issued by lane 0 of the first warp of the slot
+    // (G issuers in parallel); the barrier expects G arrivals, each with its
+    // slot's bytes (possibly 0), so it cannot complete before every slot's
+    // gathers are registered
+    if ((tid & 31) == 0 && (tid % L::NG) == 0) {
+      const int g = tid / L::NG;
+      const int nk = pk_nk<G>(beg, end, g, c), last = nk - 1;
       uint64_t* gb = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR) + L::BAR_GATHER + (c % L::NB);
-      mbar_expect_tx(gb, bytes);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int nk = pk_nk<G>(beg, end, g, c), last = nk - 1;
-        const int* m = mc + g * L::KC;
-        for (int k = 0; k < nk; k += 4)
-          tma_gather4(smem_u32(X + (g * L::KC + k) * L::SW), st.fmap, p.fb0, m[min(k, last)],
-                      m[min(k + 1, last)], m[min(k + 2, last)], m[min(k + 3, last)], gb);
-      }
+      mbar_expect_tx(gb, (uint32_t)((nk + 3) >> 2) * 4 * L::SW * 4);
+      const int* m = mc + g * L::KC;
+      for (int k = 0; k < nk; k += 4)
+        tma_gather4(smem_u32(X + (g * L::KC + k) * L::SW), st.fmap, p.fb0, m[min(k, last)],
+                    m[min(k + 1, last)], m[min(k + 2, last)], m[min(k + 3, last)], gb);
     }
   } else if (p.vec) {   // 16-byte pieces: thread <-> (entry, piece)
     constexpr int PV = L::SW / 4;
@@ -523,18 +526,18 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
   }
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_TPTR);
-  int* trow = reinterpret_cast<int*>(smem + L::OFF_TILE);
-  int* tbeg = trow + 4;
-  int* tend = trow + 8;
-  float* tlam = reinterpret_cast<float*>(trow + 12);
+  int* tinfo = reinterpret_cast<int*>(smem + L::OFF_TILE);   // [2][16]: rows, beg, end, lam
   int* FLAG = reinterpret_cast<int*>(smem + L::OFF_FLAG);
   float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
   float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
   ds[tid] = 0.f;
   if (tid == 0) {
-    for (int k = 0; k < L::NXT + L::NB; ++k) mbar_init(bar + k, 1);
+    for (int k = 0; k < L::NXT; ++k) mbar_init(bar + k, 1);
+    for (int k = 0; k < L::NB; ++k) mbar_init(bar + L::BAR_GATHER + k, G);
     if (use_tma) prefetch_tmap(&fmap);
   }
+  float* tpl_s = reinterpret_cast<float*>(smem + L::OFF_TPL);
+  for (int k = tid; k < L::TPL_FLOATS; k += L::NT) tpl_s[k] = __ldg(p.tpl + k);
   if (tid < 32) tmem_alloc(tptr, 128);
   tc_fence_before();
   __syncthreads();
@@ -557,25 +560,35 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
   const int n_tiles = (n_light + G - 1) / G;
   int* queue = p.redo_cnt + 2;
   int* next = FLAG + 4;
+  // tile t's rows (G consecutive rows of the longest-first list), their entry
+  // ranges and lam into tile buffer tb (an empty slot solves I x = 0)
+  auto tile_row = [&](int t, int s) { const int k = t * G + s; return k < n_light ? lrows[k] : -1; };
+  auto put_tile = [&](int tb, int s, int r) {
+    int* ti = tinfo + 16 * tb;
+    ti[s] = r;
+    ti[4 + s] = r >= 0 ? p.side.ptr[r] : 0;
+    ti[8 + s] = r >= 0 ? p.side.ptr[r + 1] : 0;
+    reinterpret_cast<float*>(ti)[12 + s] = r >= 0 ? p.side.lam[r] : 1.f;
+  };
   if (tid == 0) *next = atomicAdd(queue, 1);
   __syncthreads();
   int task = *next;
+  if (tid < G && task < n_tiles) put_tile(0, tid, tile_row(task, tid));
+  if (tid < G) FLAG[tid] = 0;
+  __syncthreads();
+  int tb = 0;
   while (task < n_tiles) {
-    int nxt = 0;
-    if (tid == 0) nxt = atomicAdd(queue, 1);
-    if (tid < G) {   // the tile's rows (consecutive in the longest-first list)
-      const int k = task * G + tid;
-      const int row = k < n_light ? lrows[k] : -1;
-      trow[tid] = row;
-      tbeg[tid] = row >= 0 ? p.side.ptr[row] : 0;
-      tend[tid] = row >= 0 ? p.side.ptr[row + 1] : 0;
-      tlam[tid] = row >= 0 ? p.side.lam[row] : 1.f;   // an empty slot solves I x = 0
-      FLAG[tid] = 0;
-    }
-    __syncthreads();
+    if (tid == 0) *next = atomicAdd(queue, 1);   // read by all after the accumulate's barriers
+    const int* trow = tinfo + 16 * tb;
+    const int* tbeg = trow + 4;
+    const int* tend = trow + 8;
+    const float* tlam = reinterpret_cast<const float*>(trow + 12);
     const int row = trow[g];
+    // this row's projection and own block value: loaded now, used after the accumulate
+    const float pj = (row >= 0 && m < b) ? __ldg(p.proj + (size_t)row * b + m) : 0.f;
+    const float ow = (row >= 0 && m < b) ? p.own[(size_t)row * p.ldo + p.b0 + m] : 0.f;
     {  // step 1: TMEM row := template row m in this slot's columns, zeros elsewhere
-      const float* tp = p.tpl + pk_off(m);
+      const float* tp = (L::TPL_FLOATS ? tpl_s : p.tpl) + pk_off(m);
 #pragma unroll 1
       for (int c8 = 0; c8 < 16; ++c8) {
         const int col = 8 * c8;   // warp-uniform
@@ -584,7 +597,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int c = col - g * L::NG + j;
-          w8[j] = (mine && c <= m) ? __ldg(tp + c) : 0.f;
+          w8[j] = (mine && c <= m) ? tp[c] : 0.f;
         }
         tmem_st8(row_addr + col, w8);
       }
@@ -596,6 +609,9 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
     for (int s = 0; s < G; ++s) nch = max(nch, (tend[s] - tbeg[s] + L::KC - 1) / L::KC);
     double gacc = 0.0;
     pk_accumulate<G, UNIT>(p, smem, st, gacc, tbeg, tend, nch, tid);
+    const int task_next = *next;   // published by the accumulate's barriers
+    int nrow = -1;                 // the next tile's row of slot tid: its loads overlap the factorisation
+    if (tid < G && task_next < n_tiles) nrow = tile_row(task_next, tid);
     const float lam = tlam[g];
     {  // lam on the diagonal (global column tid); the diagonal before factoring
       const int lane = tid & 31, e = lane & 7;
@@ -621,13 +637,12 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
     }
     {
       float gv = 0.f;
-      if (row >= 0 && m < b)
-        gv = (float)(gacc + (double)p.proj[(size_t)row * b + m] +
-                     (double)lam * (double)p.own[(size_t)row * p.ldo + p.b0 + m]);
+      if (row >= 0 && m < b) gv = (float)(gacc + (double)pj + (double)lam * (double)ow);
       ys[tid] = gv;
     }
     __syncthreads();
     pk_factor<G>(p, smem, st, row_addr, tid);
+    if (tid < G && task_next < n_tiles) put_tile(tb ^ 1, tid, nrow);
     pk_block_inverses<G>(p, smem, tid);
     __syncthreads();
     pk_backward<G>(p, smem, tid);
@@ -636,7 +651,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
       if (bad) {
         p.drow[(size_t)row * b + m] = 0.f;
       } else {
-        p.own[(size_t)row * p.ldo + p.b0 + m] -= ds[tid];
+        p.own[(size_t)row * p.ldo + p.b0 + m] = ow - ds[tid];
         p.drow[(size_t)row * b + m] = ds[tid];
       }
     }
@@ -645,12 +660,11 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
       atomicAdd(p.redo_total, 1ull);
     }
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();   // this tile's state (FLAG, tile buffer tb) is no longer read
     tc_fence_after();
-    if (tid == 0) *next = nxt;
-    __syncthreads();
-    task = *next;
-    __syncthreads();
+    if (tid < G) FLAG[tid] = 0;
+    task = task_next;
+    tb ^= 1;
   }
   tc_fence_before();
   __syncthreads();

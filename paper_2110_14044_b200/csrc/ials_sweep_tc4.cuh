@@ -55,7 +55,8 @@ struct TcLay4 {
   static constexpr int OFF_DIAG = OFF_D + BT * 4;  // H_kk before the factorisation
   static constexpr int OFF_FLAG = OFF_DIAG + BT * 4;
   static constexpr int OFF_BAR = OFF_FLAG + 16;    // MMA mbarriers [2], gather mbarriers [2], TMEM base
-  static constexpr int BYTES = OFF_BAR + 48 + 1024;
+  static constexpr int OFF_RI = OFF_BAR + 48;      // [2][4]: row, entry begin / end, lam (row prefetch)
+  static constexpr int BYTES = OFF_RI + 32 + 1024;
 };
 
 // K-major, 64B-swizzle float index of operand element (row m, k) of a
@@ -619,9 +620,6 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
   // row runs
   int* queue = p.redo_cnt + 2;
   int* next = reinterpret_cast<int*>(smem + L::OFF_FLAG) + 2;
-  if (tid == 0) *next = atomicAdd(queue, 1);
-  __syncthreads();
-  int task = *next;
   // the first user pass of ials_epoch_host sweeps the light rows chunk by
   // chunk as their rows of W arrive: this launch's slice of the grouped list
   const int* lrows = p.light_rows;
@@ -632,20 +630,41 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
     lrows += off;
     n_light = p.chunk_tot[p.chunk];
   }
+  // row info double buffer: the next row's id, entry range and lam are
+  // fetched by thread 0 while the current row is factored
+  int* RI = reinterpret_cast<int*>(smem + L::OFF_RI);
+  auto put_row = [&](int rb, int r) {
+    RI[4 * rb] = r;
+    RI[4 * rb + 1] = p.side.ptr[r];
+    RI[4 * rb + 2] = p.side.ptr[r + 1];
+    reinterpret_cast<float*>(RI)[4 * rb + 3] = p.side.lam[r];
+  };
+  if (tid == 0) {
+    const int t0 = atomicAdd(queue, 1);
+    *next = t0;
+    if (t0 < n_light) put_row(0, lrows[t0]);
+  }
+  __syncthreads();
+  int task = *next;
+  int rb = 0;
   while (task < n_light) {
     int nxt = 0;
-    if (tid == 0) nxt = atomicAdd(queue, 1);   // consumed at the end of the row
+    if (tid == 0) nxt = atomicAdd(queue, 1);   // consumed after the accumulate
     const bool rec = ndone == rec_row && tid == 0;
     if (rec) tph[0] = clock64();
-    const int row = lrows[task];
-    const int ebeg = p.side.ptr[row], eend = p.side.ptr[row + 1];
-    const float lam = p.side.lam[row];
+    const int row = RI[4 * rb];
+    const int ebeg = RI[4 * rb + 1], eend = RI[4 * rb + 2];
+    const float lam = reinterpret_cast<const float*>(RI)[4 * rb + 3];
+    // the projection and own value of this thread's column, used after the accumulate
+    const float pj = (tid < b) ? __ldg(p.proj + (size_t)row * b + tid) : 0.f;
+    const float ow = (tid < b) ? p.own[(size_t)row * p.ldo + p.b0 + tid] : 0.f;
     tc4_init(p, row_addr, tid);
     if (rec) tph[1] = clock64();
     tmem_wait_st();
     tc_fence_before();   // the first chunk's barrier orders these stores before the MMAs
     double gacc = 0.0;
     const int nch = tc4_accumulate<UNIT>(p, smem, st, gacc, ebeg, eend, tid);
+    const int nrow = (tid == 0 && nxt < n_light) ? lrows[nxt] : -1;   // lands during the factorisation
     if (rec) tph[2] = clock64();
     {  // + lam on the diagonal, and the diagonal itself (the cancellation
        // test's reference): lane l of warp w owns column 32w + l, reached with
@@ -675,14 +694,16 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
     }
     {
       float gv = 0.f;
-      if (tid < b)
-        gv = (float)(gacc + (double)p.proj[(size_t)row * b + tid] +
-                     (double)lam * (double)p.own[(size_t)row * p.ldo + p.b0 + tid]);
+      if (tid < b) gv = (float)(gacc + (double)pj + (double)lam * (double)ow);
       ys[tid] = gv;
     }
     __syncthreads();
     if (rec) tph[3] = clock64();
     tc4_factor(p, smem, st, row_addr, row, tid, ndone == rec_row);
+    if (tid == 0) {
+      if (nrow >= 0) put_row(rb ^ 1, nrow);
+      *next = nxt;
+    }
     if (rec) tph[4] = clock64();
     (void)nch;
     if (*reinterpret_cast<volatile int*>(smem + L::OFF_FLAG)) {
@@ -698,7 +719,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
       tc4_backward(p, smem, tid);
       if (rec) tph[5] = clock64();
       if (tid < b) {
-        p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
+        p.own[(size_t)row * p.ldo + p.b0 + tid] = ow - ds[tid];
         p.drow[(size_t)row * b + tid] = ds[tid];   // for k_pass_cache
       }
     }
@@ -711,10 +732,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
       for (int k = 0; k < 8; ++k) p.dbg[blockIdx.x * 8 + k] = tph[k];
     }
     ++ndone;
-    if (tid == 0) *next = nxt;
-    __syncthreads();
-    task = *next;
-    __syncthreads();   // everyone has read it before the next row's fetch lands
+    task = *next;   // written after the factorisation, published by the barriers since
+    rb ^= 1;
   }
   tc_fence_before();
   __syncthreads();

@@ -159,3 +159,120 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
 }
 
 }  // namespace ials
+
+namespace ials {
+
+// float64 scores (top_k_from_scores on the caller's f64 array, metrics.py:31-57):
+// the same selection over 64-bit order-preserving keys (8 radix passes), the
+// winners sorted by (score descending, index ascending) as (key, index) pairs.
+IALS_DEVI uint64_t rank_key64(double s) {
+  const uint64_t u = (uint64_t)__double_as_longlong(s + 0.0);   // -0 -> +0
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void k_topk_exclude64(double* __restrict__ scores, int64_t lds, const int* __restrict__ ptr,
+                                 const int* __restrict__ cols) {
+  const int r = blockIdx.x;
+  for (int e = ptr[r] + threadIdx.x; e < ptr[r + 1]; e += blockDim.x)
+    scores[(int64_t)r * lds + cols[e]] = -INFINITY;
+}
+
+__global__ void __launch_bounds__(kTopkThreads) k_topk64(const double* __restrict__ scores, int64_t lds,
+                                                         int n, int k, int* __restrict__ out,
+                                                         int* __restrict__ counts) {
+  __shared__ int hist[256];
+  __shared__ int sh[40];
+  __shared__ uint64_t bkey[kTopkMax];
+  __shared__ int bidx[kTopkMax];
+  __shared__ uint64_t sel[2];
+  const int tid = threadIdx.x, r = blockIdx.x;
+  const double* s = scores + (int64_t)r * lds;
+  int cnt = 0;
+  for (int i = tid; i < n; i += kTopkThreads) cnt += isfinite(s[i]) ? 1 : 0;
+  int pool;
+  block_scan_excl(cnt, sh, &pool);
+  const int K = min(k, pool);
+  if (K == 0) {
+    for (int j = tid; j < k; j += kTopkThreads) out[(int64_t)r * k + j] = -1;
+    if (tid == 0) counts[r] = 0;
+    return;
+  }
+  uint64_t prefix = 0, mask = 0;
+  int remaining = K;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kTopkThreads) {
+      const double v = s[i];
+      if (!isfinite(v)) continue;
+      const uint64_t key = rank_key64(v);
+      if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 255)], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int c = 0, dgt = 255;
+      for (; dgt > 0; --dgt) {
+        if (c + hist[dgt] >= remaining) break;
+        c += hist[dgt];
+      }
+      sel[0] = (uint64_t)dgt;
+      sel[1] = (uint64_t)(remaining - c);
+    }
+    __syncthreads();
+    prefix |= sel[0] << shift;
+    mask |= 0xFFull << shift;
+    remaining = (int)sel[1];
+    __syncthreads();
+  }
+  const uint64_t T = prefix;
+  const int need = remaining, G = K - need;
+  int gt_run = 0, eq_run = 0;
+  for (int base = 0; base < n; base += kTopkThreads) {
+    const int i = base + tid;
+    uint64_t key = 0;
+    bool gt = false, eq = false;
+    if (i < n) {
+      const double v = s[i];
+      if (isfinite(v)) {
+        key = rank_key64(v);
+        gt = key > T;
+        eq = key == T;
+      }
+    }
+    int tg, te;
+    const int pg = block_scan_excl(gt ? 1 : 0, sh, &tg);
+    const int pe = block_scan_excl(eq ? 1 : 0, sh, &te);
+    if (gt) { bkey[gt_run + pg] = key; bidx[gt_run + pg] = i; }
+    if (eq && eq_run + pe < need) { bkey[G + eq_run + pe] = key; bidx[G + eq_run + pe] = i; }
+    gt_run += tg;
+    eq_run += te;
+  }
+  int P = 1;
+  while (P < K) P <<= 1;
+  for (int j = K + tid; j < P; j += kTopkThreads) { bkey[j] = 0ull; bidx[j] = 0x7FFFFFFF; }
+  __syncthreads();
+  // (key desc, index asc): x before y when x.key > y.key or (equal and x.idx < y.idx)
+  for (int len = 2; len <= P; len <<= 1) {
+    for (int st = len >> 1; st > 0; st >>= 1) {
+      for (int a = tid; a < P; a += kTopkThreads) {
+        const int b = a ^ st;
+        if (b > a) {
+          const bool desc = (a & len) == 0;
+          const uint64_t ka = bkey[a], kb = bkey[b];
+          const int ia = bidx[a], ib = bidx[b];
+          const bool a_first = ka > kb || (ka == kb && ia < ib);
+          if (a_first != desc) {
+            bkey[a] = kb; bkey[b] = ka;
+            bidx[a] = ib; bidx[b] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = tid; j < k; j += kTopkThreads) out[(int64_t)r * k + j] = (j < K) ? bidx[j] : -1;
+  if (tid == 0) counts[r] = K;
+}
+
+}  // namespace ials

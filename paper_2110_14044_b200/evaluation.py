@@ -11,9 +11,11 @@ Host mirror of the reference's ``project_user`` / ``fold_in_users``
   from w = 0 is the closed-form solve.  Block widths go up to 256; wider
   models iterate user passes over 128-column blocks (block Gauss-Seidel on
   the same strictly convex quadratic) to a relative change below 1e-6.
-* Scores are a plain FP32 GEMM (cuBLAS through torch.matmul: allowed as a
-  library GEMM); the exclusion of each user's input items and the top-k with
-  the reference's tie order run in ``ials_topk`` (csrc/ials_topk.cuh).
+* Scores are the repo's own 3xTF32 tensor-core GEMM (``ials_scores``: the TMA
+  GEMM of the epoch with 128-item output tiles, FP32-accurate); the exclusion
+  of each user's input items and the top-k with the reference's tie order run
+  in ``ials_topk`` (csrc/ials_topk.cuh).  ``top_k_from_scores`` on the
+  caller's float64 scores ranks the f64 values themselves (``ials_topk64``).
 * recall / NDCG are the reference's set arithmetic on the top-k lists.
 * k above 1024 (the kernel's selection buffer) uses a stable device sort of
   the row instead (torch.sort), with the same order.
@@ -118,16 +120,41 @@ def project_user(item_factors, items, labels=None, weights=None,
     return fold_in_users(item_factors, [(items, labels, weights)], config, device)[0]
 
 
-def _topk_device(scores: torch.Tensor, k: int, ex_ptr=None, ex_cols=None) -> list:
-    """Rows of a device score matrix -> top-k index lists (ials_topk)."""
+def _padded_f32(a, device) -> torch.Tensor:
+    """A 2-d float32 device copy whose row stride is a multiple of 4 floats
+    (the TMA maps of ials_scores), padding columns zero."""
+    a = np.asarray(a, dtype=np.float32)
+    n, d = a.shape
+    ld = (d + 3) & ~3
+    t = torch.zeros((max(n, 1), ld), dtype=torch.float32, device=device)[:n]
+    t[:, :d] = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    return t
+
+
+def device_scores(E: torch.Tensor, H: torch.Tensor, d: int) -> torch.Tensor:
+    """E @ H^T (rows of E x rows of H) with ials_scores; E / H from _padded_f32."""
+    rt = default_engine_session(E.device)
+    n_u, n_i = E.shape[0], H.shape[0]
+    out = torch.empty((max(n_u, 1), max(n_i, 1)), dtype=torch.float32, device=E.device)[:n_u, :n_i]
+    rc = rt.lib.ials_scores(rt.session.handle, _ptr(E), E.stride(0), n_u, _ptr(H), H.stride(0), n_i,
+                            d, _ptr(out), out.stride(0), current_stream_handle(E.device))
+    rt.session.check(rc, "scores")
+    return out
+
+
+def _topk_device(scores: torch.Tensor, k: int, ex_ptr=None, ex_cols=None, as_tensor=False):
+    """Rows of a device score matrix (fp32: ials_topk, f64: ials_topk64) ->
+    top-k index lists, or the (index, count) device tensors."""
     rt = default_engine_session(scores.device)
     n_rows, n_cols = scores.shape
     out = torch.empty((max(n_rows, 1), k), dtype=torch.int32, device=scores.device)
     counts = torch.empty(max(n_rows, 1), dtype=torch.int32, device=scores.device)
-    rc = rt.lib.ials_topk(rt.session.handle, n_rows, n_cols, _ptr(scores), scores.stride(0),
-                          _ptr(ex_ptr), _ptr(ex_cols), k, _ptr(out), _ptr(counts),
-                          current_stream_handle(scores.device))
+    fn = rt.lib.ials_topk64 if scores.dtype == torch.float64 else rt.lib.ials_topk
+    rc = fn(rt.session.handle, n_rows, n_cols, _ptr(scores), scores.stride(0), _ptr(ex_ptr),
+            _ptr(ex_cols), k, _ptr(out), _ptr(counts), current_stream_handle(scores.device))
     rt.session.check(rc, "topk")
+    if as_tensor:
+        return out[:n_rows], counts[:n_rows]
     o, c = out.cpu().numpy(), counts.cpu().numpy()
     return [o[r, :c[r]].astype(np.int64) for r in range(n_rows)]
 
@@ -167,16 +194,19 @@ def top_k_from_scores(scores, k, exclude=None, device=None) -> np.ndarray:
     if k < 1:
         raise ValueError("k must be positive")
     rt = default_engine_session(device)
-    s = torch.from_numpy(np.asarray(scores, dtype=np.float64).astype(np.float32)).to(rt.device)
+    # the caller's float64 scores are ranked as float64 (ials_topk64): no
+    # rounding can merge or reorder near-ties before the selection
+    s = torch.from_numpy(np.ascontiguousarray(scores, dtype=np.float64)).to(rt.device)
     return _top_k_row(s, k, exclude)
 
 
 def rank_items(user_embedding, item_factors, exclude=None, k=10, device=None) -> np.ndarray:
     """Top-k item indices for a user embedding, excluding ``exclude``."""
     rt = default_engine_session(device)
-    h = torch.from_numpy(np.ascontiguousarray(item_factors, dtype=np.float32)).to(rt.device)
-    e = torch.from_numpy(np.asarray(user_embedding, dtype=np.float32)).to(rt.device)
-    return _top_k_row(h @ e, k, exclude)
+    hf = np.asarray(item_factors)
+    H = _padded_f32(hf, rt.device)
+    E = _padded_f32(np.asarray(user_embedding, dtype=np.float64).reshape(1, -1), rt.device)
+    return _top_k_row(device_scores(E, H, hf.shape[1])[0], k, exclude)
 
 
 def recall_at_k(topk, targets, k) -> float:
@@ -219,9 +249,10 @@ def evaluate_holdout(item_factors, split, config, recall_ks=(20, 50), ndcg_ks=(1
                                        for f in evaluated], config, device)
     rt = default_engine_session(device)
     dev = rt.device
-    H = torch.from_numpy(np.ascontiguousarray(item_factors, dtype=np.float32)).to(dev)
+    d = np.asarray(item_factors).shape[1]
+    H = _padded_f32(item_factors, dev)
     n_items = H.shape[0]
-    E = torch.from_numpy(emb.astype(np.float32)).to(dev)
+    E = _padded_f32(emb, dev)
     ex = [np.asarray(f.input_items, dtype=np.int64) for f in evaluated]
     ex_ptr = np.zeros(len(ex) + 1, dtype=np.int64)
     ex_ptr[1:] = np.cumsum([a.size for a in ex])
@@ -234,7 +265,7 @@ def evaluate_holdout(item_factors, split, config, recall_ks=(20, 50), ndcg_ks=(1
     k_run = min(k_max, n_items)
     for r0 in range(0, len(evaluated), users_per_batch):
         r1 = min(len(evaluated), r0 + users_per_batch)
-        scores = (E[r0:r1] @ H.T).contiguous()
+        scores = device_scores(E[r0:r1], H, d)
         ptr = torch.from_numpy((ex_ptr[r0:r1 + 1] - ex_ptr[r0]).astype(np.int32)).to(dev)
         cols = ex_cols[int(ex_ptr[r0]):] if ex_ptr[r1] > ex_ptr[r0] else ex_cols
         tops = _topk_device(scores, k_run, ptr, cols)

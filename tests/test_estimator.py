@@ -7,7 +7,7 @@ import pytest
 import scipy.sparse as sp
 
 import paper_2110_14044_b200 as ials
-from paper_2110_14044_b200.estimator import _as_dataset
+from paper_2110_14044_b200.estimator import _interactions as _as_dataset
 
 from conftest import relf
 

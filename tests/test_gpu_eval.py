@@ -120,3 +120,46 @@ def test_fold_in_with_labels_and_weights(d):
     got = ials.fold_in_users(hf, hist, cfg)
     want = orc.fold_in(hf, hist, 0.1, 1e-3, 1.0)
     assert relf(got, want) < 1e-3
+
+
+def test_top_k_float64_near_ties_exact():
+    """top_k_from_scores ranks the caller's float64 scores as float64: values
+    that differ below fp32 resolution keep the reference's order (metrics.py:31-57)."""
+    from oracle import ialspp_oracle as orc
+    rng = np.random.default_rng(9)
+    for n, k in [(20108, 100), (5000, 1024), (64, 10)]:
+        base = rng.standard_normal(n // 4 + 1)
+        s = np.repeat(base, 4)[:n] + rng.integers(-3, 4, n) * 1e-13   # near-ties within 1 ulp of fp32
+        s[rng.choice(n, 5)] = base[0]                                   # exact ties
+        s[rng.choice(n, 2)] = np.nan
+        ex = rng.choice(n, n // 7, replace=False)
+        want = orc.top_k(s, k, ex)
+        assert np.array_equal(ials.top_k_from_scores(s, k, exclude=ex), want)
+
+
+def test_scores_gemm_and_batched_recommend():
+    """ials_scores (3xTF32 tensor-core GEMM, 128-item tiles) against f64, and
+    ImplicitALS.recommend (one batched device ranking) against per-row
+    rank_items with the same exclusions (the reference's loop, estimator.py:135-152)."""
+    import torch
+    from paper_2110_14044_b200.evaluation import _padded_f32, device_scores
+    rng = np.random.default_rng(4)
+    for nu, ni, d in [(300, 20108, 64), (1, 1000, 30), (129, 257, 128)]:
+        E = rng.standard_normal((nu, d)).astype(np.float32)
+        H = rng.standard_normal((ni, d)).astype(np.float32)
+        got = device_scores(_padded_f32(E, "cuda"), _padded_f32(H, "cuda"), d).double().cpu().numpy()
+        want = E.astype(np.float64) @ H.astype(np.float64).T
+        assert np.abs(got - want).max() <= 2e-6 * np.abs(want).max() * np.sqrt(d)
+    import scipy.sparse as sp
+    X = sp.random(400, 150, density=0.05, random_state=1, format="csr")
+    X.data[:] = 1.0
+    est = ials.ImplicitALS(factors=16, block_size=8, epochs=2).fit(X)
+    Q = sp.random(37, 150, density=0.1, random_state=2, format="csr")
+    Q.data[:] = 1.0
+    items, scores = est.recommend(Q, k=12)
+    emb = est.transform(Q)
+    for r in range(Q.shape[0]):
+        seen = Q[r].indices
+        top = ials.rank_items(emb[r], est.item_factors_, exclude=seen, k=12)
+        assert np.array_equal(items[r, :top.size], top)
+        np.testing.assert_allclose(scores[r, :top.size], est.item_factors_[top] @ emb[r])
