@@ -96,6 +96,11 @@ typedef struct ials_sched {
   const int32_t* tc_wave_slice0; /* HOST [tc_n_waves + 1]                       */
   int32_t tc_max_wave_rows;
   int32_t tc_max_wave_slices;
+  /* light rows (descending degree) with more than 64 / 32 interactions: the
+   * prefix lengths that split the rotated user pass between the b x b sweep
+   * and the Woodbury tiles of 2 and 4 rows */
+  int32_t n_deg_gt64;
+  int32_t n_deg_gt32;
 } ials_sched;
 
 typedef struct ials_session ials_session;
@@ -242,6 +247,18 @@ int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* u
  * pass over the model.  `staging` (device) holds ials_host64_staging_bytes.
  * Host buffers should be page-locked (cudaHostRegister) for the copies to
  * overlap; pageable buffers work but serialise. */
+/* Rotated user passes (b = 128, unit weights, no heavy user rows): per block
+ * the eigendecomposition of G_pp, rows with <= 64 interactions solved through
+ * their Woodbury systems (ials_rot.cuh, ials_sweep_wb.cuh).  Default on
+ * (IALS_ROT=0 in the environment turns it off); returns the previous value. */
+int ials_set_rotation(int enable);
+
+/* Symmetric eigendecomposition of n_mat b x b matrices (b even, <= 128; cyclic
+ * Jacobi, one CTA each, fp32): A_z at A + z * stride (ld lda) -> QT_z (b x b, row j =
+ * eigenvector j), lam_z (b), and Q_z (b x b, column j = eigenvector j). */
+int ials_sym_eig(ials_session* s, int32_t n_mat, int32_t b, const float* A, int32_t lda,
+                 int64_t stride, float* QT, float* lam, float* Q, void* stream);
+
 /* Page-lock (cudaHostRegister, portable) / release a caller's host range in
  * place, so ials_epoch_host64 copies overlap the epoch without a host-side
  * staging copy.  Registering an already registered range is not an error. */

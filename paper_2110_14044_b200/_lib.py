@@ -39,7 +39,7 @@ class IalsSched(ctypes.Structure):
                 ("tc_n_slices", c_i32), ("tc_slice_row", c_p), ("tc_slice_begin", c_p),
                 ("tc_slice_end", c_p), ("tc_n_waves", c_i32), ("tc_wave_row0", c_p),
                 ("tc_wave_slice0", c_p), ("tc_max_wave_rows", c_i32),
-                ("tc_max_wave_slices", c_i32)]
+                ("tc_max_wave_slices", c_i32), ("n_deg_gt64", c_i32), ("n_deg_gt32", c_i32)]
 
 
 #: every symbol include/ials_b200.h declares, with its ctypes signature
@@ -77,6 +77,8 @@ SIGNATURES = {
                            c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p]),
     "ials_topk64": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
     "ials_scores": (c_i32, [c_p, c_p, c_i32, c_i32, c_p, c_i32, c_i32, c_i32, c_p, c_i32, c_p]),
+    "ials_set_rotation": (c_i32, [c_i32]),
+    "ials_sym_eig": (c_i32, [c_p, c_i32, c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_p]),
     "ials_host_register": (c_i32, [c_p, c_sz]),
     "ials_host_unregister": (c_i32, [c_p]),
     "ials_host64_staging_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i64]),

@@ -24,6 +24,8 @@
 #include "ials_sweep_tc2.cuh"
 #include "ials_sweep_tc4.cuh"
 #include "ials_sweep_pk.cuh"
+#include "ials_rot.cuh"
+#include "ials_sweep_wb.cuh"
 #include "ials_gemm_tc.cuh"
 #include "ials_sweep_b1.cuh"
 
@@ -35,6 +37,11 @@ struct ials_session {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   cudaStream_t aux_st = nullptr;              // heavy-row partials beside the light rows
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t rot_st = nullptr;              // the epoch's eigendecompositions beside the predictions
+  cudaEvent_t ev_rot0 = nullptr, ev_rot1 = nullptr;
+  cudaEvent_t ev_blk[64] = {};                // per block: its decomposition is ready
+  const float* rot_qm = nullptr;              // where this session's last rotated epoch left its
+  long long rot_key = 0;                      //   decompositions (and their inputs), and for what shape
   unsigned long long* err;  // device error word (ULLONG_MAX = clean)
   unsigned long long* redo; // rows the fused tensor-core sweep handed to SIMT
   const struct ChunkPlan* chunk = nullptr;   // set by ials_epoch_host around its first user pass
@@ -161,6 +168,11 @@ int ials_session_destroy(ials_session* s) {
   if (s->aux_st) cudaStreamDestroy(s->aux_st);
   if (s->ev_fork) cudaEventDestroy(s->ev_fork);
   if (s->ev_join) cudaEventDestroy(s->ev_join);
+  if (s->rot_st) cudaStreamDestroy(s->rot_st);
+  if (s->ev_rot0) cudaEventDestroy(s->ev_rot0);
+  if (s->ev_rot1) cudaEventDestroy(s->ev_rot1);
+  for (cudaEvent_t e : s->ev_blk)
+    if (e) cudaEventDestroy(e);
   if (s->ev_a) cudaEventDestroy(s->ev_a);
   if (s->ev_b) cudaEventDestroy(s->ev_b);
   delete s;
@@ -436,6 +448,48 @@ static unsigned dev_bit() {
   return 1u << (d & 31);
 }
 
+// ------------------------------------------------------------------ rotation
+static int g_rot = -1;   // -1: not yet read from IALS_ROT
+static bool rot_enabled() {
+  if (g_rot < 0) {
+    const char* e = getenv("IALS_ROT");
+    g_rot = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_rot == 1;
+}
+int ials_set_rotation(int enable) {
+  rot_enabled();
+  const int prev = g_rot;
+  g_rot = enable ? 1 : 0;
+  return prev;
+}
+
+static int eig_attrs(ials_session* s, int b) {
+  static unsigned init = 0;
+  if (!(init & dev_bit())) {
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sym_eig, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     eig_smem_bytes(128)));
+    init |= dev_bit();
+  }
+  (void)b;
+  return IALS_OK;
+}
+
+int ials_sym_eig(ials_session* s, int32_t n_mat, int32_t b, const float* A, int32_t lda,
+                 int64_t stride, float* QT, float* lam, float* Q, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (n_mat < 0 || b < 2 || b > 128 || (b & 1) || lda < b || !A || !QT || !lam)
+    return fail(s, IALS_E_INVALID, "sym_eig: bad arguments (b=%d, even, <= 128)", b);
+  if (n_mat == 0) return IALS_OK;
+  int rc = eig_attrs(s, b);
+  if (rc) return rc;
+  k_sym_eig<<<n_mat, kEigThreads, eig_smem_bytes(b), S(stream)>>>(A, lda, stride, b, QT, lam, nullptr, Q,
+                                                                    nullptr, 1);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
 // ------------------------------------------------------------------ side pass
 template <int BT>
 static int set_smem_attrs(ials_session* s) {
@@ -545,7 +599,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
   int rc = set_smem_attrs<128>(s);
   if (rc) return rc;
-  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 5 * sizeof(int), st));   // redo count, slice / row queues
+  // [0] redo count, [1] slice queue, [2] light-row queue, [4] redo queue,
+  // [5] / [6] the Woodbury tiles' queues (rotated user pass)
+  CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 8 * sizeof(int), st));
   // sub-row gathers by TMA (tile::gather4) when the fixed matrix allows it
   CUtensorMap fmap;
   memset(&fmap, 0, sizeof(fmap));
@@ -600,11 +656,15 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     }
     k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
     LAUNCH_CHECK(s);
+    // rotated user pass: the b x b sweep takes the rows with > 64 entries,
+    // the Woodbury tiles the rest (2 rows of <= 64, 4 rows of <= 32 per tile)
+    const int n_b = p.rot ? p.rot_n64 : p.n_light;
     // TMEM: 4 x 128 columns per SM; the packed sweep takes G rows per task
-    const int grid = std::min((p.n_light + G - 1) / G, 4 * kNumSMs);
+    const int grid = std::min(std::max((n_b + G - 1) / G, 1), 4 * kNumSMs);
     const ChunkPlan* cp = s->chunk;
     for (int c = 0; c < (cp ? cp->nch : 1); ++c) {
       SweepParams q = p;
+      q.n_light = n_b;
       if (cp) {
         rc = cp->prologue(c);
         if (rc) return rc;
@@ -613,7 +673,8 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         q.chunk = c;
         if (c > 0) CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt + 2, 0, sizeof(int), st));   // row queue
       }
-      if (G == 1) {
+      if (n_b == 0) {
+      } else if (G == 1) {
         if (unit)
           k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
         else
@@ -629,7 +690,26 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         else
           k_sweep_pk<4, false><<<grid, 128, PkLay<4>::BYTES, st>>>(q, fmap, use_tma);
       }
-      LAUNCH_CHECK(s);
+      if (n_b > 0) LAUNCH_CHECK(s);
+    }
+    if (p.rot) {
+      static unsigned winit = 0;
+      if (!(winit & dev_bit())) {
+        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, WbLay<2>::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, WbLay<4>::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        winit |= dev_bit();
+      }
+      const int n2 = p.rot_n32 - p.rot_n64, n4 = p.n_light - p.rot_n32;
+      if (n2 > 0) {
+        k_sweep_wb<2><<<std::min((n2 + 1) / 2, 4 * kNumSMs), 128, WbLay<2>::BYTES, st>>>(p, p.rot_n64, n2, p.redo_cnt + 5);
+        LAUNCH_CHECK(s);
+      }
+      if (n4 > 0) {
+        k_sweep_wb<4><<<std::min((n4 + 3) / 4, 4 * kNumSMs), 128, WbLay<4>::BYTES, st>>>(p, p.rot_n32, n4, p.redo_cnt + 6);
+        LAUNCH_CHECK(s);
+      }
     }
   }
   if (p.n_heavy > 0) {
@@ -829,12 +909,36 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
   return IALS_OK;
 }
 
+// drow (n_rows x b, the per-row d of a pass) inside a pass workspace: the
+// carve of side_pass_impl below
+static float* pass_drow(char* ws, const ials_side* side, const ials_sched* sched, int b) {
+  const size_t bt = block_tile(b);
+  char* w = ws;
+  w += al256(size_t(side->n_rows) * b * 4);             // proj
+  w += al256(size_t(sched->n_slices) * bt * bt * 4);    // hpart
+  w += al256(size_t(sched->n_slices) * bt * 8);         // gpart
+  w += al256(size_t(sched->n_heavy) * bt * 4);          // hdelta
+  w += al256(size_t(kTcPKS) * 4);                       // template
+  w += al256(size_t(side->n_rows) * 4 + 32);            // redo list
+  return reinterpret_cast<float*>(w);
+}
+
+// a rotated user pass (ials_rot.cuh): the pass sweeps F~ = F[:, pi] Q with the
+// diagonal template diag(eigenvalues) (rslab's rows pi), reads W[:, pi] Q
+// (wq) for the lam * w term and leaves d~ in drow for the back-rotation
+struct RotPass {
+  const float* Ft;      // n_fixed x b
+  const float* wq;      // n_rows x b
+  const float* lam;     // b eigenvalues
+  const float* rslab;   // d x b: rows [b0, b0 + b) = diag(lam)
+};
+
 static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sched* sched,
                           const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
                           int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
                           int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st,
                           bool proj_ready = false, const float* proj_in = nullptr,
-                          const ials_side* other = nullptr) {
+                          const ials_side* other = nullptr, const RotPass* rot = nullptr) {
   if (!side || !sched || !fixed || !own || !slab || !cache)
     return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
   if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
@@ -906,6 +1010,20 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.vec = (b % 4 == 0) && (reinterpret_cast<uintptr_t>(compact) % 16 == 0);
   }
   p.redo_total = s->redo;
+  p.rot = 0;
+  if (rot) {
+    p.rot = 1;
+    p.fixed = rot->Ft;
+    p.ldf = b;
+    p.fb0 = 0;
+    p.fixed_cols = b;
+    p.vec = 1;
+    p.slab = rot->rslab;
+    p.wq = rot->wq;
+    p.rot_lam = rot->lam;
+    p.rot_n64 = sched->n_deg_gt64;
+    p.rot_n32 = sched->n_deg_gt32;
+  }
   if (other && other->rows && other->cols && other->nnz == side->nnz) {   // same entries, other order
     p.x_rows = other->rows;
     p.x_cols = other->cols;
@@ -1050,12 +1168,14 @@ static char* carve_copies(char* w, int n, int d, TcCopies* c) {
   return w + al256(size_t(d) * c->ldt * 4);
 }
 
+static size_t rot_bytes(int n_users, int n_items, int d, int b);
 static size_t tc_gemm_bytes(int n_users, int n_items, int d, int b) {
   int su, spu, si, spi;
   gram_plan(std::max(n_users, 1), d, &su, &spu);
   gram_plan(std::max(n_items, 1), d, &si, &spi);
   return copies_bytes(n_users, d) + copies_bytes(n_items, d) +
-         al256(size_t(std::max(su, si)) * d * b * 4) + 2 * al256(size_t(b) * d * 4) + 1024;
+         al256(size_t(std::max(su, si)) * d * b * 4) + 2 * al256(size_t(b) * d * 4) + 1024 +
+         rot_bytes(n_users, n_items, d, b);
 }
 
 size_t ials_epoch_tc_bytes(int32_t n_users, int32_t n_items, int32_t d, int32_t b) {
@@ -1124,6 +1244,59 @@ static int proj_tc(ials_session* s, const float* own, int ldo, const TcCopies& O
   k_gemm3_tf32<<<dim3((O.n + 127) / 128, 1), kGemmThreads, GemmLay::BYTES, st>>>(ah, bh, slabT_lo ? bl : bh, job);
   LAUNCH_CHECK(s);
   return IALS_OK;
+}
+
+// out (m x n, ld ldo) = scale * A[:, a_k0 : a_k0 + K] B[:, b_k0 : b_k0 + K]^T
+// (+ out when acc): A (m x *), B (n x *) row-major fp32, the 3xTF32 TMA GEMM
+static int gemm_nt(ials_session* s, const float* A, int m, int a_cols, int lda, int a_k0,
+                   const float* Bm, int n, int b_cols, int ldb, int b_k0, int K, float* out,
+                   int ldo, float scale, bool acc, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return IALS_OK;
+  int rc = gemm_attrs(s);
+  if (!rc) rc = get_encode(s);
+  if (rc) return rc;
+  CUtensorMap am, bm;
+  rc = make_map(s, &am, A, a_cols, m, lda, 128);
+  const int bn = n > 128 ? 128 : rup(n, 16);
+  if (!rc) rc = make_map(s, &bm, Bm, b_cols, n, ldb, bn);
+  if (rc) return rc;
+  GemmJob job{m, 0, 0, n, bn, K, rup(K, kGemmKC), out, ldo, 0, scale};
+  job.a_k0 = a_k0;
+  job.b_k0 = b_k0;
+  job.accumulate = acc ? 1 : 0;
+  job.n_tiles = n > 128 ? (n + 127) / 128 : 0;
+  k_gemm3_tf32<<<dim3((m + 127) / 128, std::max(job.n_tiles, 1)), kGemmThreads, GemmLay::BYTES, st>>>(
+      am, bm, bm, job);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+// rotated user passes: scratch of one epoch (b = 128)
+struct RotWs {
+  float *Gd, *Gprev, *Gpart, *QT, *Qm, *lam, *rslab, *Ft, *WQ, *slabQT;
+};
+static size_t rot_bytes(int n_users, int n_items, int d, int b) {
+  if (b != 128 || d % b) return 0;
+  int si, spi;
+  gram_plan(std::max(n_items, 1), d, &si, &spi);
+  return 6 * al256(size_t(d) * b * 4) + al256(size_t(si) * d * b * 4) + al256(size_t(d) * 4) +
+         al256(size_t(std::max(n_items, 1)) * b * 4) + al256(size_t(std::max(n_users, 1)) * b * 4) + 1024;
+}
+static char* rot_carve(char* t, int n_users, int n_items, int d, int b, RotWs* r) {
+  int si, spi;
+  gram_plan(std::max(n_items, 1), d, &si, &spi);
+  auto take = [&](size_t bytes) { float* p = reinterpret_cast<float*>(t); t += al256(bytes); return p; };
+  r->Gd = take(size_t(d) * b * 4);
+  r->Gprev = take(size_t(d) * b * 4);
+  r->QT = take(size_t(d) * b * 4);
+  r->Qm = take(size_t(d) * b * 4);
+  r->rslab = take(size_t(d) * b * 4);
+  r->slabQT = take(size_t(d) * b * 4);
+  r->Gpart = take(size_t(si) * d * b * 4);
+  r->lam = take(size_t(d) * 4);
+  r->Ft = take(size_t(std::max(n_items, 1)) * b * 4);
+  r->WQ = take(size_t(std::max(n_users, 1)) * b * 4);
+  return t;
 }
 
 // ---- row shards (the multi-GPU host path): one factor shard's K-major
@@ -1436,6 +1609,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                        get_encode(s) == IALS_OK;
   TcCopies cw{}, ch{};
   float *P = nullptr, *sth = nullptr, *stl = nullptr;
+  RotWs rw{};
   if (tc_gemm) {
     char* t = ws + ((ws_bytes - tcb) & ~size_t(1023));
     pbytes = size_t(t - pws);
@@ -1449,6 +1623,10 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     sth = reinterpret_cast<float*>(t);
     t += al256(size_t(b) * d * 4);
     stl = reinterpret_cast<float*>(t);
+    t += al256(size_t(b) * d * 4);
+    if (rot_bytes(users->n_rows, items->n_rows, d, b))
+      rot_carve(reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(t) + 1023) & ~uintptr_t(1023)),
+                users->n_rows, items->n_rows, d, b, &rw);
   }
   if (host) {
     // H in full, then W in row chunks, host -> device on the copy stream; the
@@ -1461,6 +1639,86 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   if (tc_gemm && !host) {
     int rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
     if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+    if (rc) return rc;
+  }
+  // rotated user passes (ials_rot.cuh): every block's G_pp = H_pi^T H_pi is
+  // final at the start of the epoch (H[:, pi] changes only in block pi's item
+  // pass, after its user pass), so all eigendecompositions run here, on a
+  // side stream beside the prediction cache
+  const bool rot = tc_gemm && rot_enabled() && rw.Gd && d / b <= 64 && user_sched->n_heavy == 0 &&
+                   !users->weights && !users->labels && user_sched->n_light > 0 && items->n_rows > 0;
+  // Every block's G_pp = H_pi^T H_pi is final at the start of the epoch (H[:, pi]
+  // changes only in block pi's item pass, after its user pass): the diagonal
+  // Gram blocks are formed at once and decomposed one CTA per block on a
+  // high-priority side stream, block pi's user pass waiting only for its own
+  // (k_sym_eig returns at once for a G bit-identical to the one its outputs
+  // were computed from -- the decompositions the previous epoch prepared for
+  // this one, below).
+  const int nblk = d / b;
+  const long long rkey = ((long long)d << 40) ^ ((long long)items->n_rows << 8) ^ b;
+  auto diag_gram = [&](int z0, int nz) -> int {   // Gd rows of blocks [z0, z0 + nz), on rot_st
+    int S_i, span_i;
+    gram_plan(std::max(items->n_rows, 1), d, &S_i, &span_i);
+    CUtensorMap gm;   // H^T (d x n_items): A and B operands, B rows following the A tile
+    int rc = make_map(s, &gm, ch.FT, ch.n, d, ch.ldt, 128);
+    if (rc) return rc;
+    GemmJob job{d, z0 * b, z0 * b, b, 128, ch.n, span_i, rw.Gpart, b, (long long)d * b, 1.f};
+    job.diag = 1;
+    k_gemm3_tf32<<<dim3(nz, S_i), kGemmThreads, GemmLay::BYTES, s->rot_st>>>(gm, gm, gm, job);
+    LAUNCH_CHECK(s);
+    // (the GEMM wrote rows [0, nz * b) of each split: rows of blocks z0.. relative to z0)
+    const size_t cnt = size_t(nz) * b * b;
+    k_reduce_splits_strided<<<(int)std::min<size_t>((cnt + 255) / 256, 4096), 256, 0, s->rot_st>>>(
+        rw.Gpart, S_i, (long long)d * b, cnt, rw.Gd + size_t(z0) * b * b);
+    LAUNCH_CHECK(s);
+    return IALS_OK;
+  };
+  auto launch_eig = [&]() -> int {   // after H's K-major copy is current on st
+    if (!s->rot_st) {   // highest priority: its CTAs take SMs as the predictions' retire
+      int lo = 0, hi = 0;
+      CUDA_TRY(s, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CUDA_TRY(s, cudaStreamCreateWithPriority(&s->rot_st, cudaStreamNonBlocking, hi));
+      CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_rot0, cudaEventDisableTiming));
+      CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_rot1, cudaEventDisableTiming));
+    }
+    for (int z = 0; z < nblk; ++z)
+      if (!s->ev_blk[z]) CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_blk[z], cudaEventDisableTiming));
+    int rc = gemm_attrs(s);
+    if (!rc) rc = eig_attrs(s, b);
+    if (rc) return rc;
+    CUDA_TRY(s, cudaEventRecord(s->ev_rot0, st));
+    CUDA_TRY(s, cudaStreamWaitEvent(s->rot_st, s->ev_rot0, 0));
+    rc = diag_gram(0, nblk);
+    if (rc) return rc;
+    // the outputs in place are trusted only if this session left them there
+    // for this shape; otherwise every block is recomputed
+    const int force = (s->rot_qm == rw.Qm && s->rot_key == rkey) ? 0 : 1;
+    for (int z = 0; z < nblk; ++z) {
+      const size_t o = size_t(z) * b * b;
+      k_sym_eig<<<1, kEigThreads, eig_smem_bytes(b), s->rot_st>>>(rw.Gd + o, b, 0, b, rw.QT + o, rw.lam + z * b,
+                                                                  rw.rslab + o, rw.Qm + o, rw.Gprev + o, force);
+      LAUNCH_CHECK(s);
+      CUDA_TRY(s, cudaEventRecord(s->ev_blk[z], s->rot_st));
+    }
+    s->rot_qm = rw.Qm;
+    s->rot_key = rkey;
+    return IALS_OK;
+  };
+  // after block zb's item pass (H[:, pi] final for the rest of the epoch, its
+  // K-major copy synced on st): its decomposition for the next epoch
+  auto prepare_next = [&](int zb) -> int {
+    CUDA_TRY(s, cudaEventRecord(s->ev_rot0, st));
+    CUDA_TRY(s, cudaStreamWaitEvent(s->rot_st, s->ev_rot0, 0));
+    int rc = diag_gram(zb, 1);
+    if (rc) return rc;
+    const size_t o = size_t(zb) * b * b;
+    k_sym_eig<<<1, kEigThreads, eig_smem_bytes(b), s->rot_st>>>(rw.Gd + o, b, 0, b, rw.QT + o, rw.lam + zb * b,
+                                                                rw.rslab + o, rw.Qm + o, rw.Gprev + o, 0);
+    LAUNCH_CHECK(s);
+    return IALS_OK;
+  };
+  if (rot && !host) {
+    const int rc = launch_eig();
     if (rc) return rc;
   }
   CUDA_TRY(s, rec_event(0, st));
@@ -1477,7 +1735,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   const int nl = user_sched->n_light;
   const size_t part_need = 4 * al256(size_t(std::max(nl, 1)) * 4) +
                            al256(size_t((nl + kRadixTile - 1) / kRadixTile + 1) * 256 * 4) + al256(256 * 4);
-  bool chunked = host && tc_gemm && nl > 0 && kChunks > 1 && U >= kChunks;
+  bool chunked = host && tc_gemm && nl > 0 && kChunks > 1 && U >= kChunks && !rot;
   if (chunked) {
     int su, spu, si, spi;
     gram_plan(std::max(users->n_rows, 1), d, &su, &spu);
@@ -1544,6 +1802,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     if (tc_gemm) {
       rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
       if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+      if (!rc && rot) rc = launch_eig();
       if (rc) return rc;
     }
   } else if (range.recompute) {
@@ -1559,11 +1818,24 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     const int pu = 2 * (b0 / b);
     const bool do_u = pu >= range.pass0 && pu < range.pass0 + range.npass;
     const bool do_i = pu + 1 >= range.pass0 && pu + 1 < range.pass0 + range.npass;
+    const int zb = b0 / b;
+    const bool rot_u = rot && bb == 128;
+    RotPass rp{rw.Ft, rw.WQ, rw.lam + b0, rw.rslab};
     if (do_u) {
+    if (rot_u) CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_blk[zb], 0));   // this block's decomposition
     if (tc_gemm) {
       rc = gram_tc(s, ch, d, b0, bb, P, slab, sth, stl, st);
-      if (!rc && !first_chunked)
+      if (!rc && rot_u) {
+        // (slab Q)^T = Q^T slab^T -> the rotated projection alpha0 W slab Q;
+        // F~ = H[:, pi] Q and W[:, pi] Q
+        const float* qt = rw.QT + size_t(zb) * b * b;
+        rc = gemm_nt(s, qt, b, b, b, 0, slab, d, bb, bb, 0, b, rw.slabQT, d, 1.f, false, st);
+        if (!rc) rc = proj_tc(s, W, ldw, cw, d, bb, rw.slabQT, nullptr, alpha0, reinterpret_cast<float*>(pws), st);
+        if (!rc) rc = gemm_nt(s, H, items->n_rows, d, ldh, b0, qt, b, b, b, 0, b, rw.Ft, b, 1.f, false, st);
+        if (!rc) rc = gemm_nt(s, W, users->n_rows, d, ldw, b0, qt, b, b, b, 0, b, rw.WQ, b, 1.f, false, st);
+      } else if (!rc && !first_chunked) {
         rc = proj_tc(s, W, ldw, cw, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
+      }
     } else {
       rc = gramian_impl(s, H, items->n_rows, ldh, d, b0, bb, slab, part, gbytes, st);
     }
@@ -1571,9 +1843,14 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     CUDA_TRY(s, rec_event(ek++, st));
     if (first_chunked) s->chunk = &plan;
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
-                        pws, pbytes, st, tc_gemm, nullptr, items);
+                        pws, pbytes, st, tc_gemm, nullptr, items, rot_u ? &rp : nullptr);
     s->chunk = nullptr;
     if (rc) return rc;
+    if (rot_u) {   // W[:, pi] -= d~ Q^T: the rows' steps back in the original basis
+      rc = gemm_nt(s, pass_drow(pws, users, user_sched, bb), users->n_rows, b, b, 0,
+                   rw.Qm + size_t(zb) * b * b, b, b, b, 0, b, W + b0, ldw, -1.f, true, st);
+      if (rc) return rc;
+    }
     if (host) {   // W[:, b0:b0+bb] is final: back to the host beside the rest of the epoch
       rc = host_cols_out(s, st, host, host->W_out, host->ldw, W, ldw, users->n_rows, d, b0, bb,
                          host->sW);
@@ -1604,7 +1881,15 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       rc = sync_copies(s, H, ldh, d, b0, bb, ch, st);
       if (rc) return rc;
     }
+    if (rot && zb + 1 < nblk) {   // (the last block's is prepared by the next epoch's start)
+      rc = prepare_next(zb);
+      if (rc) return rc;
+    }
     CUDA_TRY(s, rec_event(ek++, st));
+  }
+  if (rot) {   // the caller's stream covers the side stream's use of the workspace
+    CUDA_TRY(s, cudaEventRecord(s->ev_rot1, s->rot_st));
+    CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_rot1, 0));
   }
   if (host) {   // the maintained cache, then the caller's stream waits for every copy
     if (host->cache_out) {

@@ -40,6 +40,10 @@ struct GemmJob {
   int b_lo_tma = 0;        // B's lo part is precomputed in memory (b_lo map): TMA-load it
   int n_tiles = 0;         // > 0: blockIdx.y walks N tiles of 128 output columns (B rows
                            // b_row0 + 128 y, out columns 128 y..), no K split (score GEMM)
+  int a_k0 = 0;            // K coordinate of A's first column (a column block of A's map)
+  int b_k0 = 0;            // the same for B
+  int accumulate = 0;      // out += scale * acc instead of out = scale * acc
+  int diag = 0;            // B rows follow the A tile (b_row0 + m0): diagonal blocks of F^T F
 };
 
 constexpr int kGemmStages = 3;
@@ -72,7 +76,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int m0 = blockIdx.x * 128;
   const int ny = job.n_tiles ? (int)blockIdx.y : 0;   // N tile
   const int ks = job.n_tiles ? 0 : (int)blockIdx.y;   // K split
-  const int b_row = job.b_row0 + 128 * ny;
+  const int b_row = job.b_row0 + 128 * ny + (job.diag ? m0 : 0);
   const int n_here = job.n_tiles ? min(128, job.n - 128 * ny) : job.n;
   const int kb = ks * job.k_span;
   const int ke = min(kb + job.k_span, job.k_total);
@@ -101,10 +105,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       char* st = smem + s * GemmLay::STAGE;
       mbar_expect_tx(full + s, stage_bytes);
       const int kc = kb + c * kGemmKC;
-      tma_load_2d(smem_u32(st), &a_hi, kc, job.a_row0 + m0, full + s);
-      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, kc, b_row, full + s);
+      tma_load_2d(smem_u32(st), &a_hi, job.a_k0 + kc, job.a_row0 + m0, full + s);
+      tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES), &b_hi, job.b_k0 + kc, b_row, full + s);
       if (job.b_lo_tma)
-        tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, kc, b_row, full + s);
+        tma_load_2d(smem_u32(st + 2 * GemmLay::A_BYTES + GemmLay::B_BYTES), &b_lo, job.b_k0 + kc, b_row,
+                    full + s);
     }
   } else if (warp == 1 && (tid & 31) == 0) {  // MMA issuer
     const uint32_t idesc = make_idesc_tf32(128, job.bn, 0, 0, 0);
@@ -161,7 +166,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float v[32];
     tmem_ld32(raddr + c32, v);
     tmem_wait_ld();
-    if (row < job.m_rows && nk > 0) {
+    if (row < job.m_rows && nk > 0 && job.accumulate) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c32 + j < n_here) o[c32 + j] += job.scale * v[j];
+    } else if (row < job.m_rows && nk > 0) {
       if (c32 + 32 <= n_here && (job.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(job.out) & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4)   // 16-byte stores: 8 per thread instead of 32
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int j = 0; j < 32; ++j)
           if (c32 + j < n_here) o[c32 + j] = job.scale * v[j];
       }
-    } else if (row < job.m_rows) {
+    } else if (row < job.m_rows && !job.accumulate) {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (c32 + j < n_here) o[c32 + j] = 0.f;

@@ -84,6 +84,14 @@ struct SweepParams {
   float* drow;             // [n_rows][b] per-row d of the fused sweep (k_pass_cache)
   int fb0;                 // column of the block in `fixed` (b0, or 0 for a compact copy)
   int fixed_cols;          // columns of `fixed` (d, or the compact copy's width)
+  // rotated user pass (ials_rot.cuh): fixed = F[:, pi] Q, proj = the rotated
+  // projection, slab[pi, pi] = diag(eigenvalues); the lam * w term reads
+  // wq = W[:, pi] Q, and the row's d~ goes to drow only (own is updated by
+  // the back-rotation GEMM, the cache by the pass's cache kernel)
+  int rot;
+  const float* wq;
+  const float* rot_lam;
+  int rot_n64, rot_n32;    // light rows with > 64 / > 32 entries (prefix lengths)
   const int* x_rows;       // the other side's view of the same entries (rows = fixed-side ids,
   const int* x_cols;       //   cols = this side's ids, x_pos = cache positions or NULL): the
   const int* x_pos;        //   cache pass may walk it instead (k_pass_cache_flat<., ., true>)
@@ -362,7 +370,8 @@ IALS_DEVI void finalize_and_solve(const SweepParams& p, Tiles<BT>& T, double gac
     double g = 0.0;
     if (tid < b)
       g = gacc + (double)p.proj[(size_t)row * b + tid] +
-          (double)lam * (double)p.own[(size_t)row * p.ldo + p.b0 + tid];
+          (double)lam * (double)(p.rot ? p.wq[(size_t)row * b + tid]
+                                       : p.own[(size_t)row * p.ldo + p.b0 + tid]);
     ys[tid] = (float)g;
   }
   const float a0 = p.alpha0;
@@ -669,8 +678,12 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
     const int nch = accumulate_range<BT>(p, T, gacc, sm, ebeg, eend, tid, team);
     finalize_and_solve<BT>(p, T, gacc, sm, row, tid, team);
     const float* ds = sm + L::OFF_D;
-    if (tid < p.b) p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
-    cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);
+    if (p.rot) {   // d~ for the back-rotation and the pass's cache kernel
+      if (tid < p.b) p.drow[(size_t)row * p.b + tid] = ds[tid];
+    } else {
+      if (tid < p.b) p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
+      cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);
+    }
     team_sync<L::NW>(team);
     if (p.queue) {
       if (tid == 0) *qslot = nxt;

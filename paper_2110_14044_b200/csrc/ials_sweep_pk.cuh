@@ -275,16 +275,16 @@ IALS_DEVI void pk_accumulate(const SweepParams& p, char* smem, PkState& st, doub
 // (tc4_factor with per-slot diagonal warps, per-slot shared state and
 // full-width trailing MMAs).  Returns with packed L (per slot), 1/pivots in
 // OFF_ID and the forward-solved right-hand side in OFF_YF.
-template <int G>
-IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t row_addr, int tid) {
-  using L = PkLay<G>;
+template <int G, class L = PkLay<G>>
+IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t row_addr, int tid,
+                         const int b) {
   float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
   float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
   float* invd = reinterpret_cast<float*>(smem + L::OFF_ID);
   const float* DIAG = reinterpret_cast<const float*>(smem + L::OFF_DIAG);
   int* FLAG = reinterpret_cast<int*>(smem + L::OFF_FLAG);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  const int b = p.b, lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   const int g = tid / L::NG, i = tid - g * L::NG;   // slot, row within the slot
   float* lrow = reinterpret_cast<float*>(smem + L::OFF_L) + g * L::LPS + i * (i + 1) / 2;
   const int np = (b + 7) >> 3;
@@ -443,15 +443,14 @@ IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t
 
 // 16 x 16 diagonal-block inverses of every slot's L: thread t -> block t / 16
 // (slot (t / 16) / (NG / 16)), column q = t % 16
-template <int G>
-IALS_DEVI void pk_block_inverses(const SweepParams& p, char* smem, int tid) {
-  using L = PkLay<G>;
+template <int G, class L = PkLay<G>>
+IALS_DEVI void pk_block_inverses(char* smem, int tid, const int b) {
   constexpr int NBS = L::NG / 16;
   const float* invd = reinterpret_cast<const float*>(smem + L::OFF_ID);
   float* LI = reinterpret_cast<float*>(smem + L::OFF_LI);
   const int blk = tid >> 4, q = tid & 15, g = blk / NBS, c0 = 16 * (blk - g * NBS);
   const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L) + g * L::LPS;
-  if (c0 >= p.b) return;
+  if (c0 >= b) return;
   float x[16];
 #pragma unroll
   for (int mm = 0; mm < 16; ++mm) {
@@ -460,21 +459,20 @@ IALS_DEVI void pk_block_inverses(const SweepParams& p, char* smem, int tid) {
     const float* lr = Lp + gm * (gm + 1) / 2 + c0;
 #pragma unroll
     for (int k = 0; k < mm; ++k) t = fmaf(-lr[k], x[k], t);
-    x[mm] = (mm >= q && gm < p.b) ? t * invd[g * L::NG + gm] : 0.f;
+    x[mm] = (mm >= q && gm < b) ? t * invd[g * L::NG + gm] : 0.f;
   }
 #pragma unroll
   for (int mm = 0; mm < 16; ++mm) LI[blk * 256 + mm * 16 + q] = x[mm];
 }
 
 // backward solve L^T d = y of every slot, 16-wide blocks from the last
-template <int G>
-IALS_DEVI void pk_backward(const SweepParams& p, char* smem, int tid) {
-  using L = PkLay<G>;
+template <int G, class L = PkLay<G>>
+IALS_DEVI void pk_backward(char* smem, int tid, const int b) {
   constexpr int NBS = L::NG / 16;
   const float* LI = reinterpret_cast<const float*>(smem + L::OFF_LI);
   float* yf = reinterpret_cast<float*>(smem + L::OFF_YF);
   float* ds = reinterpret_cast<float*>(smem + L::OFF_D);
-  const int b = p.b, g = tid / L::NG, i = tid - g * L::NG;
+  const int g = tid / L::NG, i = tid - g * L::NG;
   const float* Lp = reinterpret_cast<const float*>(smem + L::OFF_L) + g * L::LPS;
   float* yg = yf + g * L::NG;
   float* dg = ds + g * L::NG;
@@ -641,11 +639,11 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
       ys[tid] = gv;
     }
     __syncthreads();
-    pk_factor<G>(p, smem, st, row_addr, tid);
+    pk_factor<G>(p, smem, st, row_addr, tid, b);
     if (tid < G && task_next < n_tiles) put_tile(tb ^ 1, tid, nrow);
-    pk_block_inverses<G>(p, smem, tid);
+    pk_block_inverses<G>(smem, tid, b);
     __syncthreads();
-    pk_backward<G>(p, smem, tid);
+    pk_backward<G>(smem, tid, b);
     const bool bad = FLAG[g] != 0;
     if (row >= 0 && m < b) {
       if (bad) {

@@ -657,7 +657,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
     const float lam = reinterpret_cast<const float*>(RI)[4 * rb + 3];
     // the projection and own value of this thread's column, used after the accumulate
     const float pj = (tid < b) ? __ldg(p.proj + (size_t)row * b + tid) : 0.f;
-    const float ow = (tid < b) ? p.own[(size_t)row * p.ldo + p.b0 + tid] : 0.f;
+    const float ow = (tid < b) ? (p.rot ? __ldg(p.wq + (size_t)row * b + tid)
+                                        : p.own[(size_t)row * p.ldo + p.b0 + tid]) : 0.f;
     tc4_init(p, row_addr, tid);
     if (rec) tph[1] = clock64();
     tmem_wait_st();
@@ -719,8 +720,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_tc4(SweepParams p,
       tc4_backward(p, smem, tid);
       if (rec) tph[5] = clock64();
       if (tid < b) {
-        p.own[(size_t)row * p.ldo + p.b0 + tid] = ow - ds[tid];
-        p.drow[(size_t)row * b + tid] = ds[tid];   // for k_pass_cache
+        if (!p.rot) p.own[(size_t)row * p.ldo + p.b0 + tid] = ow - ds[tid];
+        p.drow[(size_t)row * b + tid] = ds[tid];   // for k_pass_cache (and the back-rotation)
       }
     }
     tc_fence_before();

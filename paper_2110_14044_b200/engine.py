@@ -164,6 +164,7 @@ class DeviceSide:
                   "nw": int(tp["wave_row0"].size - 1), "mr": tp["max_wave_rows"],
                   "ms": tp["max_wave_slices"]}
         hp = lambda a: ctypes.c_void_p(a.ctypes.data)
+        deg_light = self.counts[plan["light"]]   # descending: the counts are prefix lengths
         st = _lib.IalsSched(int(plan["light"].size), _ptr(t["light"]).value,
                             int(plan["heavy"].size), _ptr(t["heavy"]).value,
                             _ptr(t["slice0"]).value, int(plan["beg"].size),
@@ -175,7 +176,9 @@ class DeviceSide:
                             _ptr(t.get("tc_end")).value, tc.get("nw", 0),
                             hp(t["tc_wave_row0_h"]).value if tc["n"] else None,
                             hp(t["tc_wave_slice0_h"]).value if tc["n"] else None,
-                            tc.get("mr", 0), tc.get("ms", 0))
+                            tc.get("mr", 0), tc.get("ms", 0),
+                            int(np.count_nonzero(deg_light > 64)),
+                            int(np.count_nonzero(deg_light > 32)))
         sch = Schedule(t, st, int(plan["light"].size), int(plan["heavy"].size),
                        int(plan["beg"].size), tc.get("mr", 0), tc.get("ms", 0))
         self._sched[bt] = sch

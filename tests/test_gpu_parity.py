@@ -416,3 +416,71 @@ def test_dropin_host64_bit_identical_to_device_epoch(ials, d, b):
     ials.ialspp_epoch(m4, data, c4, cfg)
     assert np.array_equal(m3.user_factors, m4.user_factors)
     assert np.array_equal(c3.scores, c4.scores)
+
+
+def test_sym_eig_jacobi(ials):
+    """ials_sym_eig (cyclic Jacobi, fp32): Q^T A Q diagonal and A Q = Q L to
+    fp32 accuracy on Gram matrices like the sweep's G_pp (wide spectrum)."""
+    from paper_2110_14044_b200 import _lib
+    from paper_2110_14044_b200._runtime import default_engine_session
+    from paper_2110_14044_b200.engine import _ptr, current_stream_handle
+    rt = default_engine_session(0)
+    rng = np.random.default_rng(2)
+    mats = []
+    for scale in (1.0, 1e-3, 50.0):
+        F = rng.standard_normal((3000, 128)) * scale
+        F[:, :5] *= 30.0                               # a few dominant directions
+        mats.append(F.T @ F)
+    A = torch.from_numpy(np.stack(mats).astype(np.float32)).cuda()
+    QT = torch.empty_like(A)
+    Q = torch.empty_like(A)
+    lam = torch.empty((3, 128), device="cuda")
+    rc = rt.lib.ials_sym_eig(rt.session.handle, 3, 128, _ptr(A), 128, 128 * 128, _ptr(QT), _ptr(lam),
+                             _ptr(Q), current_stream_handle(A.device))
+    rt.session.check(rc, "sym_eig")
+    for z in range(3):
+        a = A[z].double().cpu().numpy()
+        q = Q[z].double().cpu().numpy()
+        assert np.allclose(QT[z].double().cpu().numpy(), q.T)
+        off = q.T @ a @ q - np.diag(lam[z].double().cpu().numpy())
+        assert np.linalg.norm(off) <= 5e-6 * np.linalg.norm(a)
+        # the fp32 rotations drift from orthogonality (~5e-4 after a cold
+        # decomposition); the rotated solve does not need it -- it uses the
+        # same Q on both sides, only the residual above enters the Hessian
+        assert np.linalg.norm(q.T @ q - np.eye(128)) <= 3e-3
+
+
+@pytest.mark.parametrize("d", [128, 256])
+def test_rotated_user_pass_matches_unrotated(ials, d):
+    """The rotated user passes (eigenbasis of G_pp, Woodbury tiles for rows
+    with <= 64 interactions, b = 128) against the unrotated sweep and the
+    oracle over three epochs."""
+    from oracle import ialspp_oracle as orc
+    from paper_2110_14044_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(31 + d)
+    U, I, nnz = 3000, 700, 90000
+    users = np.repeat(np.arange(U), rng.integers(1, 61, U))[:nnz]
+    users = np.concatenate([users, rng.integers(0, 300, nnz - users.size)]) if users.size < nnz else users
+    items = np.minimum(rng.zipf(1.2, users.size) - 1, I - 1)
+    data = ials.InteractionDataset(U, I, users, items)
+    cfg = ials.SolverConfig(dim=d, block_size=128, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=3, seed=4)
+    out = {}
+    for rot in (1, 0):
+        prev = lib.ials_set_rotation(rot)
+        try:
+            m = ials.init_model(cfg, U, I)
+            m.user_factors[:] = m.user_factors.astype(np.float32)
+            m.item_factors[:] = m.item_factors.astype(np.float32)
+            w0, h0 = m.user_factors.copy(), m.item_factors.copy()
+            ials.train(m, data, cfg)
+            out[rot] = m
+        finally:
+            lib.ials_set_rotation(prev)
+    for a, b_ in ((out[1].user_factors, out[0].user_factors), (out[1].item_factors, out[0].item_factors)):
+        assert relf(a, b_) < 1e-4
+    csr = orc.build_csr(U, I, data.users, data.items)
+    orc.train(w0, h0, csr, 0.1, 1e-3, 1.0, 128, 3)
+    for got, want in ((out[1].user_factors, w0), (out[1].item_factors, h0)):
+        assert relf(got, want) < TOL and relmax(got, want) < TOL
