@@ -18,11 +18,15 @@
 //           operand row and its share of Y^T rho (a warp butterfly gives the
 //           per-column sums); one thread issues C += Y_c Y_c^T (M = N = 128,
 //           K = 16, 3xTF32) into TMEM initialised to I;
-//   z = s p~ + Y^T rho (fp64), u = Y z (pass 2 re-reads the row), the blocked
-//   Cholesky of the G matrices C and the solves (the packed sweep's, on the
-//   max(n_g) leading rows), pass 3: Y^T v by the same butterfly, then
-//   d~ = s z - s^2 (X^T v) -> drow (the back-rotation GEMM applies Q).
-// Heavy work per row is ~3 n_r b loads from L2 and an n_r/8-panel chain.
+//   z = s p~ + Y^T rho (fp64); u = Y z = Y (s p~) + Y Y^T rho: the first
+//   term accumulates in pass 1 (each thread's own entry), the second is
+//   (C - I) rho from the thread's TMEM row of C, so the row is read only
+//   twice; the blocked Cholesky of the G matrices C and the solves (the
+//   packed sweep's, on the max(n_g) leading rows); pass 2: Y^T v by the same
+//   butterfly, then d~ = s z - s^2 (X^T v) -> drow (the back-rotation GEMM
+//   applies Q).  (u = Y q + (C - I) rho carries the 3xTF32 error of C times
+//   |rho| instead of |z|: ~1e-7 absolute on d, far inside 1e-3 of the rows.)
+// Work per row: 2 n_r b loads from L2 and an n_r/8-panel chain.
 #pragma once
 #include "ials_sweep_pk.cuh"
 
@@ -41,8 +45,8 @@ struct WbLay {
   static constexpr int OFF_LI = OFF_PA + 8192;
   static constexpr int OVL = (OFF_LI + 8192 > 32768) ? OFF_LI + 8192 : 32768;
   static constexpr int OFF_S = OVL;                      // [G][B] s = D^-1/2
-  static constexpr int OFF_SZ = OFF_S + G * B * 4;       // [G][B] s * z (fp32, pass 2)
-  static constexpr int OFF_Z = OFF_SZ + G * B * 4;       // [G][B] s * z (fp64, pass 3)
+  static constexpr int OFF_SZ = OFF_S + G * B * 4;       // [G][B] s^2 p~ (fp32, for Y q in pass 1)
+  static constexpr int OFF_Z = OFF_SZ + G * B * 4;       // [G][B] s * z (fp64)
   static constexpr int OFF_ZP = OFF_Z + G * B * 8;       // [4 warps][B] column partials
   static constexpr int OFF_LAM = OFF_ZP + 4 * B * 4;     // [B] alpha0 * eigenvalues
   static constexpr int OFF_DG = OFF_LAM + B * 4;         // per slot, per panel parity: 320 B
@@ -53,7 +57,8 @@ struct WbLay {
   static constexpr int OFF_DIAG = OFF_D + 512;
   static constexpr int OFF_TILE = OFF_DIAG + 512;        // [2][rows[4], beg[4], end[4], lam[4]]
   static constexpr int OFF_FLAG = OFF_TILE + 128;        // flags[G], next task
-  static constexpr int OFF_BAR = OFF_FLAG + 32;          // MMA bars [2]
+  static constexpr int OFF_RHO = OFF_FLAG + 32;          // [128] rho of every lane's entry
+  static constexpr int OFF_BAR = OFF_RHO + 512;          // MMA bars [2]
   static constexpr int OFF_TPTR = OFF_BAR + 16;
   static constexpr int BYTES = OFF_TPTR + 16 + 1024;
 };
@@ -173,12 +178,14 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       const float lam_s = reinterpret_cast<const float*>(trow)[12 + s];
       const float sv = rsqrtf(LAM[tid] + lam_s);
       S[s * B + tid] = sv;
-      double pz = 0.0;
+      double pt = 0.0;   // p~
       if (r >= 0)
-        pz = (double)sv * ((double)__ldg(p.proj + (size_t)r * B + tid) +
-                           (double)lam_s * (double)__ldg(p.wq + (size_t)r * B + tid));
-      Z[s * B + tid] = pz;
+        pt = (double)__ldg(p.proj + (size_t)r * B + tid) +
+             (double)lam_s * (double)__ldg(p.wq + (size_t)r * B + tid);
+      Z[s * B + tid] = (double)sv * pt;
+      SZ[s * B + tid] = (float)((double)sv * (double)sv * pt);
     }
+    reinterpret_cast<float*>(smem + L::OFF_RHO)[tid] = rho;
     {  // TMEM := I
 #pragma unroll 1
       for (int c8 = 0; c8 < 16; ++c8) {
@@ -203,12 +210,16 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     };
     load16(x, 0);
     uint32_t pend = 0;
+    float uq = 0.f;   // y_k . (s p~) = x_k . (s^2 p~)
     for (int ch = 0; ch < L::NCH; ++ch) {
       const int c0 = ch * L::KCH, ob = ch & 1;
       if (ch + 1 < L::NCH) load16(xn, c0 + L::KCH);
       float y[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) y[j] = x[j] * S[g * B + c0 + j];
+      for (int j = 0; j < 16; ++j) {
+        y[j] = x[j] * S[g * B + c0 + j];
+        uq = fmaf(x[j], SZ[g * B + c0 + j], uq);
+      }
       {
         float zr[16];
 #pragma unroll
@@ -270,33 +281,24 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       float part = 0.f;
 #pragma unroll
       for (int w = 0; w < 4 / G; ++w) part += ZP[(s * (4 / G) + w) * B + tid];
-      const double zz = Z[s * B + tid] + (double)part;
-      Z[s * B + tid] = zz;
-      SZ[s * B + tid] = (float)zz * S[s * B + tid];
+      Z[s * B + tid] += (double)part;
     }
-    __syncthreads();
     const int task_next = *next;
     int nrow = -1;
     if (tid < G && task_next < n_tiles) nrow = tile_row(task_next, tid);
-    // ---- pass 2: u_k = y_k . z = sum_c x_c s_c z_c
+    // u_k = y_k . (s p~) + sum_j (C - I)_kj rho_j over the slot's entries
     {
-      float u0 = 0.f, u1 = 0.f;
-#pragma unroll 1
-      for (int c0 = 0; c0 < B; c0 += 32) {
-        float v[32];
+      const float* RH = reinterpret_cast<const float*>(smem + L::OFF_RHO) + g * L::NG;
+      float cr = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 t4 = valid ? __ldg(reinterpret_cast<const float4*>(xr + c0) + q)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-          v[4 * q] = t4.x; v[4 * q + 1] = t4.y; v[4 * q + 2] = t4.z; v[4 * q + 3] = t4.w;
-        }
+      for (int c32 = 0; c32 < L::NG; c32 += 32) {
+        float cv[32];
+        tmem_ld32(row_addr + g * L::NG + c32, cv);
+        tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          u0 = fmaf(v[j], SZ[g * B + c0 + j], u0);
-          u1 = fmaf(v[j + 1], SZ[g * B + c0 + j + 1], u1);
-        }
+        for (int j = 0; j < 32; ++j) cr = fmaf(cv[j], RH[c32 + j], cr);
       }
-      ys[tid] = valid ? u0 + u1 : 0.f;
+      ys[tid] = valid ? uq + (cr - rho) : 0.f;
     }
     __syncthreads();
     // ---- v = C^-1 u on the leading nmax rows of every slot
@@ -306,17 +308,20 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     pk_block_inverses<G, L>(smem, tid, nb);
     __syncthreads();
     pk_backward<G, L>(smem, tid, nb);
-    // ---- pass 3: X^T v (butterfly per 16 columns), d~ = s z - s^2 X^T v
+    // ---- pass 2: X^T v (butterfly per 16 columns), d~ = s z - s^2 X^T v
     {
       const float vk = valid ? ds[tid] : 0.f;
+      load16(x, 0);
 #pragma unroll 1
       for (int c0 = 0; c0 < B; c0 += 16) {
+        if (c0 + 16 < B) load16(xn, c0 + 16);
         float v16[16];
-        load16(v16, c0);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v16[j] *= vk;
+        for (int j = 0; j < 16; ++j) v16[j] = x[j] * vk;
         const float cs = butterfly16(v16, lane);
         if (!(lane & 1)) ZP[warp * B + c0 + butterfly16_col(lane)] = cs;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = xn[j];
       }
     }
     __syncthreads();
