@@ -1011,6 +1011,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   }
   p.redo_total = s->redo;
   p.rot = 0;
+  p.flat_skip_deg = 0;
   if (rot) {
     p.rot = 1;
     p.fixed = rot->Ft;
@@ -1023,6 +1024,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.rot_lam = rot->lam;
     p.rot_n64 = sched->n_deg_gt64;
     p.rot_n32 = sched->n_deg_gt32;
+    p.flat_skip_deg = 64;   // the Woodbury tiles update their rows' cache themselves
   }
   if (other && other->rows && other->cols && other->nnz == side->nnz) {   // same entries, other order
     p.x_rows = other->rows;

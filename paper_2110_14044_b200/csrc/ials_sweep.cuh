@@ -92,6 +92,8 @@ struct SweepParams {
   const float* wq;
   const float* rot_lam;
   int rot_n64, rot_n32;    // light rows with > 64 / > 32 entries (prefix lengths)
+  int flat_skip_deg;       // k_pass_cache_flat skips rows with at most this many entries
+                           // (their cache is updated by the kernel that solved them)
   const int* x_rows;       // the other side's view of the same entries (rows = fixed-side ids,
   const int* x_cols;       //   cols = this side's ids, x_pos = cache positions or NULL): the
   const int* x_pos;        //   cache pass may walk it instead (k_pass_cache_flat<., ., true>)
@@ -680,6 +682,7 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
     const float* ds = sm + L::OFF_D;
     if (p.rot) {   // d~ for the back-rotation and the pass's cache kernel
       if (tid < p.b) p.drow[(size_t)row * p.b + tid] = ds[tid];
+      if (eend - ebeg <= p.flat_skip_deg) cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);
     } else {
       if (tid < p.b) p.own[(size_t)row * p.ldo + p.b0 + tid] -= ds[tid];
       cache_range<BT>(p, sm, ebeg, eend, nch, tid, team);

@@ -921,7 +921,8 @@ __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(Sweep
   const int* __restrict__ R = SWAP ? p.x_rows : p.side.rows;   // the run's (held) vector
   const int* __restrict__ C = SWAP ? p.x_cols : p.side.cols;   // the gathered vector
   const int* __restrict__ PS = SWAP ? p.x_pos : p.side.pos;
-  int cur = -1;
+  int cur = -1, cur_skip_row = -1;
+  bool cur_skip = false;
   float dv[4 * NQ];
 #pragma unroll
   for (int j = 0; j < 4 * NQ; ++j) dv[j] = 0.f;
@@ -938,7 +939,14 @@ __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(Sweep
       nrow = e < end ? __ldg(R + e) : -1;
       ncol = e < end ? __ldg(C + e) : 0;
     }
-    const bool live = row >= 0;
+    bool live = row >= 0;
+    if (!SWAP && p.flat_skip_deg > 0 && live) {   // rows whose solver updated their cache itself
+      if (row != cur_skip_row) {
+        cur_skip_row = row;
+        cur_skip = __ldg(p.side.ptr + row + 1) - __ldg(p.side.ptr + row) <= p.flat_skip_deg;
+      }
+      live = !cur_skip;
+    }
     float4 x[NQ];
     const float* xr = SWAP ? p.drow + (size_t)col * b : p.fixed + (size_t)col * p.ldf + p.fb0;
 #pragma unroll

@@ -8,9 +8,9 @@
 // s = D^-1/2, Y = X diag(s) and z = s * g = Y^T rho + s * p~:
 //     C = I + Y Y^T (n_r x n_r),  u = Y z,  v = C^-1 u,
 //     d = s * (z - Y^T v)                        (Woodbury)
-// -- an n_r x n_r factorisation instead of a b x b one.  (And X d = v: the
-// cache update of the row is v itself; here it is left to the pass's
-// entry-parallel cache pass, which applies X~ d for every row.)
+// -- an n_r x n_r factorisation instead of a b x b one.  And X d = v: the
+// row's cache update is v itself (yhat_k -= v_k, no gather); the pass's
+// entry-parallel cache kernel skips these rows.
 //
 // Thread t = g * NG + k <-> TMEM lane t <-> entry k of slot g (k < n_g <= NG).
 //   pass 1  per 16-column chunk of b: each thread loads its entry's 16 values
@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       const double sv = S[s * B + tid];
       p.drow[(size_t)r * B + tid] = (float)(sv * Z[s * B + tid] - sv * sv * (double)xv);
     }
+    if (valid && !FLAG[g]) p.cache[ebeg + k] -= ds[tid];   // X~ d~ = v: the row's cache update
     if (tid < G && trow[tid] >= 0 && FLAG[tid]) {   // non-finite pivot: the SIMT sweep redoes the row
       p.redo_rows[atomicAdd(p.redo_cnt, 1)] = trow[tid];
       atomicAdd(p.redo_total, 1ull);
