@@ -224,6 +224,7 @@ def run_ours(args, cfg_key):
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # NCCL's init lines (ranks, NVLS / NVLink) ...
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
     ds = dataset(shape)
@@ -706,6 +707,9 @@ def run_reference(args, cfg_key):
 
 
 def main():
+    # NCCL writes its log (and its version banner) to stdout unless told
+    # otherwise: stdout carries the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

@@ -247,6 +247,16 @@ int ials_epoch_host(ials_session* s, const ials_side* users, const ials_sched* u
  * pass over the model.  `staging` (device) holds ials_host64_staging_bytes.
  * Host buffers should be page-locked (cudaHostRegister) for the copies to
  * overlap; pageable buffers work but serialise. */
+/* Multi-GPU column-block exchange (one process per GPU, replicated W / H):
+ * after the all-gather of every rank's updated rows of X[:, b0:b0+b] into
+ * recv (rank r's rows bounds[r]..bounds[r+1] at recv + r * nmax * b, b floats
+ * per row), write the other ranks' rows into X and form the block's change
+ * delta (n_rows x b, new - old; old_local = this rank's pre-sweep rows).
+ * bounds: device array of world + 1 row offsets. */
+int ials_shard_apply_block(ials_session* s, const float* recv, int32_t nmax, const int32_t* bounds,
+                           int32_t world, int32_t rank, const float* old_local, float* X, int32_t ldx,
+                           int32_t b0, int32_t b, float* delta, int32_t n_rows, void* stream);
+
 /* Rotated user passes (b = 128, unit weights, no heavy user rows): per block
  * the eigendecomposition of G_pp, rows with <= 64 interactions solved through
  * their Woodbury systems (ials_rot.cuh, ials_sweep_wb.cuh).  Default on

@@ -77,6 +77,8 @@ SIGNATURES = {
                            c_i32, c_i32, c_i32, c_f, c_p, c_p, c_sz, c_p]),
     "ials_topk64": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
     "ials_scores": (c_i32, [c_p, c_p, c_i32, c_i32, c_p, c_i32, c_i32, c_i32, c_p, c_i32, c_p]),
+    "ials_shard_apply_block": (c_i32, [c_p, c_p, c_i32, c_p, c_i32, c_i32, c_p, c_p, c_i32, c_i32,
+                                       c_i32, c_p, c_i32, c_p]),
     "ials_set_rotation": (c_i32, [c_i32]),
     "ials_sym_eig": (c_i32, [c_p, c_i32, c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_p]),
     "ials_host_register": (c_i32, [c_p, c_sz]),

@@ -1380,6 +1380,22 @@ int ials_shard_projection(ials_session* s, const float* F, int32_t ldf, int32_t 
   return proj_tc(s, F, ldf, w.c, d, bb, w.sth, w.stl, alpha0, proj, st);
 }
 
+int ials_shard_apply_block(ials_session* s, const float* recv, int32_t nmax, const int32_t* bounds,
+                           int32_t world, int32_t rank, const float* old_local, float* X, int32_t ldx,
+                           int32_t b0, int32_t b, float* delta, int32_t n_rows, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (world < 1 || rank < 0 || rank >= world || nmax < 0 || b < 1 || b0 < 0 || ldx < b0 + b ||
+      n_rows < 0 || !recv || !bounds || !X || !delta)
+    return fail(s, IALS_E_INVALID, "shard_apply_block: bad arguments");
+  if (n_rows == 0) return IALS_OK;
+  const long long n = (long long)n_rows * b;
+  k_apply_block<<<(int)std::min<long long>((n + 255) / 256, 16LL * kNumSMs), 256, 0, S(stream)>>>(
+      recv, nmax, bounds, world, rank, old_local, X, ldx, b0, b, delta, n_rows);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
 // optional phase events: 0 start, 1 after the cache, then per block
 // (user Gramian, user pass, item Gramian, item pass) -> 2 + 4 * blocks
 // (per host thread: the Python mirror sets them around one ials_epoch call

@@ -543,4 +543,28 @@ __global__ void __launch_bounds__(256)
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[i] = s;
 }
+// Multi-GPU column-block exchange (distributed.py): recv holds every rank's
+// rows of the block X[:, b0:b0+b] after the all-gather, rank r's at
+// recv[r * nmax ..] (bounds[r]..bounds[r+1] global rows).  Per global row u:
+// delta[u] = new - old (old = the rank's own pre-sweep copy for its rows, the
+// replicated table for the others), and the remote rows are written into X.
+__global__ void __launch_bounds__(256)
+    k_apply_block(const float* __restrict__ recv, int nmax, const int* __restrict__ bounds, int world,
+                  int rank, const float* __restrict__ old_local, float* X, int ldx, int b0, int b,
+                  float* __restrict__ delta, int n_rows) {
+  const long long n = (long long)n_rows * b;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int u = (int)(i / b), c = (int)(i - (long long)u * b);
+    int r = 0;
+    while (r + 1 < world && u >= bounds[r + 1]) ++r;
+    const int lo = bounds[r];
+    const float v = recv[((long long)r * nmax + (u - lo)) * b + c];
+    float* x = X + (size_t)u * ldx + b0 + c;
+    const float old = (r == rank) ? old_local[(size_t)(u - lo) * b + c] : *x;
+    if (r != rank) *x = v;
+    delta[i] = v - old;
+  }
+}
+
 }  // namespace ials

@@ -230,6 +230,22 @@ class GpuOps:
                                           _ptr(ws), ws.numel(), self._stream())
         self.sess.check(rc, "side_pass")
 
+    def apply_block(self, recv, nmax, bounds, rank, old_local, X, b0, b):
+        """Remote rows of the gathered block into X, and the block's change
+        (n x b, new - old) for the other side's cache correction."""
+        from .engine import _ptr
+        if not hasattr(self, "_bounds") or self._bounds[0] != tuple(bounds):
+            flat = [lo for lo, _ in bounds] + [bounds[-1][1]]
+            self._bounds = (tuple(bounds),
+                            torch.tensor(flat, dtype=torch.int32, device=self.device))
+        n = X.shape[0]
+        delta = torch.empty((n, b), dtype=self.dtype, device=self.device)
+        rc = self.sess.lib.ials_shard_apply_block(
+            self.sess.handle, _ptr(recv), nmax, _ptr(self._bounds[1]), len(bounds), rank,
+            _ptr(old_local), _ptr(X), X.stride(0), b0, b, _ptr(delta), n, self._stream())
+        self.sess.check(rc, "shard_apply_block")
+        return delta
+
     def check(self):
         self.sess.raise_if_singular()
 
@@ -271,21 +287,39 @@ class ShardedTrainer:
             dist.all_reduce(t, group=self.group)
         return t
 
-    def _allgather_block(self, X, bounds, nmax, b0, b):
-        """All-gather rows [lo_r, hi_r) of the column block X[:, b0:b0+b]."""
+    def _start_exchange(self, X, bounds, nmax, b0, b):
+        """Start the all-gather of this rank's rows of X[:, b0:b0+b] (padded to
+        nmax rows per rank, one contiguous receive buffer); returns (work, recv)."""
         lo, hi = bounds[self.rank]
-        if self.world == 1:
-            return
-        send = torch.zeros((nmax, b), dtype=X.dtype, device=X.device)
+        key = (id(bounds), b)
+        bufs = self.__dict__.setdefault("_xbufs", {})
+        if key not in bufs:
+            send = torch.zeros((nmax, b), dtype=X.dtype, device=X.device)
+            recv = send if self.world == 1 else torch.empty((self.world * nmax, b), dtype=X.dtype,
+                                                            device=X.device)
+            bufs[key] = (send, recv)
+        send, recv = bufs[key]
         send[: hi - lo] = X[lo:hi, b0:b0 + b]
-        recv = [torch.empty_like(send) for _ in range(self.world)]
-        dist.all_gather(recv, send, group=self.group)
-        for r, (l, h) in enumerate(bounds):
-            if r != self.rank and h > l:
-                X[l:h, b0:b0 + b] = recv[r][: h - l]
+        work = None
+        if self.world > 1:
+            work = dist.all_gather_into_tensor(recv, send, group=self.group, async_op=True)
+        return work, recv
+
+    def _finish_exchange(self, work, recv, X, bounds, nmax, b0, b, old_local):
+        """Wait for the all-gather, write the other ranks' rows into X; the
+        block's change new - old for every row (n x b)."""
+        if work is not None:
+            work.wait()
+        return self.ops.apply_block(recv, nmax, bounds, self.rank, old_local, X, b0, b)
 
     # ---------------------------------------------------------------- epoch
     def epoch(self, block_size):
+        """Per block: the user pass on the local users, the all-gather of their
+        new W[:, pi] rows overlapped with the partial item-side slab, the item
+        pass, the all-gather of H[:, pi] overlapped with the next block's
+        partial user-side slab.  Only the local rows are copied before a sweep
+        (the change of a remote row is formed while its new values land), so
+        no full-table pass remains per block."""
         W, H, ops = self.W, self.H, self.ops
         d = W.shape[1]
         ulo, uhi = self.user_bounds[self.rank]
@@ -297,23 +331,28 @@ class ShardedTrainer:
         ops.predictions(self.us, Wl, H, self.Cu)
         ops.predictions(self.is_, Hl, W, self.Ci)
         prev = None        # (b0, b, dH) of the last item pass
+        g_h = ops.gram(Hl, 0, min(block_size, d))
         for b0 in range(0, d, block_size):
             b = min(block_size, d - b0)
             # ---- user pass
             if prev is not None:
                 ops.correct(self.us, Wl, prev[0], prev[2], self.Cu)
-            slab = self._allreduce(ops.gram(Hl, b0, b))
-            w_old = W[:, b0:b0 + b].clone()
+            slab = self._allreduce(g_h)
+            w_old = Wl[:, b0:b0 + b].clone()          # local rows only
             ops.sweep(self.us, H, Wl, b0, b, slab, self.alpha0, self.Cu, 0)
-            self._allgather_block(W, self.user_bounds, self._umax, b0, b)
-            dW = W[:, b0:b0 + b] - w_old
+            work, recv = self._start_exchange(W, self.user_bounds, self._umax, b0, b)
+            g_w = ops.gram(Wl, b0, b)                  # overlaps the all-gather
+            dW = self._finish_exchange(work, recv, W, self.user_bounds, self._umax, b0, b, w_old)
             # ---- item pass
             ops.correct(self.is_, Hl, b0, dW, self.Ci)
-            slab = self._allreduce(ops.gram(Wl, b0, b))
-            h_old = H[:, b0:b0 + b].clone()
+            slab = self._allreduce(g_w)
+            h_old = Hl[:, b0:b0 + b].clone()
             ops.sweep(self.is_, W, Hl, b0, b, slab, self.alpha0, self.Ci, 1)
-            self._allgather_block(H, self.item_bounds, self._imax, b0, b)
-            prev = (b0, b, H[:, b0:b0 + b] - h_old)
+            work, recv = self._start_exchange(H, self.item_bounds, self._imax, b0, b)
+            if b0 + b < d:                             # the next block's slab partial, overlapped
+                g_h = ops.gram(Hl, b0 + b, min(block_size, d - b0 - b))
+            dH = self._finish_exchange(work, recv, H, self.item_bounds, self._imax, b0, b, h_old)
+            prev = (b0, b, dH)
         # bring C_u up to date with the last item pass
         if prev is not None:
             ops.correct(self.us, Wl, prev[0], prev[2], self.Cu)

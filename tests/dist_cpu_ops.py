@@ -41,3 +41,14 @@ class CpuOps:
 
     def check(self):
         pass
+
+    def apply_block(self, recv, nmax, bounds, rank, old_local, X, b0, b):
+        delta = torch.empty((X.shape[0], b), dtype=X.dtype)
+        for r, (lo, hi) in enumerate(bounds):
+            new = recv[r * nmax: r * nmax + (hi - lo)]
+            old = old_local if r == rank else X[lo:hi, b0:b0 + b].clone()
+            if r != rank:
+                X[lo:hi, b0:b0 + b] = new
+            delta[lo:hi] = new - old
+        return delta
+
