@@ -49,6 +49,15 @@ IALS_DEVI float group_sum(float v) {   // sum over aligned groups of G lanes
   return v;
 }
 
+// 32-byte read-only global load (LDG.E.256 on sm_100): one L1 wavefront per
+// 32 B of a scattered row instead of two 16-byte loads; p 32-byte aligned
+IALS_DEVI void ldg256(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+                 "=f"(v[7])
+               : "l"(p));
+}
+
 // Singular-row report: min over (side, row), first failing pivot of that row.
 IALS_DEVI void report_singular(unsigned long long* err, int side, int row, int pivot) {
   unsigned long long key = (static_cast<unsigned long long>(side) << 62) |

@@ -200,12 +200,19 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     __syncthreads();   // S, Z visible; TMEM initialised
     // ---- pass 1: C += Y_c Y_c^T, Y^T rho
     float x[16], xn[16];
-    auto load16 = [&](float (&v)[16], int c0) {
+    auto load16 = [&](float (&v)[16], int c0) {   // two 32-byte loads (rows are 512 B aligned)
+      float a[8], b8[8];
+      if (valid) {
+        ldg256(xr + c0, a);
+        ldg256(xr + c0 + 8, b8);
+      } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 t4 = valid ? __ldg(reinterpret_cast<const float4*>(xr + c0) + q)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[4 * q] = t4.x; v[4 * q + 1] = t4.y; v[4 * q + 2] = t4.z; v[4 * q + 3] = t4.w;
+        for (int j = 0; j < 8; ++j) a[j] = b8[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = a[j];
+        v[8 + j] = b8[j];
       }
     };
     load16(x, 0);

@@ -8,7 +8,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+extra = sys.argv[3:]
+out = subprocess.run(["ncu", "-i", rep, *extra, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
