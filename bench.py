@@ -48,8 +48,16 @@ ALPHA0, REG, NU, SIGMA = 0.1, 1e-3, 1.0, 0.1
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # FP32 FFMA peak: tools/microbench.cu on this pool's B200 (MEASURED_PEAKS.json has no FP32 figure)
-FP32_PEAK_TFLOPS = 64.5
-FP32_NOMINAL_TFLOPS = 74.4   # 148 SM x 128 lanes x 2 x 1.965 GHz
+# FP32 peak: nominal 148 SM x 128 lanes x 2 FLOP x the SM clock measured under
+# load during the timed region (74.4 TFLOP/s at 1965 MHz); MEASURED_PEAKS.json
+# has no FP32 figure.  The FFMA microbenchmark (tools/microbench.cu) reaches
+# 64.5 TFLOP/s on this pool's B200s -- reported beside it, not used as the peak.
+FP32_FFMA_MEASURED_TFLOPS = 64.5
+FP32_NOMINAL_TFLOPS = 74.4   # at 1965 MHz
+
+
+def fp32_peak_tflops(sm_mhz):
+    return 148 * 128 * 2 * (sm_mhz or 1965.0) * 1e6 / 1e12
 
 
 def load_peaks():
@@ -190,28 +198,6 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------- ours
-def epoch_launches(d, b, spans, su, si):
-    """Kernel launches of one ials_epoch call, mirroring its dispatch
-    (csrc/ials_abi.cu: ials_epoch, side_pass_impl, launch_sweep_tc4)."""
-    tc = 64 < b <= 128 and d % 4 == 0   # tensor-core GEMMs + fused sweep
-    n = 1                                # prediction cache
-    if tc:
-        n += 2                           # K-major copies of W and H
-    for _b0, bb in spans:
-        for sch in (su, si):
-            if tc:
-                n += 3 + 1               # Gramian GEMM + split reduce + projection GEMM; copy sync
-            else:
-                n += 2 + 1               # slab partials + reduce; projection
-            if tc and 64 < bb <= 128:
-                n += (2 if sch.n_light else 0) + (2 if sch.n_heavy else 0)
-                n += 1 if (sch.n_light or sch.n_heavy) else 0      # SIMT redo sweep
-                n += 1 if (sch.n_light or sch.n_slices) else 0     # cache pass
-            else:
-                n += (1 if sch.n_light else 0) + (3 if sch.n_heavy else 0)
-    return n
-
-
 def run_ours(args, cfg_key):
     import torch
 
@@ -310,12 +296,15 @@ def run_ours(args, cfg_key):
     value = updates * world / (ms_step / 1e3)
 
     hbm, hbm_src = load_peaks()
-    rl = roofline_model(U, I, S, d, b, FP32_PEAK_TFLOPS, hbm)
+    clocks = clk.summary()
+    p32 = fp32_peak_tflops(clocks.get("sm_mhz"))
+    rl = roofline_model(U, I, S, d, b, p32, hbm)
     sweep_ms = (ph["user"] + ph["item"]) / args.steps
     if rl["sweep_bound"] == "fp32":
         achieved = rl["F_sw"] / (sweep_ms / 1e3) / 1e12
-        roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": FP32_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TFLOPS, 4)}
+        roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(p32, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / p32, 4),
+                "frac_of_measured_ffma": round(achieved / FP32_FFMA_MEASURED_TFLOPS, 4)}
     else:
         achieved = rl["Q_sw"] / (sweep_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -330,13 +319,13 @@ def run_ours(args, cfg_key):
                   "k_pass_cache; else k_sweep_light + k_heavy_*)",
         "per_launch_algorithmic": (rl["F_sw"] if roof["unit"] == "TFLOP/s" else rl["Q_sw"]) / (2 * rl["B"]),
         "avg_launch_ms": round(sweep_ms / (2 * rl["B"]), 4),
-        "peak_source": "tools/microbench.cu FFMA (measured, this pool)" if roof["bound"] == "fp32" else hbm_src,
+        "peak_source": ("nominal FP32 (148 SM x 128 x 2 x measured SM clock; MEASURED_PEAKS.json has "
+                        "no FP32 figure)") if roof["bound"] == "fp32" else hbm_src,
         "sweep_share_of_step": round(sweep_ms / ms_step, 4),
         "epoch_roofline_ms": round(rl["t_epoch"] * 1e3, 3),
         "epoch_frac_of_roofline": round(rl["t_epoch"] * 1e3 / ms_step, 4),
         "sweep_roofline_ms": round(rl["t_sw"] * 1e3, 3),
     })
-    launches_per_epoch = epoch_launches(d, b, spans, su, si)
 
     # ---- e2e through the C-ABI epoch call with host (pinned) buffers
     e2e = None
@@ -420,9 +409,8 @@ def run_ours(args, cfg_key):
             "e2e": e2e_api if e2e_api is not None else e2e,
             "e2e_cabi": e2e,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "gpu_launches": n_launches,
-            "gpu_launches_model": launches_per_epoch * args.steps,
             # rows the fused tensor-core sweep's cancellation guard handed to the
             # FP32 sweep during the timed epochs (numerics transparency)
             "tc_redo_rows": tc_redo,
@@ -508,7 +496,7 @@ def run_sharded(args, cfg_key, ds, dev, rank, world):
                "path": "per rank: full W/H from pinned host, sharded epoch, local rows + C_u back"}
     if rank == 0:
         hbm, _ = load_peaks()
-        rl = roofline_model(U, I, S, d, b, FP32_PEAK_TFLOPS, hbm)
+        rl = roofline_model(U, I, S, d, b, FP32_NOMINAL_TFLOPS, hbm)
         print(json.dumps({
             "metric": "ialspp_epoch_nnz_d_updates_per_s", "value": value, "unit": "nnz*d/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -80,22 +80,6 @@ typedef struct ials_sched {
   const int32_t* slice_heavy;   /* [n_slices] heavy index of each slice        */
   const int32_t* slice_begin;   /* [n_slices] absolute entry range             */
   const int32_t* slice_end;     /* [n_slices]                                  */
-  /* Tensor-core plan (block widths 33..128, used when tensor cores are on):
-   * every row (descending degree) cut into slices; rows are processed in
-   * waves.  Device arrays except the two wave tables, which are HOST arrays
-   * of n_waves + 1 entries.  tc_n_rows == 0 disables the tensor-core path. */
-  int32_t tc_n_rows;
-  const int32_t* tc_rows;        /* [tc_n_rows]                                 */
-  const int32_t* tc_row_slice0;  /* [tc_n_rows + 1]                             */
-  int32_t tc_n_slices;
-  const int32_t* tc_slice_row;   /* [tc_n_slices] index into tc_rows            */
-  const int32_t* tc_slice_begin; /* [tc_n_slices]                               */
-  const int32_t* tc_slice_end;   /* [tc_n_slices]                               */
-  int32_t tc_n_waves;
-  const int32_t* tc_wave_row0;   /* HOST [tc_n_waves + 1]                       */
-  const int32_t* tc_wave_slice0; /* HOST [tc_n_waves + 1]                       */
-  int32_t tc_max_wave_rows;
-  int32_t tc_max_wave_slices;
   /* light rows (descending degree) with more than 64 / 32 interactions: the
    * prefix lengths that split the rotated user pass between the b x b sweep
    * and the Woodbury tiles of 2 and 4 rows */
@@ -143,13 +127,10 @@ int64_t ials_heavy_threshold(int32_t b);
 /* Slice length (entries) of heavy rows for block width b. */
 int64_t ials_slice_len(int32_t b);
 
-/* Bytes of scratch ials_side_pass / ials_partial_gramian / ials_epoch need
- * (SIMT schedules).  Add ials_tc_workspace_bytes for the tensor-core plan. */
+/* Bytes of scratch ials_side_pass / ials_partial_gramian / ials_epoch need. */
 size_t ials_workspace_bytes(int32_t n_rows_max, int32_t n_fixed_max, int32_t d, int32_t b,
                             int32_t n_slices_max, int32_t n_heavy_max);
-size_t ials_tc_workspace_bytes(int32_t max_wave_rows, int32_t max_wave_slices);
-/* Slices per tensor-core wave the plan should target (L2-resident partials). */
-int32_t ials_tc_wave_slices(void);
+
 
 /* out[e] = <W[user of e], H[col e]> for the user-major CSR (ptr, cols). */
 int ials_predictions(ials_session* s, int32_t n_rows, const int32_t* ptr, const int32_t* cols,

@@ -31,15 +31,11 @@ class IalsSide(ctypes.Structure):
 
 
 class IalsSched(ctypes.Structure):
-    """``ials_sched`` (light / heavy row schedule of one side + tensor-core plan)."""
+    """``ials_sched`` (light / heavy row schedule of one side)."""
     _fields_ = [("n_light", c_i32), ("light_rows", c_p), ("n_heavy", c_i32),
                 ("heavy_rows", c_p), ("heavy_slice0", c_p), ("n_slices", c_i32),
                 ("slice_heavy", c_p), ("slice_begin", c_p), ("slice_end", c_p),
-                ("tc_n_rows", c_i32), ("tc_rows", c_p), ("tc_row_slice0", c_p),
-                ("tc_n_slices", c_i32), ("tc_slice_row", c_p), ("tc_slice_begin", c_p),
-                ("tc_slice_end", c_p), ("tc_n_waves", c_i32), ("tc_wave_row0", c_p),
-                ("tc_wave_slice0", c_p), ("tc_max_wave_rows", c_i32),
-                ("tc_max_wave_slices", c_i32), ("n_deg_gt64", c_i32), ("n_deg_gt32", c_i32)]
+                ("n_deg_gt64", c_i32), ("n_deg_gt32", c_i32)]
 
 
 #: every symbol include/ials_b200.h declares, with its ctypes signature
@@ -58,8 +54,6 @@ SIGNATURES = {
     "ials_heavy_threshold": (c_i64, [c_i32]),
     "ials_slice_len": (c_i64, [c_i32]),
     "ials_workspace_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
-    "ials_tc_workspace_bytes": (c_sz, [c_i32, c_i32]),
-    "ials_tc_wave_slices": (c_i32, []),
     "ials_epoch_tc_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32]),
     "ials_epoch_events": (c_i32, [ctypes.POINTER(c_p), c_i32]),
     "ials_predictions": (c_i32, [c_p, c_i32, c_p, c_p, c_p, c_i32, c_p, c_i32, c_i32, c_p, c_p]),

@@ -20,8 +20,6 @@
 #include "ials_topk.cuh"
 #include "ials_sweep.cuh"
 #include "ials_loss.cuh"
-#include "ials_sweep_tc.cuh"
-#include "ials_sweep_tc2.cuh"
 #include "ials_sweep_tc4.cuh"
 #include "ials_sweep_pk.cuh"
 #include "ials_rot.cuh"
@@ -243,13 +241,7 @@ static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
   return al256(std::max(size_t(kMaxSplits) * d * b, narrow) * sizeof(float));
 }
 
-size_t ials_tc_workspace_bytes(int32_t max_wave_rows, int32_t max_wave_slices) {
-  return al256(size_t(max_wave_slices) * kTcPKS * 4) + al256(size_t(max_wave_slices) * 128 * 8) +
-         al256(size_t(max_wave_rows) * 128 * 4) + al256(size_t(kTcPKS) * 4);
-}
 
-// 1024 partial Hessians (35 MB) stay L2-resident between k_tc_hess and k_tc_factor
-int32_t ials_tc_wave_slices(void) { return 1024; }
 
 // narrow blocks gather from a compact copy of the fixed side's column block
 // (n_fixed x ldc): L2-resident, unlike the full d-wide rows
@@ -513,13 +505,15 @@ int ials_debug_timestamps(void* dev_buf) {
 }
 
 static int g_tc = -1;  // -1: not yet read from IALS_TC
-static bool tc_enabled() {
+// 2 (default): the fused tensor-core sweeps for b in 17..128; 0: the FP32
+// SIMT sweep everywhere (IALS_TC=0).  (The round-1 mode 1 -- three kernels per
+// wave of rows -- was slower than the fused sweep and is gone; 1 means 2.)
+static bool tc4_enabled() {
   if (g_tc < 0) {
     const char* e = getenv("IALS_TC");
-    // default: the fused tensor-core sweep (mode 2) for b in 33..128
-    g_tc = (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 2;
+    g_tc = (e && e[0] == '0') ? 0 : 2;
   }
-  return g_tc == 1;
+  return g_tc == 2;
 }
 static float g_cond = 0.f;
 static float tc_cond_max() {
@@ -536,15 +530,10 @@ float ials_set_tc_cond_max(float v) {
   if (v > 1.f) g_cond = v;
   return prev;
 }
-static bool tc4_enabled() {
-  tc_enabled();
-  return g_tc == 2;
-}
-
 int ials_set_tensor_cores(int enable) {
-  tc_enabled();
+  tc4_enabled();
   const int prev = g_tc;
-  g_tc = (enable == 1 || enable == 2) ? enable : 0;
+  g_tc = enable ? 2 : 0;
   return prev;
 }
 
@@ -771,114 +760,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   return IALS_OK;
 }
 
-// BT = 128 on the tensor core: light rows fused (k_sweep_tc128), heavy-row
-// partial Hessians on the tensor core, their solve / cache update on SIMT.
-static int launch_sweep_tc128(ials_session* s, const SweepParams& p, cudaStream_t st) {
-  using L = Lay<128>;
-  int rc = set_smem_attrs<128>(s);
-  if (rc) return rc;
-  static int per_sm = 0;
-  static unsigned per_dev = 0;
-  if (!(per_dev & dev_bit())) {
-    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc128, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     TcLay::BYTES));
-    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc128,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, TcLay::BYTES));
-    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_tc128, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     100));
-    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_tc128,
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    // residency from the kernel's real resources (the occupancy API has been
-    // seen to under-report here): shared memory, registers, TMEM columns
-    cudaFuncAttributes fa;
-    CUDA_TRY(s, cudaFuncGetAttributes(&fa, k_sweep_tc128));
-    int dev = 0;
-    CUDA_TRY(s, cudaGetDevice(&dev));
-    int smem_sm = 0, regs_sm = 0;
-    CUDA_TRY(s, cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    CUDA_TRY(s, cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-    const int by_smem = smem_sm / (TcLay::BYTES + 1024);
-    const int by_regs = regs_sm / (((fa.numRegs + 7) / 8) * 8 * 128);
-    per_sm = std::max(1, std::min(std::min(by_smem, by_regs), 4));
-    per_dev |= dev_bit();
-  }
-  if (p.n_light > 0) {
-    const int grid = std::min(p.n_light, per_sm * kNumSMs);
-    k_sweep_tc128<<<grid, 128, TcLay::BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-  }
-  if (p.n_heavy > 0) {
-    const int grid = std::min(p.n_slices, per_sm * kNumSMs);
-    k_heavy_partial_tc128<<<grid, 128, TcLay::BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-    const int threads = L::NT * L::RPC;
-    k_heavy_solve<128><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-    k_heavy_cache<128><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-  }
-  return IALS_OK;
-}
-
-// residency of a 128-thread tensor-core kernel from its real resources
-template <typename K>
-static int tc_per_sm(ials_session* s, K kernel, int bytes, int* out) {
-  CUDA_TRY(s, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(s, cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  cudaFuncAttributes fa;
-  CUDA_TRY(s, cudaFuncGetAttributes(&fa, kernel));
-  int dev = 0, smem_sm = 0, regs_sm = 0;
-  CUDA_TRY(s, cudaGetDevice(&dev));
-  CUDA_TRY(s, cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-  CUDA_TRY(s, cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-  const int by_smem = smem_sm / (bytes + 1024);
-  const int by_regs = regs_sm / (((fa.numRegs + 7) / 8) * 8 * 128);
-  *out = std::max(1, std::min(std::min(by_smem, by_regs), 32));
-  return IALS_OK;
-}
-
-static int launch_tc_waves(ials_session* s, SweepParams p, const ials_sched* sched,
-                           cudaStream_t st) {
-  static int h_sm = 0, f_sm = 0, c_sm = 0;
-  static unsigned per_dev = 0;
-  if (!(per_dev & dev_bit())) {
-    int rc = tc_per_sm(s, k_tc_hess, TcLayH::BYTES, &h_sm);
-    if (!rc) rc = tc_per_sm(s, k_tc_factor, TcLayF::BYTES, &f_sm);
-    if (!rc) rc = tc_per_sm(s, k_tc_cache, TcLayC::BYTES, &c_sm);
-    if (rc) return rc;
-    h_sm = std::min(h_sm, 4);  // TMEM: 128 columns per CTA
-    f_sm = std::min(f_sm, 4);
-    if (const char* e = getenv("IALS_TC_FSM")) f_sm = std::max(1, std::min(f_sm, atoi(e)));
-    if (const char* e = getenv("IALS_TC_HSM")) h_sm = std::max(1, std::min(h_sm, atoi(e)));
-    per_dev |= dev_bit();
-  }
-  k_tc_template<<<128, 128, 0, st>>>(p, const_cast<float*>(p.tpl));
-  LAUNCH_CHECK(s);
-  for (int w = 0; w < sched->tc_n_waves; ++w) {
-    p.w_r0 = sched->tc_wave_row0[w];
-    p.w_r1 = sched->tc_wave_row0[w + 1];
-    p.w_s0 = sched->tc_wave_slice0[w];
-    p.w_s1 = sched->tc_wave_slice0[w + 1];
-    const int ns = p.w_s1 - p.w_s0, nr = p.w_r1 - p.w_r0;
-    if (nr <= 0) continue;
-    if (ns > 0) {
-      k_tc_hess<<<std::min(ns, h_sm * kNumSMs), 128, TcLayH::BYTES, st>>>(p);
-      LAUNCH_CHECK(s);
-    }
-    k_tc_factor<<<std::min(nr, f_sm * kNumSMs), 128, TcLayF::BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-    if (ns > 0) {
-      k_tc_cache<<<std::min(ns, c_sm * kNumSMs), 128, TcLayC::BYTES, st>>>(p);
-      LAUNCH_CHECK(s);
-    }
-  }
-  return IALS_OK;
-}
-
 template <int BT>
 static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<BT>;
-  if (BT == 128 && p.b > 32 && tc_enabled()) return launch_sweep_tc128(s, p, st);
   if (BT == 128 && p.b > 16 && tc4_enabled()) return launch_sweep_tc4(s, p, nnz, st);
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
@@ -944,11 +828,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
     return fail(s, IALS_E_INVALID, "side_pass: bad block (d=%d b0=%d b=%d)", d, b0, b);
   const int bt = block_tile(b);
-  const bool use_tc = bt == 128 && b > 32 && tc_enabled() && sched->tc_n_rows > 0;
-  const size_t need_simt = pass_ws(side->n_rows, side->n_fixed, b, sched->n_slices, sched->n_heavy);
-  const size_t need_tc = al256(size_t(side->n_rows) * b * 4) +
-                         ials_tc_workspace_bytes(sched->tc_max_wave_rows, sched->tc_max_wave_slices);
-  const size_t need = use_tc ? need_tc : need_simt;
+  const size_t need = pass_ws(side->n_rows, side->n_fixed, b, sched->n_slices, sched->n_heavy);
   if (need > ws_bytes)
     return fail(s, IALS_E_NOMEM, "side_pass: workspace %zu < %zu bytes", ws_bytes, need);
   SweepParams p{};
@@ -995,7 +875,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   w += al256(size_t(side->n_rows) * 4 + 32);
   p.drow = reinterpret_cast<float*>(w);
   w += al256(size_t(side->n_rows) * b * 4);
-  if (b <= kCompactMaxB && !use_tc && side->n_fixed > 0) {
+  if (b <= kCompactMaxB && side->n_fixed > 0) {
     // gather from a compact, L2-resident copy of fixed[:, b0:b0+b]
     const int ldc = compact_ld(b);
     float* compact = reinterpret_cast<float*>(w);
@@ -1022,9 +902,15 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     p.slab = rot->rslab;
     p.wq = rot->wq;
     p.rot_lam = rot->lam;
-    p.rot_n64 = sched->n_deg_gt64;
-    p.rot_n32 = sched->n_deg_gt32;
-    p.flat_skip_deg = 64;   // the Woodbury tiles update their rows' cache themselves
+    static const bool wb_off = getenv("IALS_WB") && getenv("IALS_WB")[0] == '0';   // (diagnostics)
+    p.rot_n64 = wb_off ? sched->n_light : sched->n_deg_gt64;
+    p.rot_n32 = wb_off ? sched->n_light : sched->n_deg_gt32;
+    // the Woodbury tiles update their rows' cache themselves (yhat -= v) when
+    // the pass's cache kernel walks this side's order and can skip their
+    // rows; when it walks the other side's order (this side the smaller) it
+    // updates every entry and the tiles leave the cache alone
+    const bool walks_other = other && other->rows && other->cols && side->n_rows < side->n_fixed;
+    p.flat_skip_deg = walks_other ? 0 : 64;
   }
   if (other && other->rows && other->cols && other->nnz == side->nnz) {   // same entries, other order
     p.x_rows = other->rows;
@@ -1041,28 +927,8 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     proj_ready = true;
   }
   p.proj = proj;
-  p.tc_rows = sched->tc_rows;
-  p.tc_row_slice0 = sched->tc_row_slice0;
-  p.tc_slice_row = sched->tc_slice_row;
-  p.tc_slice_beg = sched->tc_slice_begin;
-  p.tc_slice_end = sched->tc_slice_end;
-  p.w_r0 = p.w_r1 = p.w_s0 = p.w_s1 = 0;
   p.dbg = g_dbg;
-  if (use_tc) {  // tensor-core scratch follows proj
-    char* t = ws + al256(size_t(side->n_rows) * b * 4);
-    p.hbuf = reinterpret_cast<float*>(t);
-    t += al256(size_t(sched->tc_max_wave_slices) * kTcPKS * 4);
-    p.gbuf = reinterpret_cast<double*>(t);
-    t += al256(size_t(sched->tc_max_wave_slices) * 128 * 8);
-    p.dbuf = reinterpret_cast<float*>(t);
-    t += al256(size_t(sched->tc_max_wave_rows) * 128 * 4);
-    p.tpl = reinterpret_cast<const float*>(t);
-  } else {
-    p.tpl = tpl_simt;
-    p.hbuf = nullptr;
-    p.gbuf = nullptr;
-    p.dbuf = nullptr;
-  }
+  p.tpl = tpl_simt;
   if (side->n_rows > 0 && !proj_ready) {
     if (b <= 4) {
       const int g = (side->n_rows + 7) / 8;
@@ -1082,7 +948,6 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     }
     LAUNCH_CHECK(s);
   }
-  if (use_tc) return launch_tc_waves(s, p, sched, st);
   if (b == 1) {  // scalar blocks: the iCD special case
     if (p.n_light > 0) {
       k_sweep_b1<<<std::min((p.n_light + 7) / 8, kNumSMs * 16), 256, 0, st>>>(p);
@@ -1618,18 +1483,20 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   const size_t pass_need =
       std::max(pass_ws(users->n_rows, users->n_fixed, b, user_sched->n_slices, user_sched->n_heavy),
                pass_ws(items->n_rows, items->n_fixed, b, item_sched->n_slices, item_sched->n_heavy));
+  // the tensor-core region starts at the first 1 KB-aligned address at or
+  // above ws + ws_bytes - tcb (tcb reserves the 1 KB this rounding can take),
+  // so the pass scratch below it keeps all of ws_bytes - tcb
+  char* tc_start = reinterpret_cast<char*>(
+      (reinterpret_cast<uintptr_t>(ws) + (ws_bytes - std::min(tcb, ws_bytes)) + 1023) & ~uintptr_t(1023));
   const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 16 && d % 4 == 0 &&
                        ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= tcb &&
-                       // the pass scratch left below the 1 KB-aligned carve start
-                       (long long)(((ws_bytes - tcb) & ~size_t(1023)) - (slab_bytes + gbytes)) >=
-                           (long long)pass_need &&
-                       get_encode(s) == IALS_OK;
+                       tc_start - pws >= (long long)pass_need && get_encode(s) == IALS_OK;
   TcCopies cw{}, ch{};
   float *P = nullptr, *sth = nullptr, *stl = nullptr;
   RotWs rw{};
   if (tc_gemm) {
-    char* t = ws + ((ws_bytes - tcb) & ~size_t(1023));
+    char* t = tc_start;
     pbytes = size_t(t - pws);
     t = carve_copies(t, users->n_rows, d, &cw);
     t = carve_copies(t, items->n_rows, d, &ch);

@@ -14,9 +14,10 @@
 // Frobenius norm below 1e-6 of the matrix norm or 20 sweeps.  Outputs Q^T
 // (row j = eigenvector j), the eigenvalues, and the rotated block template
 // (diag(L) at rows b0.. of a d x b buffer: what the sweep kernels read as
-// slab[pi, pi]).  The exactness argument does not need Q to be orthogonal to
-// full precision: the sweep uses the same Q for X~, g~ and d = Q d~, so only
-// the dropped off-diagonal part of Q^T A Q (~ 2^-23 |A|) perturbs the solve.
+// slab[pi, pi]).  The sweep uses the same Q for X~, g~ and d = Q d~; what
+// perturbs the solve is the dropped off-diagonal part of Q^T G Q (~1e-6 of |G|)
+// and Q^T Q - I in the lam I term, which two Newton-Schulz steps keep at fp32
+// level.
 #pragma once
 #include "ials_common.cuh"
 
@@ -144,6 +145,59 @@ __global__ void __launch_bounds__(kEigThreads, 1)
       __syncthreads();
     }
   }
+  // The accumulated rotations drift from orthogonality (~5e-4 in |V^T V - I|_F
+  // after a cold decomposition) and the solve needs Q^T Q = I for the lam I
+  // term of every row's Hessian: two Newton-Schulz steps V <- V (3I - V^T V)/2
+  // bring V back to fp32 orthogonality (the error squares each step).  A's
+  // storage holds V^T V, then G again for the final eigenvalues.
+  __shared__ float evals[256];
+  for (int it = 0; it < 2; ++it) {
+    // T = (3 I - V^T V) / 2 -> A's storage
+    for (int i = tid; i < n * n; i += kEigThreads) {
+      const int r = i / n, c = i - r * n;
+      float acc = 0.f;
+      for (int k = 0; k < n; ++k) acc = fmaf(V[k * ld + r], V[k * ld + c], acc);
+      A[r * ld + c] = ((r == c) ? 1.5f : 0.f) - 0.5f * acc;
+    }
+    __syncthreads();
+    // V <- V T, row by row: every output of a row is formed before the row is rewritten
+    for (int r0 = 0; r0 < n; r0 += kEigThreads / n) {
+      const int r = r0 + tid / n, c = tid % n;
+      float acc = 0.f;
+      if (r < n)
+        for (int k = 0; k < n; ++k) acc = fmaf(V[r * ld + k], A[k * ld + c], acc);
+      __syncthreads();
+      if (r < n) V[r * ld + c] = acc;
+      __syncthreads();
+    }
+  }
+  // the eigenvalues of the final basis: diag(V^T G V), G reloaded (symmetrised)
+  // into A's storage; thread t sums the rows r = t / n (mod 4 parts) of column t % n
+  for (int i = tid; i < n * n; i += kEigThreads) {
+    const int r = i / n, c = i - r * n;
+    A[r * ld + c] = 0.5f * (g[(size_t)r * ldg + c] + g[(size_t)c * ldg + r]);
+  }
+  __syncthreads();
+  {
+    constexpr int PARTS = kEigThreads / 128;
+    __shared__ float epart[kEigThreads];
+    const int i = tid % n, part = tid / n;
+    float acc = 0.f;
+    if (tid < n * PARTS)
+      for (int r = part; r < n; r += PARTS) {
+        float gv = 0.f;
+        for (int c = 0; c < n; ++c) gv = fmaf(A[r * ld + c], V[c * ld + i], gv);
+        acc = fmaf(V[r * ld + i], gv, acc);
+      }
+    epart[tid] = acc;
+    __syncthreads();
+    if (tid < n) {
+      float s = 0.f;
+      for (int q = 0; q < PARTS; ++q) s += epart[q * n + tid];
+      evals[tid] = s;
+    }
+    __syncthreads();
+  }
   float* qt = QT + (size_t)z * n * n;
   for (int i = tid; i < n * n; i += kEigThreads) {
     const int j = i / n, k = i - j * n;   // QT[j][k] = V[k][j]
@@ -153,12 +207,12 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     float* qm = Qm + (size_t)z * n * n;
     for (int i = tid; i < n * n; i += kEigThreads) qm[i] = V[(i / n) * ld + i % n];
   }
-  if (tid < n) lam[(size_t)z * n + tid] = A[tid * ld + tid];
+  if (tid < n) lam[(size_t)z * n + tid] = evals[tid];
   if (tpl) {
     float* tp = tpl + (size_t)z * n * n;   // rows b0 = z * b of the d x b template
     for (int i = tid; i < n * n; i += kEigThreads) {
       const int r = i / n, c = i - r * n;
-      tp[i] = (r == c) ? A[r * ld + r] : 0.f;
+      tp[i] = (r == c) ? evals[r] : 0.f;
     }
   }
 }

@@ -60,17 +60,6 @@ struct SweepParams {
   float* hpart;   // [n_slices][BT*BT]
   double* gpart;  // [n_slices][BT] (fp64: the gradient sum cancels strongly)
   float* hdelta;  // [n_heavy][BT]
-  // tensor-core wave plan (BT = 128): every row cut into slices, rows in
-  // descending degree; a wave is rows [w_r0, w_r1) = slices [w_s0, w_s1)
-  const int* tc_rows;
-  const int* tc_row_slice0;
-  const int* tc_slice_row;
-  const int* tc_slice_beg;
-  const int* tc_slice_end;
-  int w_r0, w_r1, w_s0, w_s1;
-  float* hbuf;    // [wave slices][8448] packed lower rows (4-aligned)
-  double* gbuf;   // [wave slices][128]
-  float* dbuf;    // [wave rows][128]
   long long* dbg; // optional per-CTA phase timestamps (profiling builds only)
   const float* tpl;  // [8448] packed alpha0 * slab[pi, pi] (tensor-core plan)
   // fused tensor-core sweep: rows whose Cholesky pivots cancel more than

@@ -20,7 +20,7 @@
 //      backward solve, W update and the cache update yhat -= X d
 // Shared memory ~55 KB and 128 TMEM columns per CTA -> 4 CTAs per SM.
 #pragma once
-#include "ials_sweep_tc2.cuh"
+#include "ials_tc_common.cuh"
 
 namespace ials {
 

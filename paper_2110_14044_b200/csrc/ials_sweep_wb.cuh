@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     load16(x, 0);
     uint32_t pend = 0;
     float uq = 0.f;   // y_k . (s p~) = x_k . (s^2 p~)
+    float yy = 0.f;   // |y_k|^2: (C - I)_kk, kept out of the TMEM diagonal 1 + |y_k|^2
     for (int ch = 0; ch < L::NCH; ++ch) {
       const int c0 = ch * L::KCH, ob = ch & 1;
       if (ch + 1 < L::NCH) load16(xn, c0 + L::KCH);
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       for (int j = 0; j < 16; ++j) {
         y[j] = x[j] * S[g * B + c0 + j];
         uq = fmaf(x[j], SZ[g * B + c0 + j], uq);
+        yy = fmaf(y[j], y[j], yy);
       }
       {
         float zr[16];
@@ -293,19 +295,21 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     const int task_next = *next;
     int nrow = -1;
     if (tid < G && task_next < n_tiles) nrow = tile_row(task_next, tid);
-    // u_k = y_k . (s p~) + sum_j (C - I)_kj rho_j over the slot's entries
+    // u_k = y_k . (s p~) + sum_j (C - I)_kj rho_j over the slot's entries; the
+    // diagonal term from |y_k|^2 itself (in TMEM it is 1 + |y_k|^2, whose
+    // rounding would lose |y_k|^2's low bits when the rows are small)
     {
       const float* RH = reinterpret_cast<const float*>(smem + L::OFF_RHO) + g * L::NG;
-      float cr = 0.f;
+      float cr = yy * rho;
 #pragma unroll
       for (int c32 = 0; c32 < L::NG; c32 += 32) {
         float cv[32];
         tmem_ld32(row_addr + g * L::NG + c32, cv);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) cr = fmaf(cv[j], RH[c32 + j], cr);
+        for (int j = 0; j < 32; ++j) cr = fmaf((c32 + j == k) ? 0.f : cv[j], RH[c32 + j], cr);
       }
-      ys[tid] = valid ? uq + (cr - rho) : 0.f;
+      ys[tid] = valid ? uq + cr : 0.f;
     }
     __syncthreads();
     // ---- v = C^-1 u on the leading nmax rows of every slot
@@ -342,7 +346,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       const double sv = S[s * B + tid];
       p.drow[(size_t)r * B + tid] = (float)(sv * Z[s * B + tid] - sv * sv * (double)xv);
     }
-    if (valid && !FLAG[g]) p.cache[ebeg + k] -= ds[tid];   // X~ d~ = v: the row's cache update
+    // X~ d~ = v: the row's cache update (unless the pass's cache kernel does it)
+    if (p.flat_skip_deg > 0 && valid && !FLAG[g]) p.cache[ebeg + k] -= ds[tid];
     if (tid < G && trow[tid] >= 0 && FLAG[tid]) {   // non-finite pivot: the SIMT sweep redoes the row
       p.redo_rows[atomicAdd(p.redo_cnt, 1)] = trow[tid];
       atomicAdd(p.redo_total, 1ull);

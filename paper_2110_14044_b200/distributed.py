@@ -203,8 +203,7 @@ class GpuOps:
         sch = ds.schedule(b)
         d = own_rows.shape[1]
         ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(
-            max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)) +
-            int(self.sess.lib.ials_tc_workspace_bytes(sch.tc_max_wave_rows, sch.tc_max_wave_slices)))
+            max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)))
         sh = self._shard(own_rows)
         if sh is not None and b <= sh[2] and own_rows.shape[0] > 0:
             # projection alpha0 * own @ slab on the tensor core, then the sweep

@@ -104,8 +104,6 @@ class Schedule:
     n_light: int
     n_heavy: int
     n_slices: int
-    tc_max_wave_rows: int = 0
-    tc_max_wave_slices: int = 0
 
 
 class DeviceSide:
@@ -151,69 +149,18 @@ class DeviceSide:
                              int(lib.ials_slice_len(b)))
         to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(self.device)
         t = {k: to(v) for k, v in plan.items()}
-        tc = {"n": 0}
-        if bt == 128:
-            tp = plan_tc(self.ptr.cpu().numpy(), int(lib.ials_slice_len(b)),
-                         int(lib.ials_tc_wave_slices()))
-            for k in ("rows", "row_slice0", "slice_row", "beg", "end"):
-                t["tc_" + k] = to(tp[k])
-            # host wave tables must outlive the struct
-            t["tc_wave_row0_h"] = np.ascontiguousarray(tp["wave_row0"], dtype=np.int32)
-            t["tc_wave_slice0_h"] = np.ascontiguousarray(tp["wave_slice0"], dtype=np.int32)
-            tc = {"n": int(tp["rows"].size), "ns": int(tp["beg"].size),
-                  "nw": int(tp["wave_row0"].size - 1), "mr": tp["max_wave_rows"],
-                  "ms": tp["max_wave_slices"]}
-        hp = lambda a: ctypes.c_void_p(a.ctypes.data)
         deg_light = self.counts[plan["light"]]   # descending: the counts are prefix lengths
         st = _lib.IalsSched(int(plan["light"].size), _ptr(t["light"]).value,
                             int(plan["heavy"].size), _ptr(t["heavy"]).value,
                             _ptr(t["slice0"]).value, int(plan["beg"].size),
                             _ptr(t["slice_heavy"]).value, _ptr(t["beg"]).value,
                             _ptr(t["end"]).value,
-                            tc["n"], _ptr(t.get("tc_rows")).value,
-                            _ptr(t.get("tc_row_slice0")).value, tc.get("ns", 0),
-                            _ptr(t.get("tc_slice_row")).value, _ptr(t.get("tc_beg")).value,
-                            _ptr(t.get("tc_end")).value, tc.get("nw", 0),
-                            hp(t["tc_wave_row0_h"]).value if tc["n"] else None,
-                            hp(t["tc_wave_slice0_h"]).value if tc["n"] else None,
-                            tc.get("mr", 0), tc.get("ms", 0),
                             int(np.count_nonzero(deg_light > 64)),
                             int(np.count_nonzero(deg_light > 32)))
         sch = Schedule(t, st, int(plan["light"].size), int(plan["heavy"].size),
-                       int(plan["beg"].size), tc.get("mr", 0), tc.get("ms", 0))
+                       int(plan["beg"].size))
         self._sched[bt] = sch
         return sch
-
-
-def plan_tc(ptr, slice_len: int, wave_slices: int) -> dict:
-    """Tensor-core plan of one side: all rows in descending degree, each cut
-    into ceil(n / slice_len) slices (one, possibly empty, for short rows);
-    waves of consecutive rows holding at most ``wave_slices`` slices (a row
-    with more slices gets a wave of its own)."""
-    ptr = np.asarray(ptr, dtype=np.int64)
-    counts = np.diff(ptr)
-    rows = np.argsort(-counts, kind="stable")
-    nsl = np.maximum(1, (counts[rows] + slice_len - 1) // slice_len)
-    row_slice0 = np.zeros(rows.size + 1, dtype=np.int64)
-    np.cumsum(nsl, out=row_slice0[1:])
-    slice_row = np.repeat(np.arange(rows.size), nsl)
-    within = np.arange(slice_row.size) - row_slice0[slice_row]
-    beg = ptr[rows][slice_row] + within * slice_len
-    end = np.minimum(beg + slice_len, ptr[rows + 1][slice_row])
-    w_rows = [0]
-    acc = 0
-    for r in range(rows.size):
-        if acc > 0 and acc + nsl[r] > wave_slices:
-            w_rows.append(r)
-            acc = 0
-        acc += int(nsl[r])
-    w_rows.append(int(rows.size))
-    wave_row0 = np.array(w_rows, dtype=np.int64)
-    wave_slice0 = row_slice0[wave_row0]
-    return {"rows": rows, "row_slice0": row_slice0, "slice_row": slice_row, "beg": beg,
-            "end": end, "wave_row0": wave_row0, "wave_slice0": wave_slice0,
-            "max_wave_rows": int(np.diff(wave_row0).max(initial=0)),
-            "max_wave_slices": int(np.diff(wave_slice0).max(initial=0))}
 
 
 def plan_schedule(ptr, heavy_threshold: int, slice_len: int) -> dict:
@@ -308,9 +255,6 @@ class Engine:
         need = int(self.lib.ials_workspace_bytes(
             max(self.p.num_users, 1), max(self.p.num_items, 1), d, b,
             max(sch_u.n_slices, sch_i.n_slices), max(sch_u.n_heavy, sch_i.n_heavy)))
-        need += int(self.lib.ials_tc_workspace_bytes(max(sch_u.tc_max_wave_rows, sch_i.tc_max_wave_rows),
-                                                      max(sch_u.tc_max_wave_slices,
-                                                          sch_i.tc_max_wave_slices)))
         # room for the epoch's tensor-core GEMM path (K-major factor copies)
         need += int(self.lib.ials_epoch_tc_bytes(max(self.p.num_users, 1),
                                                  max(self.p.num_items, 1), d, b))

@@ -185,7 +185,7 @@ def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
     got = {}
     prev = lib.ials_set_tensor_cores(0)
     try:
-        for tc in (1, 2, 0):
+        for tc in (2, 0):
             lib.ials_set_tensor_cores(tc)
             m = init.copy()
             ials.train(m, data, cfg)
@@ -195,11 +195,11 @@ def test_tensor_core_sweep_vs_oracle_and_simt(ials, d, b):
     w, h = init.user_factors.copy(), init.item_factors.copy()
     csr = orc.build_csr(U, I, users, items)
     orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
-    for tc in (1, 2, 0):
+    for tc in (2, 0):
         m = got[tc]
         assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL, tc
         assert relmax(m.user_factors, w) < TOL and relmax(m.item_factors, h) < TOL, tc
-    assert relf(got[1].user_factors, got[0].user_factors) < 1e-4
+    assert relf(got[2].user_factors, got[0].user_factors) < 1e-4
     assert relf(got[2].user_factors, got[0].user_factors) < 1e-4
 
 
@@ -444,10 +444,9 @@ def test_sym_eig_jacobi(ials):
         assert np.allclose(QT[z].double().cpu().numpy(), q.T)
         off = q.T @ a @ q - np.diag(lam[z].double().cpu().numpy())
         assert np.linalg.norm(off) <= 5e-6 * np.linalg.norm(a)
-        # the fp32 rotations drift from orthogonality (~5e-4 after a cold
-        # decomposition); the rotated solve does not need it -- it uses the
-        # same Q on both sides, only the residual above enters the Hessian
-        assert np.linalg.norm(q.T @ q - np.eye(128)) <= 3e-3
+        # the lam I term of the rotated Hessian needs Q^T Q = I: the Jacobi
+        # rotations' drift is removed by the Newton-Schulz steps
+        assert np.linalg.norm(q.T @ q - np.eye(128)) <= 2e-5
 
 
 @pytest.mark.parametrize("d", [128, 256])
