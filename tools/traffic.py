@@ -35,6 +35,8 @@ for d in L:
         continue
     if cur is None or "k_project" in n:   # in ials_epoch the projection is a GEMM of the Gramian phase
         continue
+    if "k_sym_eig" in n or "k_reduce_splits_strided" in n or "k_sync_copies" in n:
+        continue   # side-stream eigendecompositions / GEMM-copy upkeep: not part of a side pass
     cur["kernels"].append(n)
     cur["bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
     cur["seconds"] += d.get("gpu__time_duration.sum", 0)
