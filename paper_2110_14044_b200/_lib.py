@@ -13,6 +13,8 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libials_b200.so")
+if os.environ.get("IALS_LIB") == "checked":   # the bounds-checked build (build.py --checked)
+    LIB_PATH = os.path.join(HERE, "libials_b200_checked.so")
 
 IALS_OK = 0
 IALS_E_INVALID = -1

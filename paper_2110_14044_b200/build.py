@@ -11,6 +11,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libials_b200.so")
+# bounds-checked variant (-DIALS_CHECKS: device asserts on every index-driven
+# gather / scatter of the sweeps); loaded instead when IALS_LIB=checked
+OUT_CHECKED = os.path.join(HERE, "libials_b200_checked.so")
 SOURCES = ["ials_abi.cu"]
 DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
 
@@ -29,24 +32,26 @@ def nvcc():
     return "nvcc"
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+def up_to_date(out=OUT) -> bool:
+    if not os.path.exists(out):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     files = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(ROOT, "include", "ials_b200.h")]
     return all(os.path.getmtime(f) <= t for f in files)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    out = OUT_CHECKED if checked else OUT
+    if not force and up_to_date(out):
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DIALS_CHECKS"] if checked else []), "-o", out + ".tmp",
+           *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -833,7 +833,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     return fail(s, IALS_E_NOMEM, "side_pass: workspace %zu < %zu bytes", ws_bytes, need);
   SweepParams p{};
   p.side = SideDev{side->n_rows, side->n_fixed, side->ptr, side->cols, side->labels,
-                   side->weights, side->pos, side->lam, side->rows};
+                   side->weights, side->pos, side->lam, side->rows, side->nnz};
   p.fixed = fixed;
   p.ldf = ldf;
   p.own = own;

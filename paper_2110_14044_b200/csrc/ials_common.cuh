@@ -5,6 +5,27 @@
 
 #define IALS_DEVI __device__ __forceinline__
 
+// Checked builds (-DIALS_CHECKS, `python -m paper_2110_14044_b200.build --checked`):
+// device-side bounds checks on every index-driven gather and scatter of the
+// sweep kernels; a failure prints the site and traps (the launch then fails
+// with an illegal-instruction error).  compute-sanitizer is not available on
+// this GPU pool; the GPU test suite runs against the checked library instead.
+#ifdef IALS_CHECKS
+#include <cstdio>
+#define IALS_CHECK(cond)                                                                    \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("IALS_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                             \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define IALS_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace ials {
 
 constexpr int kNumSMs = 148;

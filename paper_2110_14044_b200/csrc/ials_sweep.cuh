@@ -32,6 +32,7 @@ struct SideDev {
   const int* pos;
   const float* lam;
   const int* rows;   // [nnz] row of each entry, or null
+  long long nnz;
 };
 
 struct SweepParams {
@@ -192,6 +193,7 @@ IALS_DEVI void stage_chunk(const SweepParams& p, float* sm, int buf, int ebeg, i
       const int k = i >> LG, v = i & (SL - 1);
       if (v >= bv) continue;
       const int col = __ldg(p.side.cols + ebeg + k);
+      IALS_CHECK(col >= 0 && col < p.side.n_fixed);
       cp_async16(X + k * L::XLD + 4 * v, p.fixed + (size_t)col * p.ldf + p.fb0 + 4 * v);
     }
   } else {

@@ -128,6 +128,7 @@ IALS_DEVI void pk_gather(const SweepParams& p, char* smem, const PkState& st, co
       uint64_t* gb = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR) + L::BAR_GATHER + (c % L::NB);
       mbar_expect_tx(gb, (uint32_t)((nk + 3) >> 2) * 4 * L::SW * 4);
       const int* m = mc + g * L::KC;
+      for (int q = 0; q < nk; ++q) IALS_CHECK(m[q] >= 0 && m[q] < p.side.n_fixed);
       for (int k = 0; k < nk; k += 4)
         tma_gather4(smem_u32(X + (g * L::KC + k) * L::SW), st.fmap, p.fb0, m[min(k, last)],
                     m[min(k + 1, last)], m[min(k + 2, last)], m[min(k + 3, last)], gb);
@@ -148,8 +149,10 @@ IALS_DEVI void pk_gather(const SweepParams& p, char* smem, const PkState& st, co
   }
   if (tid < L::EPC) {
     const int g = tid / L::KC, k = tid - g * L::KC;
-    if (k < pk_nk<G>(beg, end, g, c))
+    if (k < pk_nk<G>(beg, end, g, c)) {
+      IALS_CHECK(mp[tid] >= 0 && mp[tid] < p.side.nnz);
       cp_async4(smem + L::OFF_CV + 4 * ((c % L::NCV) * L::EPC + tid), p.cache + mp[tid]);
+    }
   }
 }
 

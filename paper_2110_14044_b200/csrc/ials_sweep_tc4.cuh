@@ -143,6 +143,7 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, const Tc4State& st, 
       mbar_expect_tx(gb, (uint32_t)ng * 4 * L::XLD * 4);
       for (int g = 0; g < ng; ++g) {
         const int k = 4 * g, last = nk - 1;
+        for (int q = k; q < min(k + 4, nk); ++q) IALS_CHECK(mc[q] >= 0 && mc[q] < p.side.n_fixed);
         tma_gather4(smem_u32(X + k * L::XLD), st.fmap, p.fb0, mc[min(k, last)],
                     mc[min(k + 1, last)], mc[min(k + 2, last)], mc[min(k + 3, last)], gb);
       }
@@ -161,8 +162,10 @@ IALS_DEVI void tc4_gather(const SweepParams& p, char* smem, const Tc4State& st, 
       cp_async4(X + k * L::XLD + v, p.fixed + (size_t)mc[k] * p.ldf + p.fb0 + v);
     }
   }
-  if (tid < nk)
+  if (tid < nk) {
+    IALS_CHECK(mp[tid] >= 0 && mp[tid] < p.side.nnz);
     cp_async4(smem + L::OFF_CV + 4 * ((c & 3) * L::KC + tid), p.cache + mp[tid]);
+  }
 }
 
 // UNIT: every weight and label is one (the BASELINE configurations), so the
@@ -966,6 +969,7 @@ __global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(Sweep
     }
     const long long e = e0 + sub;
     const long long pos = (live && g == 0) ? (PS ? (long long)__ldg(PS + e) : e) : 0;
+    IALS_CHECK(!live || (col >= 0 && row >= 0 && pos >= 0 && pos < nnz));
     const float cold = (live && g == 0) ? p.cache[pos] : 0.f;
     if (live && row != cur) {
       const float* dr = SWAP ? p.fixed + (size_t)row * p.ldf + p.fb0 : p.drow + (size_t)row * b;

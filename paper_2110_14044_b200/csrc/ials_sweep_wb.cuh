@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     for (int s = 0; s < G; ++s) nmax = max(nmax, trow[8 + s] - trow[4 + s]);
     const bool valid = row >= 0 && k < n_g;
     const int col = valid ? __ldg(p.side.cols + ebeg + k) : 0;
+    IALS_CHECK(!valid || (col >= 0 && col < p.side.n_fixed && ebeg + k < p.side.nnz));
     const float rho = valid ? p.cache[ebeg + k] - 1.f : 0.f;   // user side: pos = e; UNIT
     const float* xr = p.fixed + (size_t)col * B;
     // per slot: s = D^-1/2 and z := s * p~ (column tid of every slot)
