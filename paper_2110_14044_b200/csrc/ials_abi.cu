@@ -711,17 +711,48 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
       hinit |= dev_bit();
     }
     const int threads = L::NT * L::RPC;
-    const int hg = std::min(p.n_slices, 4 * kNumSMs);
-    if (unit)
-      k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, hst>>>(p, hmap, use_tma_h);
-    else
-      k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, hst>>>(p, hmap, use_tma_h);
-    LAUNCH_CHECK(s);
+    if (G == 1) {
+      const int hg = std::min(p.n_slices, 4 * kNumSMs);
+      if (unit)
+        k_heavy_partial_tc4<true><<<hg, 128, TcLay4::BYTES, hst>>>(p, hmap, use_tma_h);
+      else
+        k_heavy_partial_tc4<false><<<hg, 128, TcLay4::BYTES, hst>>>(p, hmap, use_tma_h);
+      LAUNCH_CHECK(s);
+    } else {   // b <= 64: G slices per tile, [slice][NG x NG] partials
+      static unsigned pinit = 0;
+      if (!(pinit & dev_bit())) {
+        for (auto k : {k_heavy_partial_pk<2, false>, k_heavy_partial_pk<2, true>})
+          CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PkLay<2>::BYTES));
+        for (auto k : {k_heavy_partial_pk<4, false>, k_heavy_partial_pk<4, true>})
+          CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PkLay<4>::BYTES));
+        int rc2 = set_smem_attrs<32>(s);
+        if (!rc2) rc2 = set_smem_attrs<64>(s);
+        if (rc2) return rc2;
+        pinit |= dev_bit();
+      }
+      const int hg = std::min((p.n_slices + G - 1) / G, 4 * kNumSMs);
+      if (G == 2) {
+        if (unit) k_heavy_partial_pk<2, true><<<hg, 128, PkLay<2>::BYTES, hst>>>(p, fmap, use_tma);
+        else k_heavy_partial_pk<2, false><<<hg, 128, PkLay<2>::BYTES, hst>>>(p, fmap, use_tma);
+      } else {
+        if (unit) k_heavy_partial_pk<4, true><<<hg, 128, PkLay<4>::BYTES, hst>>>(p, fmap, use_tma);
+        else k_heavy_partial_pk<4, false><<<hg, 128, PkLay<4>::BYTES, hst>>>(p, fmap, use_tma);
+      }
+      LAUNCH_CHECK(s);
+    }
     if (fork) {
       CUDA_TRY(s, cudaEventRecord(s->ev_join, hst));
       CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_join, 0));
     }
-    k_heavy_solve<128, true, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    if (G == 1) {
+      k_heavy_solve<128, true, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    } else if (G == 2) {
+      using L64 = Lay<64>;
+      k_heavy_solve<64, true><<<(p.n_heavy + L64::RPC - 1) / L64::RPC, L64::NT * L64::RPC, L64::CTA_BYTES, st>>>(p);
+    } else {
+      using L32 = Lay<32>;
+      k_heavy_solve<32, true><<<(p.n_heavy + L32::RPC - 1) / L32::RPC, L32::NT * L32::RPC, L32::CTA_BYTES, st>>>(p);
+    }
     LAUNCH_CHECK(s);
   }
   if (p.n_light + p.n_heavy > 0) {
@@ -1672,6 +1703,13 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
                      reinterpret_cast<float*>(pws) + size_t(r0) * std::min(b, d), st);
     };
   } else if (host) {
+    if (tc_gemm && rot) {   // H first: its copies and the eigendecompositions overlap W's upload
+      CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));
+      CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));
+      rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+      if (!rc) rc = launch_eig();
+      if (rc) return rc;
+    }
     const int nch = 8;
     const int per = (U + nch - 1) / nch;
     for (int c = 0; c < nch && c * per < U; ++c) {
@@ -1686,8 +1724,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     }
     if (tc_gemm) {
       rc = sync_copies(s, W, ldw, d, 0, d, cw, st);
-      if (!rc) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
-      if (!rc && rot) rc = launch_eig();
+      if (!rc && !rot) rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
       if (rc) return rc;
     }
   } else if (range.recompute) {

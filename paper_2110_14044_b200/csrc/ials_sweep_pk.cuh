@@ -673,3 +673,94 @@ __global__ void __launch_bounds__(128, 4) k_sweep_pk(SweepParams p, const __grid
 }
 
 }  // namespace ials
+
+namespace ials {
+
+// Heavy-row slices for b <= 64, G slices per tile: each slot's partial Hessian
+// (its NG x NG diagonal block of the tile, summed from zero over the slice's
+// entries with the packed pipeline) and fp64 partial gradient, written in the
+// [slice][BT x BT] layout k_heavy_solve<BT = NG> reduces in a fixed order
+// (BT x BT: 4 KB at b <= 32 instead of the 64 KB 128-wide tile).
+template <int G, bool UNIT>
+__global__ void __launch_bounds__(128, 4) k_heavy_partial_pk(SweepParams p,
+                                                               const __grid_constant__ CUtensorMap fmap,
+                                                               int use_tma) {
+  using L = PkLay<G>;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = tc_smem_base(smem_raw);
+  const int tid = threadIdx.x, g = tid / L::NG, m = tid - g * L::NG;
+  {
+    float4* x = reinterpret_cast<float4*>(smem + L::OFF_X);
+    for (int i = tid; i < L::NB * G * L::KC * L::SW / 4; i += L::NT) x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + L::OFF_TPTR);
+  int* tinfo = reinterpret_cast<int*>(smem + L::OFF_TILE);   // beg[4] at +4, end[4] at +8
+  int* next = reinterpret_cast<int*>(smem + L::OFF_FLAG) + 4;
+  if (tid == 0) {
+    for (int k = 0; k < L::NXT; ++k) mbar_init(bar + k, 1);
+    for (int k = 0; k < L::NB; ++k) mbar_init(bar + L::BAR_GATHER + k, G);
+    if (use_tma) prefetch_tmap(&fmap);
+  }
+  if (tid < 32) tmem_alloc(tptr, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  PkState st;
+  st.tmem = *tptr;
+  st.ph = 0u;
+  st.gph = 0u;
+  st.fmap = use_tma ? &fmap : nullptr;
+  const uint32_t row_addr = st.tmem + ((uint32_t)((tid >> 5) * 32) << 16);
+  const int n_tiles = (p.n_slices + G - 1) / G;
+  int* queue = p.redo_cnt + 1;
+  for (;;) {
+    if (tid == 0) *next = atomicAdd(queue, 1);
+    __syncthreads();
+    const int task = *next;
+    if (task >= n_tiles) break;
+    if (tid < G) {
+      const int sl = task * G + tid;
+      tinfo[4 + tid] = sl < p.n_slices ? p.slice_begin[sl] : 0;
+      tinfo[8 + tid] = sl < p.n_slices ? p.slice_end[sl] : 0;
+    }
+    {
+      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c8 = 0; c8 < 16; ++c8) tmem_st8(row_addr + 8 * c8, z);
+      tmem_wait_st();
+      tc_fence_before();
+    }
+    __syncthreads();
+    const int* tbeg = tinfo + 4;
+    const int* tend = tinfo + 8;
+    int nch = 0;
+#pragma unroll
+    for (int s = 0; s < G; ++s) nch = max(nch, (tend[s] - tbeg[s] + L::KC - 1) / L::KC);
+    double gacc = 0.0;
+    pk_accumulate<G, UNIT>(p, smem, st, gacc, tbeg, tend, nch, tid);
+    const int sl = task * G + g;
+    if (sl < p.n_slices) {
+      float* hp = p.hpart + (size_t)sl * L::NG * L::NG + (size_t)m * L::NG;
+#pragma unroll
+      for (int c32 = 0; c32 < L::NG; c32 += 32) {
+        float v[32];
+        tmem_ld32(row_addr + g * L::NG + c32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(hp + c32 + 4 * q) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      p.gpart[(size_t)sl * L::NG + m] = gacc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_free(st.tmem, 128);
+}
+
+}  // namespace ials
