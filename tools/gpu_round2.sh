@@ -16,10 +16,17 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --c
   --log-file $O/launches_L1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   -c 400 --csv --log-file $O/traffic_L1.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_traffic.log 2>&1
-for K in k_sweep_tc4 k_sweep_wb k_gemm3_tf32 k_pass_cache_flat k_heavy_partial_tc4 k_sym_eig; do
+summarise() {   # the report is summarised on the box and dropped (gpurun_out <= 64 MiB)
+  python tools/ncu_summary.py $O/ncu_$1.ncu-rep $O/ncu_$1.txt > /dev/null 2>&1
+  python tools/ncu_stalls.py $O/ncu_$1.ncu-rep 30 > $O/ncu_$1_stalls.txt 2>&1
+  rm -f $O/ncu_$1.ncu-rep
+}
+for K in k_sweep_tc4 k_sweep_wb k_gemm3_tf32 k_pass_cache_flat k_heavy_partial_tc4 k_sym_eig k_pred_vec; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 20 -c 1 \
     -o $O/ncu_$K python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_$K.log 2>&1
+  summarise $K
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_pk -s 4 -c 1 \
   -o $O/ncu_k_sweep_pk python bench.py --config mid --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_k_sweep_pk.log 2>&1
+summarise k_sweep_pk
 echo done > $O/DONE
