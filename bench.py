@@ -38,6 +38,7 @@ CONFIGS = {
     "sw-b64": ("mid", 256, 64, "configs[2] d=256 b=64"),
     "sw-b128": ("mid", 256, 128, "configs[2] d=256 b=128"),
     "sw-b256": ("mid", 256, 256, "configs[2] d=256 b=d (iALS case)"),
+    "ials-d512": ("mid", 512, 512, "dedicated iALS (b = d): ML20M-shaped, d=512 (the wide solver, b > 256)"),
     "d64": ("mid", 64, 64, "metric d-grid: ML20M-shaped, d=64 b=d (b=128 > d)"),
     "d512": ("mid", 512, 128, "metric d-grid: ML20M-shaped, d=512 b=128"),
     "L1": ("mid", 1024, 128, "configs[3] ML20M-shaped 136,677x20,108 10.0M, d=1024 b=128"),

@@ -26,6 +26,7 @@
 #include "ials_sweep_wb.cuh"
 #include "ials_gemm_tc.cuh"
 #include "ials_sweep_b1.cuh"
+#include "ials_sweep_wide.cuh"
 
 using namespace ials;
 
@@ -238,7 +239,26 @@ static constexpr int kGemvSplits = 4 * 148;   // b <= 4: one GEMV split per 64+ 
 static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
   (void)n;
   const size_t narrow = b <= 4 ? size_t(kGemvSplits) * d * b : 0;
-  return al256(std::max(size_t(kMaxSplits) * d * b, narrow) * sizeof(float));
+  size_t splits = kMaxSplits;
+  if (b > 256) {   // wide blocks: many 64 x 64 output tiles, few splits (gramian_impl's rule)
+    const size_t tiles = size_t((d + GT - 1) / GT) * ((b + GT - 1) / GT);
+    splits = std::min<size_t>(kMaxSplits, std::max<size_t>(1, (2 * kNumSMs + tiles - 1) / tiles));
+  }
+  return al256(std::max(splits * d * b, narrow) * sizeof(float));
+}
+
+// ---- wide blocks (b > 256, ials_sweep_wide.cuh): the rows of a pass are taken
+// in batches whose normal equations live in the workspace
+static inline int wide_lda(int b) { return (b + 3) & ~3; }
+static inline size_t wide_mat_floats(int b) { return size_t(b + 1) * wide_lda(b); }
+static int wide_batch(int b) {   // rows per batch: a multiple of the SM count, <= 6 GB
+  const size_t per = wide_mat_floats(b) * 4;
+  const size_t fit = (size_t(6) << 30) / per;
+  return (int)std::min<size_t>(8 * kNumSMs, std::max<size_t>(kNumSMs, fit / kNumSMs * kNumSMs));
+}
+static size_t wide_ws(int32_t n_rows, int32_t b) {
+  const size_t R = std::min<size_t>(wide_batch(b), std::max(n_rows, 1));
+  return 2 * al256(size_t(n_rows) * b * 4) + al256(R * wide_mat_floats(b) * 4);
 }
 
 
@@ -249,6 +269,7 @@ static constexpr int kCompactMaxB = 32;
 static inline int compact_ld(int b) { return (b + 3) & ~3; }
 
 static size_t pass_ws(int32_t n_rows, int32_t n_fixed, int32_t b, int32_t n_slices, int32_t n_heavy) {
+  if (b > 256) return wide_ws(n_rows, b);
   const size_t bt = block_tile(b);
   return al256(size_t(n_rows) * b * 4) + al256(size_t(n_slices) * bt * bt * 4) +
          al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4) +
@@ -838,6 +859,59 @@ static float* pass_drow(char* ws, const ials_side* side, const ials_sched* sched
   return reinterpret_cast<float*>(w);
 }
 
+// A pass of a block wider than 256 columns (ials_sweep_wide.cuh): projection,
+// then per batch of rows the Hessians + gradients (k_wide_build) and the
+// factorisations / solves (k_wide_chol), then the entry-parallel cache update.
+static int wide_pass(ials_session* s, SweepParams p, char* ws, cudaStream_t st, bool proj_ready,
+                     const float* proj_in) {
+  const int b = p.b, n_rows = p.side.n_rows;
+  char* w = ws;
+  float* proj = reinterpret_cast<float*>(w);
+  w += al256(size_t(n_rows) * b * 4);
+  p.drow = reinterpret_cast<float*>(w);
+  w += al256(size_t(n_rows) * b * 4);
+  WideParams wp{};
+  wp.A = reinterpret_cast<float*>(w);
+  wp.lda = wide_lda(b);
+  wp.mat_stride = (long long)wide_mat_floats(b);
+  if (proj_in) proj = const_cast<float*>(proj_in);
+  p.proj = proj;
+  p.vec = p.vec && (p.ldf % 4 == 0);
+  if (n_rows == 0) return IALS_OK;
+  if (!proj_ready && !proj_in) {
+    dim3 g((n_rows + GT - 1) / GT, (b + GT - 1) / GT);
+    k_project<<<g, 256, 0, st>>>(p.own, n_rows, p.ldo, p.d, p.slab, b, p.alpha0, proj);
+    LAUNCH_CHECK(s);
+  }
+  const size_t smem = WideSm::bytes(b);
+  if (smem > 227 * 1024) return fail(s, IALS_E_INVALID, "side_pass: block width %d too wide", b);
+  {
+    int dev = 0;
+    CUDA_TRY(s, cudaGetDevice(&dev));
+    static size_t attr_bytes[64] = {};
+    if (dev < 64 && attr_bytes[dev] < smem) {
+      CUDA_TRY(s, cudaFuncSetAttribute(k_wide_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_bytes[dev] = smem;
+    }
+  }
+  const int R = std::min(wide_batch(b), n_rows);
+  const int nt = (b + kWT - 1) / kWT, ntp = nt * (nt + 1) / 2;
+  for (int i0 = 0; i0 < n_rows; i0 += R) {
+    wp.i0 = i0;
+    wp.nb = std::min(R, n_rows - i0);
+    k_wide_build<<<dim3(ntp + 1, wp.nb), 256, 0, st>>>(p, wp, ntp);
+    LAUNCH_CHECK(s);
+    k_wide_chol<<<wp.nb, 256, smem, st>>>(p, wp);
+    LAUNCH_CHECK(s);
+  }
+  if (p.side.nnz > 0) {
+    const long long nw = (p.side.nnz + 7) / 8;
+    k_wide_cache<<<(int)std::min<long long>(nw, 32 * kNumSMs), 256, 0, st>>>(p, p.side.nnz);
+    LAUNCH_CHECK(s);
+  }
+  return IALS_OK;
+}
+
 // a rotated user pass (ials_rot.cuh): the pass sweeps F~ = F[:, pi] Q with the
 // diagonal template diag(eigenvalues) (rslab's rows pi), reads W[:, pi] Q
 // (wq) for the lam * w term and leaves d~ in drow for the back-rotation
@@ -856,7 +930,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
                           const ials_side* other = nullptr, const RotPass* rot = nullptr) {
   if (!side || !sched || !fixed || !own || !slab || !cache)
     return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
-  if (d < 1 || b < 1 || b > 256 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
+  if (d < 1 || b < 1 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
     return fail(s, IALS_E_INVALID, "side_pass: bad block (d=%d b0=%d b=%d)", d, b0, b);
   const int bt = block_tile(b);
   const size_t need = pass_ws(side->n_rows, side->n_fixed, b, sched->n_slices, sched->n_heavy);
@@ -890,6 +964,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.slice_begin = sched->slice_begin;
   p.slice_end = sched->slice_end;
   p.n_slices = sched->n_slices;
+  if (b > 256) return wide_pass(s, p, ws, st, proj_ready, proj_in);
   char* w = ws;
   float* proj = reinterpret_cast<float*>(w);
   w += al256(size_t(side->n_rows) * b * 4);
@@ -1498,7 +1573,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
   if (!users || !items || !user_sched || !item_sched)
     return fail(s, IALS_E_INVALID, "epoch: NULL argument");
-  if (b < 1 || b > d || b > 256) return fail(s, IALS_E_INVALID, "epoch: bad block size %d", b);
+  if (b < 1 || b > d) return fail(s, IALS_E_INVALID, "epoch: bad block size %d", b);
   cudaStream_t st = S(stream);
   char* ws = static_cast<char*>(workspace);
   const size_t slab_bytes = al256(size_t(d) * b * 4);

@@ -8,9 +8,8 @@ Host mirror of the reference's ``project_user`` / ``fold_in_users``
 * Fold-in solves, per history, the same regularized least squares as a user
   pass.  On the device that is one user pass of the block sweep with a single
   block of width d from a zero embedding and a zero cache: the Newton step
-  from w = 0 is the closed-form solve.  Block widths go up to 256; wider
-  models iterate user passes over 128-column blocks (block Gauss-Seidel on
-  the same strictly convex quadratic) to a relative change below 1e-6.
+  from w = 0 is the closed-form solve (any d: widths above 256 take the
+  batched wide solver, csrc/ials_sweep_wide.cuh).
 * Scores are the repo's own 3xTF32 tensor-core GEMM (``ials_scores``: the TMA
   GEMM of the epoch with 128-item output tiles, FP32-accurate); the exclusion
   of each user's input items and the top-k with the reference's tie order run
@@ -38,7 +37,6 @@ from .solvers import block_update
 __all__ = ["MetricReport", "project_user", "fold_in_users", "top_k_from_scores", "rank_items",
            "recall_at_k", "ndcg_at_k", "evaluate_holdout"]
 
-_MAX_FOLD_DIM = 256
 _MAX_K = 1024
 
 
@@ -72,42 +70,7 @@ def fold_in_users(item_factors, histories, config: SolverConfig, device=None) ->
                               np.concatenate(labels), np.concatenate(weights))
     model = FactorModel(out, hf)
     cache = PredictionCache.zeros(data.n_interactions)   # exact for the zero embedding
-    if d <= _MAX_FOLD_DIM:
-        block_update(model, data, cache, config.with_(dim=d, block_size=d), np.arange(d), "user",
-                     device)
-        return model.user_factors
-    return _fold_in_blocks(model, data, cache, config, device)
-
-
-def _fold_in_blocks(model, data, cache, config, device, tol=1e-6, max_sweeps=200):
-    """d > 256 (wider than one sweep block): block Gauss-Seidel on each
-    history's quadratic with the same device passes -- user passes over
-    blocks of 128 columns, the cache kept exact -- until a whole sweep changes
-    the embeddings by less than ``tol`` (relative, Frobenius; 1e-6, above the
-    FP32 rounding floor of the change, far below the 1e-3 parity bar).  Each pass is
-    an exact block minimisation, so the iteration converges to the reference's
-    closed-form solve (the quadratic is strictly convex: lambda > 0)."""
-    import torch
-
-    from .solvers import DeviceTrainer, partition_dims
-    d = model.dim
-    cfg = config.with_(dim=d, block_size=128)
-    tr = DeviceTrainer(model, data, cfg, partition_dims(d, 128), device, cache)
-    prev = torch.zeros_like(tr.W)
-    for _ in range(max_sweeps):
-        prev.copy_(tr.W)
-        for b0, b in tr.spans:
-            tr.block(b0, b, "user")
-        num = float(torch.linalg.vector_norm(tr.W - prev))
-        den = float(torch.linalg.vector_norm(tr.W))
-        if num <= tol * max(den, 1e-30):
-            break
-    else:   # strongly coupled blocks converge slowly: say so instead of returning silently
-        import warnings   # (FP32 rounding keeps the per-sweep change near 1e-7 at best)
-        warnings.warn(f"fold_in_users: block Gauss-Seidel for d = {d} stopped after {max_sweeps} "
-                      f"sweeps at a relative change of {num / max(den, 1e-30):.2e} (> {tol:.0e})",
-                      RuntimeWarning, stacklevel=3)
-    tr.write_back()
+    block_update(model, data, cache, config.with_(dim=d, block_size=d), np.arange(d), "user", device)
     return model.user_factors
 
 

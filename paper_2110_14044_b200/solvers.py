@@ -353,10 +353,9 @@ def ials_epoch(model: FactorModel, data, config: SolverConfig, epoch_index: int 
     exact item pass.  On the device this is the block sweep with one block of
     width d: a Newton step from an exact cache solves the row's quadratic in
     closed form, so it equals the reference's direct solve (pinned by the
-    reference's own equivalence test, test_solvers.py:125-149).  The cache
-    is internal and discarded, as in the reference."""
-    if model.dim > 256:
-        raise ValueError("ials_epoch on the device supports dim <= 256 (block width of the sweep)")
+    reference's own equivalence test, test_solvers.py:125-149).  Widths
+    above 256 take the batched wide solver (csrc/ials_sweep_wide.cuh).  The
+    cache is internal and discarded, as in the reference."""
     cache = PredictionCache(np.zeros(data.n_interactions))
     return ialspp_epoch(model, data, cache, config, partition_dims(model.dim, model.dim),
                         epoch_index, device)

@@ -89,20 +89,6 @@ def test_ranking_and_metrics_match_reference(eval_golden):
         ials.evaluate_holdout(g["item_factors"], [f for f in folds if f.target_items.size == 0], CFG)
 
 
-def test_fold_in_wide_models_converge_to_the_exact_solve():
-    """d > 256: block Gauss-Seidel over 128-column user passes reaches the
-    closed-form fold-in (the oracle's f64 solve) within the north-star 1e-3."""
-    from oracle import ialspp_oracle as orc
-    rng = np.random.default_rng(17)
-    I, d = 900, 384
-    hf = (rng.standard_normal((I, d)) * 0.05).astype(np.float32).astype(np.float64)
-    hist = [(rng.choice(I, int(rng.integers(0, 60)), replace=False), None, None) for _ in range(300)]
-    cfg = ials.SolverConfig(dim=d, block_size=128, unobserved_weight=0.1, reg=1e-3)
-    got = ials.fold_in_users(hf, hist, cfg)
-    want = orc.fold_in(hf, hist, 0.1, 1e-3, 1.0)
-    assert relf(got, want) < 1e-3
-
-
 @pytest.mark.parametrize("d", [32, 128, 200])
 def test_fold_in_with_labels_and_weights(d):
     """Non-unit labels / weights reach the device fold-in (the sweep's
