@@ -416,7 +416,7 @@ def run_ours(args, cfg_key):
             # FP32 sweep during the timed epochs (numerics transparency)
             "tc_redo_rows": tc_redo,
         }
-        print(json.dumps(line))
+        emit(line)
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -498,7 +498,7 @@ def run_sharded(args, cfg_key, ds, dev, rank, world):
     if rank == 0:
         hbm, _ = load_peaks()
         rl = roofline_model(U, I, S, d, b, FP32_NOMINAL_TFLOPS, hbm)
-        print(json.dumps({
+        emit(({
             "metric": "ialspp_epoch_nnz_d_updates_per_s", "value": value, "unit": "nnz*d/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "epoch_seconds": round(ms_step / 1e3, 6),
@@ -692,13 +692,31 @@ def run_reference(args, cfg_key):
                              "epoch_seconds_est": last["epoch_seconds_est"]},
             "e2e": {"value": value, "unit": "nnz*d/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
+
+
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 
 
 def main():
-    # NCCL writes its log (and its version banner) to stdout unless told
-    # otherwise: stdout carries the one JSON line
+    # stdout carries the one JSON line: NCCL prints its version banner (and,
+    # unless told otherwise, its log) to stdout from native code, so fd 1 is
+    # pointed at stderr for the run and the line goes to the saved descriptor
+    global _JSON_FD
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

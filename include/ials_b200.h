@@ -302,6 +302,32 @@ int ials_side_pass_projected(ials_session* s, const ials_side* side, const ials_
                              float alpha0, float* cache, int32_t side_id, void* workspace,
                              size_t ws_bytes, void* stream);
 
+/* Rotated user passes over a row shard (b = 128 dividing d, unit weights, no
+ * heavy user rows): the sharded form of ials_epoch's rotated pass
+ * (_newton_side_pass, solvers.py:152-186, in the eigenbasis of G_pp).
+ *  1. ials_shard_diag_gramian: Gd (d x b; rows [z b, (z+1) b) = the partial
+ *     G_zz = F_shard[:, z]^T F_shard[:, z] of every block z) from the ITEM
+ *     shard's K-major copies (ws = its ials_shard_gemm_bytes workspace); the
+ *     caller all-reduces Gd across ranks (every G_zz is final at epoch start);
+ *  2. ials_shard_rot_prepare: every block's eigendecomposition into rot_ws
+ *     (ials_shard_rot_bytes(local users, items, d, b)), one CTA per block;
+ *  3. ials_shard_user_pass_rot: block b0's user pass on the local user rows
+ *     (own = W_local, own_ws = its shard workspace, fixed = the replicated H,
+ *     slab = the all-reduced d x b slab, workspace = ials_workspace_bytes). */
+size_t ials_shard_rot_bytes(int32_t n_rows, int32_t n_fixed, int32_t d, int32_t b);
+/* 1 when user passes of width b at dimension d can run rotated (b = 128
+ * dividing d, at most 64 blocks, rotation and the tensor-core sweep enabled). */
+int ials_rotation_available(int32_t d, int32_t b);
+int ials_shard_diag_gramian(ials_session* s, int32_t n_rows, int32_t d, int32_t b, float* Gd, void* ws,
+                            size_t ws_bytes, void* stream);
+int ials_shard_rot_prepare(ials_session* s, int32_t d, int32_t b, const float* Gd, int32_t n_rows,
+                           int32_t n_fixed, void* rot_ws, size_t rot_bytes, void* stream);
+int ials_shard_user_pass_rot(ials_session* s, const ials_side* side, const ials_sched* sched,
+                             const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                             int32_t b0, int32_t b, float* slab, float alpha0, float* cache,
+                             void* own_ws, size_t own_ws_bytes, void* rot_ws, size_t rot_bytes,
+                             void* workspace, size_t ws_bytes, void* stream);
+
 /* Workspace bytes for ials_build_csr over n interactions. */
 size_t ials_build_csr_workspace_bytes(int64_t n);
 

@@ -103,6 +103,13 @@ SIGNATURES = {
     "ials_side_pass_projected": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
                                          c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p, c_f,
                                          c_p, c_i32, c_p, c_sz, c_p]),
+    "ials_shard_rot_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32]),
+    "ials_rotation_available": (c_i32, [c_i32, c_i32]),
+    "ials_shard_diag_gramian": (c_i32, [c_p, c_i32, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
+    "ials_shard_rot_prepare": (c_i32, [c_p, c_i32, c_i32, c_p, c_i32, c_i32, c_p, c_sz, c_p]),
+    "ials_shard_user_pass_rot": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
+                                         c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_f, c_p,
+                                         c_p, c_sz, c_p, c_sz, c_p, c_sz, c_p]),
     "ials_topk": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
     "ials_build_csr": (c_i32, [c_p, c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                                c_p, c_sz, c_p]),

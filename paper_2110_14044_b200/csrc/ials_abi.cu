@@ -249,6 +249,10 @@ static size_t gram_ws(int32_t n, int32_t d, int32_t b) {
 
 // ---- wide blocks (b > 256, ials_sweep_wide.cuh): the rows of a pass are taken
 // in batches whose normal equations live in the workspace
+static int wide_min() {   // narrowest block taking the wide pass (IALS_WIDE_MIN: measurements)
+  static const int v = getenv("IALS_WIDE_MIN") ? std::max(65, atoi(getenv("IALS_WIDE_MIN"))) : 257;
+  return v;
+}
 static inline int wide_lda(int b) { return (b + 3) & ~3; }
 static inline size_t wide_mat_floats(int b) { return size_t(b + 1) * wide_lda(b); }
 static int wide_batch(int b) {   // rows per batch: a multiple of the SM count, <= 6 GB
@@ -269,7 +273,7 @@ static constexpr int kCompactMaxB = 32;
 static inline int compact_ld(int b) { return (b + 3) & ~3; }
 
 static size_t pass_ws(int32_t n_rows, int32_t n_fixed, int32_t b, int32_t n_slices, int32_t n_heavy) {
-  if (b > 256) return wide_ws(n_rows, b);
+  if (b >= wide_min()) return wide_ws(n_rows, b);
   const size_t bt = block_tile(b);
   return al256(size_t(n_rows) * b * 4) + al256(size_t(n_slices) * bt * bt * 4) +
          al256(size_t(n_slices) * bt * 8) + al256(size_t(n_heavy) * bt * 4) +
@@ -964,7 +968,7 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.slice_begin = sched->slice_begin;
   p.slice_end = sched->slice_end;
   p.n_slices = sched->n_slices;
-  if (b > 256) return wide_pass(s, p, ws, st, proj_ready, proj_in);
+  if (b >= wide_min()) return wide_pass(s, p, ws, st, proj_ready, proj_in);
   char* w = ws;
   float* proj = reinterpret_cast<float*>(w);
   w += al256(size_t(side->n_rows) * b * 4);
@@ -1365,6 +1369,138 @@ int ials_shard_apply_block(ials_session* s, const float* recv, int32_t nmax, con
       recv, nmax, bounds, world, rank, old_local, X, ldx, b0, b, delta, n_rows);
   LAUNCH_CHECK(s);
   return IALS_OK;
+}
+
+// ---- rotated user passes over a row shard (the multi-GPU host path).  Every
+// block's G_pp = H[:, pi]^T H[:, pi] is final at the start of an epoch, so the
+// ranks form their partial diagonal blocks at once (ials_shard_diag_gramian),
+// all-reduce the d x b stack, and every rank decomposes the same input
+// (ials_shard_rot_prepare: one CTA per block, all blocks side by side).  A
+// user pass then runs like ials_epoch's: rotated projection, F~ = H[:, pi] Q
+// from the replicated H, W_loc[:, pi] Q, the rotated sweep, the back-rotation.
+struct ShardRot {
+  float *QT, *Qm, *rslab, *slabQT, *lam, *Ft, *WQ;
+};
+static size_t shard_rot_bytes(int n_rows, int n_fixed, int d, int b) {
+  if (b != 128 || d % b) return 0;
+  return 4 * al256(size_t(d) * b * 4) + al256(size_t(d) * 4) +
+         al256(size_t(std::max(n_fixed, 1)) * b * 4) + al256(size_t(std::max(n_rows, 1)) * b * 4) + 1024;
+}
+static int shard_rot_carve(ials_session* s, void* ws, size_t bytes, int n_rows, int n_fixed, int d, int b,
+                           ShardRot* r) {
+  const size_t need = shard_rot_bytes(n_rows, n_fixed, d, b);
+  if (!need) return fail(s, IALS_E_INVALID, "shard_rot: b must be 128 and divide d (d=%d b=%d)", d, b);
+  if (!ws || bytes < need) return fail(s, IALS_E_NOMEM, "shard_rot: workspace %zu < %zu bytes", bytes, need);
+  char* t = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 1023) & ~uintptr_t(1023));
+  auto take = [&](size_t n) { float* p = reinterpret_cast<float*>(t); t += al256(n); return p; };
+  r->QT = take(size_t(d) * b * 4);
+  r->Qm = take(size_t(d) * b * 4);
+  r->rslab = take(size_t(d) * b * 4);
+  r->slabQT = take(size_t(d) * b * 4);
+  r->lam = take(size_t(d) * 4);
+  r->Ft = take(size_t(std::max(n_fixed, 1)) * b * 4);
+  r->WQ = take(size_t(std::max(n_rows, 1)) * b * 4);
+  return IALS_OK;
+}
+
+size_t ials_shard_rot_bytes(int32_t n_rows, int32_t n_fixed, int32_t d, int32_t b) {
+  return shard_rot_bytes(n_rows, n_fixed, d, b);
+}
+
+int ials_rotation_available(int32_t d, int32_t b) {
+  return (rot_enabled() && tc4_enabled() && b == 128 && d >= b && d % b == 0 && d / b <= 64) ? 1 : 0;
+}
+
+int ials_shard_diag_gramian(ials_session* s, int32_t n_rows, int32_t d, int32_t b, float* Gd, void* ws,
+                            size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  ShardWs w;
+  int rc = shard_carve(s, ws, ws_bytes, n_rows, d, b, &w);
+  if (rc) return rc;
+  if (!Gd || b != 128 || d % b) return fail(s, IALS_E_INVALID, "shard_diag_gramian: b must be 128 and divide d");
+  cudaStream_t st = S(stream);
+  if (n_rows == 0) {
+    CUDA_TRY(s, cudaMemsetAsync(Gd, 0, size_t(d) * b * 4, st));
+    return IALS_OK;
+  }
+  if (get_encode(s) != IALS_OK) return fail(s, IALS_E_CUDA, "shard_diag_gramian: no cuTensorMapEncodeTiled");
+  rc = gemm_attrs(s);
+  if (rc) return rc;
+  CUtensorMap gm;   // F^T (d x n): A and B operands, B rows following the A tile
+  rc = make_map(s, &gm, w.c.FT, w.c.n, d, w.c.ldt, 128);
+  if (rc) return rc;
+  const int nblk = d / b;
+  GemmJob job{d, 0, 0, b, 128, w.c.n, w.span, w.P, b, (long long)d * b, 1.f};
+  job.diag = 1;
+  k_gemm3_tf32<<<dim3(nblk, w.S), kGemmThreads, GemmLay::BYTES, st>>>(gm, gm, gm, job);
+  LAUNCH_CHECK(s);
+  const size_t cnt = size_t(d) * b;
+  k_reduce_splits_strided<<<(int)std::min<size_t>((cnt + 255) / 256, 4096), 256, 0, st>>>(
+      w.P, w.S, (long long)d * b, cnt, Gd);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+int ials_shard_rot_prepare(ials_session* s, int32_t d, int32_t b, const float* Gd, int32_t n_rows,
+                           int32_t n_fixed, void* rot_ws, size_t rot_bytes_, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  ShardRot r;
+  int rc = shard_rot_carve(s, rot_ws, rot_bytes_, n_rows, n_fixed, d, b, &r);
+  if (rc) return rc;
+  if (!Gd) return fail(s, IALS_E_INVALID, "shard_rot_prepare: NULL Gd");
+  rc = eig_attrs(s, b);
+  if (rc) return rc;
+  cudaStream_t st = S(stream);
+  k_sym_eig<<<d / b, kEigThreads, eig_smem_bytes(b), st>>>(Gd, b, (long long)b * b, b, r.QT, r.lam, r.rslab,
+                                                           r.Qm, nullptr, 1);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
+int ials_shard_user_pass_rot(ials_session* s, const ials_side* side, const ials_sched* sched,
+                             const float* fixed, int32_t ldf, float* own, int32_t ldo, int32_t d,
+                             int32_t b0, int32_t b, float* slab, float alpha0, float* cache,
+                             void* own_ws, size_t own_ws_bytes, void* rot_ws, size_t rot_bytes_,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  DevGuard _dg(s);
+  if (!s) return fail(nullptr, IALS_E_INVALID, "session is NULL");
+  if (!side || !sched || !fixed || !own || !slab || !cache)
+    return fail(s, IALS_E_INVALID, "shard_user_pass_rot: NULL argument");
+  if (b != 128 || d % b || b0 % b || b0 < 0 || b0 + b > d)
+    return fail(s, IALS_E_INVALID, "shard_user_pass_rot: bad block (d=%d b0=%d b=%d)", d, b0, b);
+  if (sched->n_heavy != 0 || side->weights || side->labels)
+    return fail(s, IALS_E_INVALID, "shard_user_pass_rot: unit weights and no heavy rows only");
+  if (!tc4_enabled()) return fail(s, IALS_E_INVALID, "shard_user_pass_rot: the tensor-core sweep is disabled");
+  if (side->n_rows == 0) return IALS_OK;
+  ShardWs w;
+  int rc = shard_carve(s, own_ws, own_ws_bytes, side->n_rows, d, b, &w);
+  if (rc) return rc;
+  ShardRot r;
+  rc = shard_rot_carve(s, rot_ws, rot_bytes_, side->n_rows, side->n_fixed, d, b, &r);
+  if (rc) return rc;
+  if (get_encode(s) != IALS_OK) return fail(s, IALS_E_CUDA, "shard_user_pass_rot: no cuTensorMapEncodeTiled");
+  cudaStream_t st = S(stream);
+  char* pws = static_cast<char*>(workspace);
+  const size_t need = pass_ws(side->n_rows, side->n_fixed, b, sched->n_slices, sched->n_heavy);
+  if (!pws || ws_bytes < need)
+    return fail(s, IALS_E_NOMEM, "shard_user_pass_rot: workspace %zu < %zu bytes", ws_bytes, need);
+  const int zb = b0 / b;
+  const float* qt = r.QT + size_t(zb) * b * b;
+  // (slab Q)^T -> the rotated projection alpha0 W_loc slab Q; F~ = H[:, pi] Q; W_loc[:, pi] Q
+  rc = gemm_nt(s, qt, b, b, b, 0, slab, d, b, b, 0, b, r.slabQT, d, 1.f, false, st);
+  if (!rc) rc = proj_tc(s, own, ldo, w.c, d, b, r.slabQT, nullptr, alpha0, reinterpret_cast<float*>(pws), st);
+  if (!rc) rc = gemm_nt(s, fixed, side->n_fixed, d, ldf, b0, qt, b, b, b, 0, b, r.Ft, b, 1.f, false, st);
+  if (!rc) rc = gemm_nt(s, own, side->n_rows, d, ldo, b0, qt, b, b, b, 0, b, r.WQ, b, 1.f, false, st);
+  if (rc) return rc;
+  RotPass rp{r.Ft, r.WQ, r.lam + b0, r.rslab};
+  rc = side_pass_impl(s, side, sched, fixed, ldf, own, ldo, d, b0, b, slab, alpha0, cache, 0, pws, ws_bytes,
+                      st, true, nullptr, nullptr, &rp);
+  if (rc) return rc;
+  // W_loc[:, pi] -= d~ Q^T: the rows' steps back in the original basis
+  return gemm_nt(s, pass_drow(pws, side, sched, b), side->n_rows, b, b, 0, r.Qm + size_t(zb) * b * b, b, b, b, 0,
+                 b, own + b0, ldo, -1.f, true, st);
 }
 
 // optional phase events: 0 start, 1 after the cache, then per block

@@ -196,6 +196,48 @@ class GpuOps:
         self.sess.check(rc, "partial_gramian")
         return out
 
+    # ---- rotated user passes (b = 128): the sharded form of ials_epoch's
+    # (eigenbasis of G_pp, Woodbury tiles for the short rows)
+    def rot_supported(self, d, b, max_user_degree, unit_weights):
+        """Whether the user passes of this run can be rotated.  Decided from
+        GLOBAL quantities only, so every rank takes the same branch (the
+        branch adds an all-reduce)."""
+        return bool(unit_weights and self.sess.lib.ials_rotation_available(d, b)
+                    and max_user_degree <= int(self.sess.lib.ials_heavy_threshold(b)))
+
+    def diag_gram(self, M_rows, b):
+        """Partial diagonal Gram blocks of the (item) shard: (d x b), rows
+        [z b, (z+1) b) = M[:, z]^T M[:, z]; None off the tensor-core path."""
+        from .engine import _ptr
+        sh = self._shard(M_rows)
+        if sh is None or sh[2] != b:
+            return None
+        ws, n, _ = sh
+        d = M_rows.shape[1]
+        out = torch.empty((d, b), dtype=self.dtype, device=self.device)
+        rc = self.sess.lib.ials_shard_diag_gramian(self.sess.handle, n, d, b, _ptr(out), _ptr(ws),
+                                                   ws.numel(), self._stream())
+        self.sess.check(rc, "shard_diag_gramian")
+        return out
+
+    def rot_prepare(self, gd, own_rows, n_fixed, b):
+        """Decompose every (all-reduced) diagonal block; the user sweeps of
+        this epoch then run rotated."""
+        from .engine import _ptr
+        d = own_rows.shape[1]
+        n = own_rows.shape[0]
+        nb = int(self.sess.lib.ials_shard_rot_bytes(n, n_fixed, d, b))
+        if getattr(self, "_rot_ws", None) is None or self._rot_ws.numel() < nb:
+            self._rot_ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        rc = self.sess.lib.ials_shard_rot_prepare(self.sess.handle, d, b, _ptr(gd), n, n_fixed,
+                                                  _ptr(self._rot_ws), self._rot_ws.numel(),
+                                                  self._stream())
+        self.sess.check(rc, "shard_rot_prepare")
+        self._rot = (own_rows.data_ptr(), b)
+
+    def rot_end(self):
+        self._rot = None
+
     def sweep(self, side, fixed, own_rows, b0, b, slab, alpha0, cache, side_id):
         from .engine import _ptr
         import ctypes
@@ -205,6 +247,18 @@ class GpuOps:
         ws = self._workspace(int(self.sess.lib.ials_workspace_bytes(
             max(ds.n_rows, 1), max(fixed.shape[0], 1), d, b, sch.n_slices, sch.n_heavy)))
         sh = self._shard(own_rows)
+        if (side_id == 0 and getattr(self, "_rot", None) == (own_rows.data_ptr(), b)
+                and sh is not None and sch.n_heavy == 0):
+            if own_rows.shape[0] > 0:
+                sws = sh[0]
+                rc = self.sess.lib.ials_shard_user_pass_rot(
+                    self.sess.handle, ctypes.byref(ds.struct), ctypes.byref(sch.struct), _ptr(fixed),
+                    fixed.stride(0), _ptr(own_rows), own_rows.stride(0), d, b0, b, _ptr(slab),
+                    float(alpha0), _ptr(cache), _ptr(sws), sws.numel(), _ptr(self._rot_ws),
+                    self._rot_ws.numel(), _ptr(ws), ws.numel(), self._stream())
+                self.sess.check(rc, "shard_user_pass_rot")
+                self.tc_sync(own_rows, b0, b)
+            return
         if sh is not None and b <= sh[2] and own_rows.shape[0] > 0:
             # projection alpha0 * own @ slab on the tensor core, then the sweep
             sws, n, bw = sh
@@ -279,6 +333,9 @@ class ShardedTrainer:
         self.Ci = torch.zeros(self.is_.nnz, dtype=dt, device=dev)
         self._umax = max(h - l for l, h in self.user_bounds)
         self._imax = max(h - l for l, h in self.item_bounds)
+        # global facts the rotated-pass decision rests on (identical on every rank)
+        self._max_user_degree = int(np.diff(up).max()) if U > 0 else 0
+        self._unit = data.get("labels") is None and data.get("weights") is None
 
     # ---------------------------------------------------------------- comms
     def _allreduce(self, t):
@@ -327,6 +384,17 @@ class ShardedTrainer:
         if hasattr(ops, "tc_enable"):   # K-major copies of both shards (no-op when b is off the TC path)
             for M in (Wl, Hl):
                 ops.tc_enable(M, block_size)
+        # rotated user passes: every block's G_pp = H[:, pi]^T H[:, pi] is final
+        # here (H[:, pi] changes only in block pi's item pass, after its user
+        # pass), so the ranks' partial diagonal blocks go through ONE all-reduce
+        # (d x b floats) and every rank decomposes the same matrices
+        rot = (hasattr(ops, "rot_supported") and self.I > 0 and self.U > 0
+               and ops.rot_supported(d, block_size, self._max_user_degree, self._unit))
+        if rot:
+            gd = ops.diag_gram(Hl, block_size)
+            rot = gd is not None
+        if rot:
+            ops.rot_prepare(self._allreduce(gd), Wl, self.I, block_size)
         ops.predictions(self.us, Wl, H, self.Cu)
         ops.predictions(self.is_, Hl, W, self.Ci)
         prev = None        # (b0, b, dH) of the last item pass
@@ -355,6 +423,8 @@ class ShardedTrainer:
         # bring C_u up to date with the last item pass
         if prev is not None:
             ops.correct(self.us, Wl, prev[0], prev[2], self.Cu)
+        if rot:
+            ops.rot_end()
 
     def gather_cache(self):
         """The canonical (user-major) cache, assembled on every rank."""

@@ -40,7 +40,7 @@ def _instance(seed, U=37, I=23, nnz=420, weighted=True):
     return csr, data
 
 
-def _worker(rank, world, port, seed, d, b, epochs, q):
+def _worker(rank, world, port, seed, d, b, epochs, q, rot=False):
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
     from dist_cpu_ops import CpuOps
@@ -48,12 +48,16 @@ def _worker(rank, world, port, seed, d, b, epochs, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        csr, data = _instance(seed)
+        csr, data = _instance(seed, weighted=not rot)
         w, h = orc.init_factors(data["num_users"], data["num_items"], d, 0.1, seed)
         W, H = torch.from_numpy(w.copy()), torch.from_numpy(h.copy())
-        tr = ShardedTrainer(data, W, H, 0.1, 0.01, 1.0, CpuOps())
+        ops = CpuOps()
+        ops.enable_rot = rot
+        tr = ShardedTrainer(data, W, H, 0.1, 0.01, 1.0, ops)
         for _ in range(epochs):
             tr.epoch(b)
+        if rot:   # every user pass of every epoch saw the all-reduced diagonal blocks
+            assert ops.rot_checks == epochs * (d // b), ops.rot_checks
         cache = tr.gather_cache()
         if rank == 0:
             q.put((W.numpy().copy(), H.numpy().copy(), cache.numpy().copy()))
@@ -61,13 +65,17 @@ def _worker(rank, world, port, seed, d, b, epochs, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,d,b,epochs", [(2, 6, 2, 2), (2, 5, 5, 1), (3, 8, 3, 2)])
-def test_sharded_epoch_matches_oracle(world, d, b, epochs):
+@pytest.mark.parametrize("world,d,b,epochs,rot", [(2, 6, 2, 2, False), (2, 5, 5, 1, False),
+                                                   (3, 8, 3, 2, False), (2, 8, 4, 2, True),
+                                                   (3, 6, 2, 1, True)])
+def test_sharded_epoch_matches_oracle(world, d, b, epochs, rot):
+    """rot: the rotated-user-pass protocol (one all-reduce of the stacked
+    diagonal Gram blocks at epoch start; unit weights)."""
     seed = 11
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, d, b, epochs, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, d, b, epochs, q, rot))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -75,7 +83,7 @@ def test_sharded_epoch_matches_oracle(world, d, b, epochs):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    csr, data = _instance(seed)
+    csr, data = _instance(seed, weighted=not rot)
     w, h = orc.init_factors(data["num_users"], data["num_items"], d, 0.1, seed)
     ref_cache = orc.train(w, h, csr, 0.1, 0.01, 1.0, b, epochs)
     assert np.abs(W - w).max() <= 1e-10 * max(1.0, np.abs(w).max())

@@ -234,7 +234,7 @@ def test_tensor_core_one_and_ten_epochs(ials, d, b):
     assert abs(reports[-1].loss - want10) / want10 < TOL
 
 
-@pytest.mark.parametrize("d,b", [(48, 16), (256, 128), (96, 48)])
+@pytest.mark.parametrize("d,b", [(48, 16), (256, 128), (96, 48), (512, 128)])
 def test_sharded_path_gpu_ops_single_rank(ials, d, b):
     """The multi-GPU orchestration with the real kernels (GpuOps, fp32) at
     world size 1: local sides, the item-major cache C_i and the delta
