@@ -87,7 +87,19 @@ typedef struct ials_sched {
   int32_t n_deg_gt32;
 } ials_sched;
 
+/* Row segments of at most a few hundred entries each (the gather-dot kernels
+ * of the multi-GPU path walk these instead of whole rows, so one long item
+ * row does not serialise a warp): segment t covers entries [beg[t], end[t])
+ * of local row row[t]. */
+typedef struct ials_segs {
+  int32_t n;
+  const int32_t* row;
+  const int32_t* beg;
+  const int32_t* end;
+} ials_segs;
+
 typedef struct ials_session ials_session;
+typedef struct ials_comm ials_comm;
 
 int ials_version(void);
 int ials_session_create(int device, ials_session** out);
@@ -327,6 +339,47 @@ int ials_shard_user_pass_rot(ials_session* s, const ials_side* side, const ials_
                              int32_t b0, int32_t b, float* slab, float alpha0, float* cache,
                              void* own_ws, size_t own_ws_bytes, void* rot_ws, size_t rot_bytes,
                              void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- multi-GPU epoch (one process per GPU, contiguous row
+ * shards of users and items, W and H replicated on every rank).  The
+ * communicator wraps an NCCL communicator over the ranks' GPUs; libnccl.so.2 is
+ * opened at run time (the process's own copy under a PyTorch host).
+ *   rank 0:     ials_comm_unique_id(id)   -> 128 bytes, sent to every rank by
+ *               the host's own means (MPI, a socket, torch.distributed ...)
+ *   every rank: ials_comm_create(sess, id, rank, world, &comm)
+ * With id == NULL and world == 1 the communicator is local (no NCCL). */
+int ials_comm_unique_id(void* id128);
+int ials_comm_create(ials_session* s, const void* id128, int32_t rank, int32_t world, ials_comm** out);
+int ials_comm_destroy(ials_comm* c);
+
+/* One rank's share of an iALS++ epoch (ialspp_epoch, solvers.py:340-375),
+ * called collectively by all ranks of `comm`.
+ *   user_bounds / item_bounds: HOST arrays of world + 1 row offsets (rank r owns
+ *     rows [bounds[r], bounds[r+1]); bounds[world] = U / I);
+ *   users / items: the LOCAL rows' CSR (ptr rebased to 0, cols = global ids of
+ *     the other side, pos = NULL, lam = the local rows' regularisers, n_fixed =
+ *     I / U) with their schedules and segment lists;
+ *   W (U x d), H (I x d): the replicated tables on this rank's device, updated
+ *     in place on every rank;
+ *   Cu / Ci: this rank's score caches (its users' entries user-major, its
+ *     items' entries item-major), recomputed at the start of the epoch;
+ *   rotate: 1 to run the user passes rotated (b = 128 | d, unit weights, no
+ *     local heavy user rows on ANY rank -- the flag must be the same on all
+ *     ranks: it adds a collective); see ials_rotation_available.
+ * Per block: all-reduce of the partial slab (NCCL, d x b floats), the local
+ * sweep, the padded all-gather of the updated column block on the
+ * communicator's stream beside the other side's partial slab GEMM, and the
+ * dual-cache correction from the gathered block's change.  Block widths up to
+ * 256.  Workspace: ials_epoch_sharded_bytes (n_slices_max / n_heavy_max: the
+ * larger of the two local schedules'). */
+size_t ials_epoch_sharded_bytes(const int32_t* user_bounds, const int32_t* item_bounds, int32_t world,
+                                int32_t rank, int32_t d, int32_t b, int32_t n_slices_max,
+                                int32_t n_heavy_max);
+int ials_epoch_sharded(ials_session* s, ials_comm* comm, const ials_side* users, const ials_sched* user_sched,
+                       const ials_segs* user_segs, const ials_side* items, const ials_sched* item_sched,
+                       const ials_segs* item_segs, const int32_t* user_bounds, const int32_t* item_bounds,
+                       float* W, int32_t ldw, float* H, int32_t ldh, int32_t d, int32_t b, float alpha0,
+                       int32_t rotate, float* Cu, float* Ci, void* workspace, size_t ws_bytes, void* stream);
 
 /* Workspace bytes for ials_build_csr over n interactions. */
 size_t ials_build_csr_workspace_bytes(int64_t n);

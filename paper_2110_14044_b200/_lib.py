@@ -40,6 +40,11 @@ class IalsSched(ctypes.Structure):
                 ("n_deg_gt64", c_i32), ("n_deg_gt32", c_i32)]
 
 
+class IalsSegs(ctypes.Structure):
+    """``ials_segs`` (row segments the multi-GPU gather-dot kernels walk)."""
+    _fields_ = [("n", c_i32), ("row", c_p), ("beg", c_p), ("end", c_p)]
+
+
 #: every symbol include/ials_b200.h declares, with its ctypes signature
 SIGNATURES = {
     "ials_version": (c_i32, []),
@@ -110,6 +115,15 @@ SIGNATURES = {
     "ials_shard_user_pass_rot": (c_i32, [c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
                                          c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_f, c_p,
                                          c_p, c_sz, c_p, c_sz, c_p, c_sz, c_p]),
+    "ials_comm_unique_id": (c_i32, [c_p]),
+    "ials_comm_create": (c_i32, [c_p, c_p, c_i32, c_i32, ctypes.POINTER(c_p)]),
+    "ials_comm_destroy": (c_i32, [c_p]),
+    "ials_epoch_sharded_bytes": (c_sz, [c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
+    "ials_epoch_sharded": (c_i32, [c_p, c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),
+                                   ctypes.POINTER(IalsSegs), ctypes.POINTER(IalsSide),
+                                   ctypes.POINTER(IalsSched), ctypes.POINTER(IalsSegs), c_p, c_p,
+                                   c_p, c_i32, c_p, c_i32, c_i32, c_i32, c_f, c_i32, c_p, c_p, c_p,
+                                   c_sz, c_p]),
     "ials_topk": (c_i32, [c_p, c_i32, c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p]),
     "ials_build_csr": (c_i32, [c_p, c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                                c_p, c_sz, c_p]),

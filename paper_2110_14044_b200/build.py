@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     if not force and up_to_date(out):
         return out
     cmd = [nvcc(), *NVCC_FLAGS, *(["-DIALS_CHECKS"] if checked else []), "-o", out + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -783,17 +783,43 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
   if (p.n_light + p.n_heavy > 0) {
     // rows the cancellation checks rejected (light or heavy): FP32 SIMT sweep
     // over the device list (persistent grid, the count is read on the device)
-    static int simt_sm = 0;
-    if (simt_sm == 0) {
-      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<128>,
-                                                               L::NT * L::RPC, L::CTA_BYTES));
-      if (simt_sm < 1) simt_sm = 1;
-    }
+    // (at the block's own tile width: a 64- or 32-wide block redone in the
+    // 128 tile would do 4x / 16x the arithmetic)
     SweepParams q = p;
     q.light_rows = p.redo_rows;
     q.n_light_dev = p.redo_cnt;
     q.queue = p.redo_cnt + 4;   // zeroed with the redo count
-    k_sweep_light<128><<<simt_sm * kNumSMs, L::NT * L::RPC, L::CTA_BYTES, st>>>(q);
+    if (G == 1) {
+      static int simt_sm = 0;
+      if (simt_sm == 0) {
+        CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<128>,
+                                                                 L::NT * L::RPC, L::CTA_BYTES));
+        if (simt_sm < 1) simt_sm = 1;
+      }
+      k_sweep_light<128><<<simt_sm * kNumSMs, L::NT * L::RPC, L::CTA_BYTES, st>>>(q);
+    } else if (G == 2) {
+      using L64 = Lay<64>;
+      static int simt_sm = 0;
+      rc = set_smem_attrs<64>(s);
+      if (rc) return rc;
+      if (simt_sm == 0) {
+        CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<64>,
+                                                                 L64::NT * L64::RPC, L64::CTA_BYTES));
+        if (simt_sm < 1) simt_sm = 1;
+      }
+      k_sweep_light<64><<<simt_sm * kNumSMs, L64::NT * L64::RPC, L64::CTA_BYTES, st>>>(q);
+    } else {
+      using L32 = Lay<32>;
+      static int simt_sm = 0;
+      rc = set_smem_attrs<32>(s);
+      if (rc) return rc;
+      if (simt_sm == 0) {
+        CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<32>,
+                                                                 L32::NT * L32::RPC, L32::CTA_BYTES));
+        if (simt_sm < 1) simt_sm = 1;
+      }
+      k_sweep_light<32><<<simt_sm * kNumSMs, L32::NT * L32::RPC, L32::CTA_BYTES, st>>>(q);
+    }
     LAUNCH_CHECK(s);
   }
   if (p.n_light + p.n_slices > 0) {
@@ -2239,3 +2265,5 @@ int ials_loss_terms(ials_session* s, const ials_side* users, const ials_side* it
   return IALS_OK;
 }
 
+// ------------------------------------------------------------------ multi-GPU epoch
+#include "ials_shard_epoch.cuh"

@@ -299,6 +299,73 @@ class GpuOps:
         self.sess.check(rc, "shard_apply_block")
         return delta
 
+    # ---- the whole epoch behind the C ABI (ials_epoch_sharded): the same steps
+    # as ShardedTrainer.epoch over these ops, with NCCL collectives issued by
+    # the library on its own communicator (no Python between the kernels)
+    def make_comm(self, rank, world, group=None):
+        """The library's communicator over the ranks of ``group`` (collective:
+        rank 0's NCCL unique id travels by torch.distributed)."""
+        import ctypes
+        lib = self.sess.lib
+        idp = None
+        if world > 1:
+            ident = ctypes.create_string_buffer(128)
+            if rank == 0:
+                self.sess.check(lib.ials_comm_unique_id(ident), "comm_unique_id")
+            box = [ident.raw if rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=group)
+            ident = ctypes.create_string_buffer(box[0], 128)
+            idp = ctypes.cast(ident, ctypes.c_void_p)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            self.sess.check(lib.ials_comm_create(self.sess.handle, idp, rank, world, ctypes.byref(h)),
+                            "comm_create")
+        self._comm = h
+        self._comm_shape = (rank, world)
+        return h
+
+    def close_comm(self):
+        if getattr(self, "_comm", None):
+            self.sess.lib.ials_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close_comm()
+        except Exception:
+            pass
+
+    def epoch_native(self, us, is_, user_bounds, item_bounds, W, H, b, alpha0, rotate, Cu, Ci):
+        from . import _lib
+        from .engine import _ptr
+        import ctypes
+        lib = self.sess.lib
+        rank, world = self._comm_shape
+        du, di = self._dev(us), self._dev(is_)
+        su, si = du.schedule(b), di.schedule(b)
+        segs = []
+        for ds in (du, di):
+            n, r, bg, en = ds.segs
+            segs.append(_lib.IalsSegs(n, _ptr(r).value, _ptr(bg).value, _ptr(en).value))
+        I32 = ctypes.c_int32 * (world + 1)
+        ub = I32(*([lo for lo, _ in user_bounds] + [user_bounds[-1][1]]))
+        ib = I32(*([lo for lo, _ in item_bounds] + [item_bounds[-1][1]]))
+        d = W.shape[1]
+        nb = int(lib.ials_epoch_sharded_bytes(ub, ib, world, rank, d, b, max(su.n_slices, si.n_slices),
+                                              max(su.n_heavy, si.n_heavy)))
+        if nb == 0:
+            raise ValueError("epoch_sharded: bad bounds")
+        if getattr(self, "_ews", None) is None or self._ews.numel() < nb:
+            self._ews = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        rc = lib.ials_epoch_sharded(
+            self.sess.handle, self._comm, ctypes.byref(du.struct), ctypes.byref(su.struct),
+            ctypes.byref(segs[0]), ctypes.byref(di.struct), ctypes.byref(si.struct),
+            ctypes.byref(segs[1]), ub, ib, _ptr(W), W.stride(0), _ptr(H), H.stride(0), d, b,
+            float(alpha0), int(bool(rotate)), _ptr(Cu), _ptr(Ci), _ptr(self._ews),
+            self._ews.numel(), self._stream())
+        self.sess.check(rc, "epoch_sharded")
+
     def check(self):
         self.sess.raise_if_singular()
 
@@ -306,7 +373,7 @@ class GpuOps:
 class ShardedTrainer:
     """One rank's share of a sharded iALS++ run (call collectively on all ranks)."""
 
-    def __init__(self, data, W, H, alpha0, reg, exponent, ops, group=None):
+    def __init__(self, data, W, H, alpha0, reg, exponent, ops, group=None, native=None):
         self.ops = ops
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -336,6 +403,14 @@ class ShardedTrainer:
         # global facts the rotated-pass decision rests on (identical on every rank)
         self._max_user_degree = int(np.diff(up).max()) if U > 0 else 0
         self._unit = data.get("labels") is None and data.get("weights") is None
+        # the epoch behind the C ABI (ials_epoch_sharded, its own NCCL
+        # communicator) when the ops provide it; ``native=False`` / IALS_SHARD_NATIVE=0
+        # keeps the orchestration below in Python (the form the gloo tests cover)
+        import os
+        self.native = bool(native if native is not None else os.environ.get("IALS_SHARD_NATIVE", "1") != "0")
+        self.native = self.native and hasattr(ops, "epoch_native") and W.dtype == torch.float32
+        if self.native:
+            ops.make_comm(self.rank, self.world, group)
 
     # ---------------------------------------------------------------- comms
     def _allreduce(self, t):
@@ -378,6 +453,14 @@ class ShardedTrainer:
         no full-table pass remains per block."""
         W, H, ops = self.W, self.H, self.ops
         d = W.shape[1]
+        if self.native and block_size <= 256:
+            rot = (self.I > 0 and self.U > 0
+                   and ops.rot_supported(d, block_size, self._max_user_degree, self._unit)
+                   and 32 < block_size <= 128 and d % 4 == 0 and W.stride(0) % 4 == 0
+                   and H.stride(0) % 4 == 0)
+            ops.epoch_native(self.us, self.is_, self.user_bounds, self.item_bounds, W, H, block_size,
+                             self.alpha0, rot, self.Cu, self.Ci)
+            return
         ulo, uhi = self.user_bounds[self.rank]
         ilo, ihi = self.item_bounds[self.rank]
         Wl, Hl = W[ulo:uhi], H[ilo:ihi]

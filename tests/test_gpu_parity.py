@@ -234,12 +234,15 @@ def test_tensor_core_one_and_ten_epochs(ials, d, b):
     assert abs(reports[-1].loss - want10) / want10 < TOL
 
 
+@pytest.mark.parametrize("native", [False, True])
 @pytest.mark.parametrize("d,b", [(48, 16), (256, 128), (96, 48), (512, 128)])
-def test_sharded_path_gpu_ops_single_rank(ials, d, b):
+def test_sharded_path_gpu_ops_single_rank(ials, d, b, native):
     """The multi-GPU orchestration with the real kernels (GpuOps, fp32) at
     world size 1: local sides, the item-major cache C_i and the delta
     corrections (k_cache_correct) against the oracle; b = 128 takes the
-    shard tensor-core GEMMs (ials_shard_*) and the fused sweep."""
+    shard tensor-core GEMMs (ials_shard_*), the rotated user pass and the
+    fused sweep.  native: the epoch behind the C ABI (ials_epoch_sharded)
+    instead of the Python orchestration."""
     import torch
     from oracle import ialspp_oracle as orc
     from paper_2110_14044_b200.distributed import GpuOps, ShardedTrainer
@@ -252,13 +255,54 @@ def test_sharded_path_gpu_ops_single_rank(ials, d, b):
     w, h = w.astype(np.float32).astype(np.float64), h.astype(np.float32).astype(np.float64)
     W = torch.from_numpy(w.astype(np.float32)).cuda()
     H = torch.from_numpy(h.astype(np.float32)).cuda()
-    tr = ShardedTrainer(data, W, H, 0.1, 1e-3, 1.0, GpuOps("cuda:0"))
+    tr = ShardedTrainer(data, W, H, 0.1, 1e-3, 1.0, GpuOps("cuda:0"), native=native)
+    assert tr.native == native
     for _ in range(2):
         tr.epoch(b)
     cache = tr.gather_cache().double().cpu().numpy()
     ref_cache = orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
     assert relf(W.double().cpu().numpy(), w) < TOL and relf(H.double().cpu().numpy(), h) < TOL
     assert relmax(cache, ref_cache) < TOL
+
+
+@pytest.mark.parametrize("d,b,nccl", [(64, 16, False), (256, 128, False), (256, 128, True), (96, 48, True)])
+def test_sharded_native_epoch_equals_python_orchestration(ials, d, b, nccl):
+    """ials_epoch_sharded (the multi-GPU epoch behind the C ABI) launches the
+    same kernels in the same order as ShardedTrainer.epoch over GpuOps: W, H
+    and both caches bit-identical after two epochs.  nccl: through a real
+    one-rank NCCL communicator (ials_comm_unique_id / ials_comm_create: the
+    library's all-reduce and all-gather calls run) instead of the local one."""
+    import ctypes
+    import torch
+    from oracle import ialspp_oracle as orc
+    from paper_2110_14044_b200.distributed import GpuOps, ShardedTrainer
+    U, I, users, items = _heavy_instance(2100, 600, 40, 1.0, 13)
+    csr = orc.build_csr(U, I, users, items)
+    data = {"num_users": U, "num_items": I, "user_ptr": csr["user_ptr"], "user_cols": csr["items"],
+            "item_ptr": csr["item_ptr"], "item_cols": csr["users"][csr["item_order"]],
+            "item_order": csr["item_order"], "labels": None, "weights": None}
+    w, h = orc.init_factors(U, I, d, 0.1, 5)
+    out = []
+    for native in (False, True):
+        W = torch.from_numpy(w.astype(np.float32)).cuda()
+        H = torch.from_numpy(h.astype(np.float32)).cuda()
+        ops = GpuOps("cuda:0")
+        tr = ShardedTrainer(data, W, H, 0.1, 1e-3, 1.0, ops, native=native)
+        if native and nccl:   # swap the local communicator for a one-rank NCCL one
+            ops.close_comm()
+            ident = ctypes.create_string_buffer(128)
+            ops.sess.check(ops.sess.lib.ials_comm_unique_id(ident), "comm_unique_id")
+            hdl = ctypes.c_void_p()
+            ops.sess.check(ops.sess.lib.ials_comm_create(ops.sess.handle, ident, 0, 1, ctypes.byref(hdl)),
+                           "comm_create")
+            ops._comm = hdl
+        for _ in range(2):
+            tr.epoch(b)
+        torch.cuda.synchronize()
+        ops.check()
+        out.append((W.cpu(), H.cpu(), tr.Cu.cpu(), tr.Ci.cpu()))
+    for a, c in zip(*out):
+        assert torch.equal(a, c)
 
 
 @pytest.mark.parametrize("which", ["ials", "icd"])
