@@ -1549,6 +1549,18 @@ static cudaError_t rec_event(int k, cudaStream_t st) {
   return cudaSuccess;
 }
 
+// the eigendecompositions' side stream (highest priority: its CTAs take SMs as
+// the predictions' retire) and its fork / join events
+static int ensure_rot_stream(ials_session* s) {
+  if (s->rot_st) return IALS_OK;
+  int lo = 0, hi = 0;
+  CUDA_TRY(s, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CUDA_TRY(s, cudaStreamCreateWithPriority(&s->rot_st, cudaStreamNonBlocking, hi));
+  CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_rot0, cudaEventDisableTiming));
+  CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_rot1, cudaEventDisableTiming));
+  return IALS_OK;
+}
+
 // ------------------------------------------------------------------ epoch
 // host staging of ials_epoch_host (all pointers pinned host memory)
 struct EpochHost {
@@ -1827,12 +1839,9 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     return IALS_OK;
   };
   auto launch_eig = [&]() -> int {   // after H's K-major copy is current on st
-    if (!s->rot_st) {   // highest priority: its CTAs take SMs as the predictions' retire
-      int lo = 0, hi = 0;
-      CUDA_TRY(s, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      CUDA_TRY(s, cudaStreamCreateWithPriority(&s->rot_st, cudaStreamNonBlocking, hi));
-      CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_rot0, cudaEventDisableTiming));
-      CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_rot1, cudaEventDisableTiming));
+    {
+      const int rc0 = ensure_rot_stream(s);
+      if (rc0) return rc0;
     }
     for (int z = 0; z < nblk; ++z)
       if (!s->ev_blk[z]) CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_blk[z], cudaEventDisableTiming));

@@ -271,10 +271,17 @@ int ials_epoch_sharded(ials_session* s, ials_comm* comm, const ials_side* users,
   if (rotate && !rot)
     return fail(s, IALS_E_INVALID, "epoch_sharded: rotate set but the rotated pass does not apply "
                                    "(b = 128 | d, unit weights, no heavy user rows)");
+  // (on the session's high-priority side stream, beside the two prediction
+  // passes below; the first user pass waits for it)
   ShardRot sr{};
   if (rot) {
     rc = shard_rot_carve(s, w.rot, w.rot_bytes + 1024, nu, I, d, b, &sr);
+    if (!rc) rc = ensure_rot_stream(s);
     if (rc) return rc;
+    CUDA_TRY(s, cudaEventRecord(s->ev_rot0, st));   // H_loc's K-major copy is current
+    CUDA_TRY(s, cudaStreamWaitEvent(s->rot_st, s->ev_rot0, 0));
+    cudaStream_t main_st = st;
+    st = s->rot_st;
     if (ni == 0) {
       CUDA_TRY(s, cudaMemsetAsync(w.gd, 0, size_t(d) * b * 4, st));
     } else {
@@ -292,12 +299,15 @@ int ials_epoch_sharded(ials_session* s, ials_comm* comm, const ials_side* users,
           ch.P, ch.S, (long long)d * b, cnt, w.gd);
       LAUNCH_CHECK(s);
     }
+    CUDA_TRY(s, cudaEventRecord(comm->ev_go, st));   // the shard's split-partial scratch is free again
     rc = allreduce(w.gd, size_t(d) * b);
     if (!rc) rc = eig_attrs(s, b);
     if (rc) return rc;
     k_sym_eig<<<d / b, kEigThreads, eig_smem_bytes(b), st>>>(w.gd, b, (long long)b * b, b, sr.QT, sr.lam, sr.rslab,
                                                              sr.Qm, nullptr, 1);
     LAUNCH_CHECK(s);
+    CUDA_TRY(s, cudaEventRecord(s->ev_rot1, st));
+    st = main_st;
   }
   // both caches from the current factors
   rc = predictions_impl(s, user_segs->n, Items{nullptr, user_segs->row, user_segs->beg, user_segs->end},
@@ -387,8 +397,10 @@ int ials_epoch_sharded(ials_session* s, ials_comm* comm, const ials_side* users,
   };
 
   int prev_b0 = -1, prev_bb = 0;
+  if (rot) CUDA_TRY(s, cudaStreamWaitEvent(st, comm->ev_go, 0));   // (the diagonal GEMM used ch.P)
   rc = gram(Hl, ldh, ni, ch, 0, std::min(b, d), w.g_h);
   if (rc) return rc;
+  if (rot) CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_rot1, 0));   // the decompositions
   for (int b0 = 0; b0 < d; b0 += b) {
     const int bb = std::min(b, d - b0);
     // ---- user pass
