@@ -608,6 +608,18 @@ static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, ui
 
 // BT = 128, b > 32: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
 // heavy rows on the SIMT slice kernels.
+static int wb_attrs(ials_session* s) {
+  static unsigned winit = 0;
+  if (!(winit & dev_bit())) {
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, WbLay<2>::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, WbLay<4>::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    winit |= dev_bit();
+  }
+  return IALS_OK;
+}
+
 static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz, cudaStream_t st) {
   using L = Lay<128>;
   const bool unit = !p.side.weights && !p.side.labels;   // all ones: not staged
@@ -684,8 +696,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         if (rc) return rc;
         q.light_rows = cp->rows;
         q.chunk_tot = cp->tot;
-        q.chunk = c;
-        if (c > 0) CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt + 2, 0, sizeof(int), st));   // row queue
+        q.chunk = p.rot ? 3 * c : c;   // rotated: buckets (chunk, class) of the grouped list
+        // the row queues [2], [5], [6] (and the idle [3], [4]) start over for every chunk
+        if (c > 0) CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt + 2, 0, 5 * sizeof(int), st));
       }
       if (n_b == 0) {
       } else if (G == 1) {
@@ -705,16 +718,27 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           k_sweep_pk<4, false><<<grid, 128, PkLay<4>::BYTES, st>>>(q, fmap, use_tma);
       }
       if (n_b > 0) LAUNCH_CHECK(s);
-    }
-    if (p.rot) {
-      static unsigned winit = 0;
-      if (!(winit & dev_bit())) {
-        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, WbLay<2>::BYTES));
-        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, WbLay<4>::BYTES));
-        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_wb<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        winit |= dev_bit();
+      if (cp && p.rot) {   // this chunk's Woodbury tiles (bucket sizes on the device)
+        rc = wb_attrs(s);
+        if (rc) return rc;
+        SweepParams qw = p;
+        qw.light_rows = cp->rows;
+        const int n2 = p.rot_n32 - p.rot_n64, n4 = p.n_light - p.rot_n32;   // upper bounds
+        if (n2 > 0) {
+          k_sweep_wb<2><<<std::min((n2 + 1) / 2, 4 * kNumSMs), 128, WbLay<2>::BYTES, st>>>(
+              qw, 0, 0, p.redo_cnt + 5, cp->tot, 3 * c + 1);
+          LAUNCH_CHECK(s);
+        }
+        if (n4 > 0) {
+          k_sweep_wb<4><<<std::min((n4 + 3) / 4, 4 * kNumSMs), 128, WbLay<4>::BYTES, st>>>(
+              qw, 0, 0, p.redo_cnt + 6, cp->tot, 3 * c + 2);
+          LAUNCH_CHECK(s);
+        }
       }
+    }
+    if (p.rot && !cp) {
+      rc = wb_attrs(s);
+      if (rc) return rc;
       const int n2 = p.rot_n32 - p.rot_n64, n4 = p.n_light - p.rot_n32;
       if (n2 > 0) {
         k_sweep_wb<2><<<std::min((n2 + 1) / 2, 4 * kNumSMs), 128, WbLay<2>::BYTES, st>>>(p, p.rot_n64, n2, p.redo_cnt + 5);
@@ -1897,7 +1921,11 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   const int nl = user_sched->n_light;
   const size_t part_need = 4 * al256(size_t(std::max(nl, 1)) * 4) +
                            al256(size_t((nl + kRadixTile - 1) / kRadixTile + 1) * 256 * 4) + al256(256 * 4);
-  bool chunked = host && tc_gemm && nl > 0 && kChunks > 1 && U >= kChunks && !rot;
+  // (rotated first pass: the grouped list is bucketed by (chunk, row class) and
+  // each chunk runs its own b x b sweep and Woodbury tiles; IALS_HOST_CHUNKS_ROT=0
+  // keeps the rotated first pass whole)
+  static const bool kChunkRot = !(getenv("IALS_HOST_CHUNKS_ROT") && getenv("IALS_HOST_CHUNKS_ROT")[0] == '0');
+  bool chunked = host && tc_gemm && nl > 0 && kChunks > 1 && U >= kChunks && (!rot || (kChunkRot && b == 128));
   if (chunked) {
     int su, spu, si, spi;
     gram_plan(std::max(users->n_rows, 1), d, &su, &spu);
@@ -1909,6 +1937,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     CUDA_TRY(s, cudaEventRecord(s->ev_b, s->copy_st));   // H is on the device
     CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_b, 0));
     rc = sync_copies(s, H, ldh, d, 0, d, ch, st);
+    if (!rc && rot) rc = launch_eig();   // the decompositions overlap W's upload
     if (rc) return rc;
     char* t = reinterpret_cast<char*>(P);
     int* keys = reinterpret_cast<int*>(t);
@@ -1927,9 +1956,12 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     plan.tot = tot;
     plan.prologue = [&, st, keys, skeys, idx, grouped, tot, hist](int c) -> int {
       if (c == 0) {   // after block 0's H Gramian, the last user of P before the sweep
-        k_chunk_keys<<<(nl + 255) / 256, 256, 0, st>>>(user_sched->light_rows, nl, per_chunk, keys);
+        if (rot)
+          k_chunk_class_keys<<<(nl + 255) / 256, 256, 0, st>>>(user_sched->light_rows, users->ptr, nl, per_chunk, keys);
+        else
+          k_chunk_keys<<<(nl + 255) / 256, 256, 0, st>>>(user_sched->light_rows, nl, per_chunk, keys);
         LAUNCH_CHECK(s);
-        int r = radix_sort_index(s, keys, nl, kChunks, skeys, idx, skeys, idx, hist, tot, st);
+        int r = radix_sort_index(s, keys, nl, rot ? 3 * kChunks : kChunks, skeys, idx, skeys, idx, hist, tot, st);
         if (r) return r;
         k_gather_i32<<<(nl + 255) / 256, 256, 0, st>>>(user_sched->light_rows, idx, nl, grouped);
         LAUNCH_CHECK(s);
@@ -1945,6 +1977,14 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
       if (r) return r;
       TcCopies part = cw;
       part.n = r1 - r0;
+      if (rot) {   // the chunk's rotated projection and its rows of W[:, pi] Q (block 0)
+        r = proj_tc(s, W + size_t(r0) * ldw, ldw, part, d, b, rw.slabQT, nullptr, alpha0,
+                    reinterpret_cast<float*>(pws) + size_t(r0) * b, st);
+        if (!r)
+          r = gemm_nt(s, W + size_t(r0) * ldw, r1 - r0, d, ldw, 0, rw.QT, b, b, b, 0, b,
+                      rw.WQ + size_t(r0) * b, b, 1.f, false, st);
+        return r;
+      }
       return proj_tc(s, W + size_t(r0) * ldw, ldw, part, d, std::min(b, d), sth, stl, alpha0,
                      reinterpret_cast<float*>(pws) + size_t(r0) * std::min(b, d), st);
     };
@@ -1997,10 +2037,13 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
         // (slab Q)^T = Q^T slab^T -> the rotated projection alpha0 W slab Q;
         // F~ = H[:, pi] Q and W[:, pi] Q
         const float* qt = rw.QT + size_t(zb) * b * b;
+        // (a chunked first pass forms its rows' projection and W Q chunk by chunk)
         rc = gemm_nt(s, qt, b, b, b, 0, slab, d, bb, bb, 0, b, rw.slabQT, d, 1.f, false, st);
-        if (!rc) rc = proj_tc(s, W, ldw, cw, d, bb, rw.slabQT, nullptr, alpha0, reinterpret_cast<float*>(pws), st);
+        if (!rc && !first_chunked)
+          rc = proj_tc(s, W, ldw, cw, d, bb, rw.slabQT, nullptr, alpha0, reinterpret_cast<float*>(pws), st);
         if (!rc) rc = gemm_nt(s, H, items->n_rows, d, ldh, b0, qt, b, b, b, 0, b, rw.Ft, b, 1.f, false, st);
-        if (!rc) rc = gemm_nt(s, W, users->n_rows, d, ldw, b0, qt, b, b, b, 0, b, rw.WQ, b, 1.f, false, st);
+        if (!rc && !first_chunked)
+          rc = gemm_nt(s, W, users->n_rows, d, ldw, b0, qt, b, b, b, 0, b, rw.WQ, b, 1.f, false, st);
       } else if (!rc && !first_chunked) {
         rc = proj_tc(s, W, ldw, cw, d, bb, sth, stl, alpha0, reinterpret_cast<float*>(pws), st);
       }

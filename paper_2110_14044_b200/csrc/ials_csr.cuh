@@ -158,6 +158,18 @@ __global__ void k_chunk_keys(const int* __restrict__ rows, int n, int per, int* 
   if (k < n) keys[k] = __ldg(rows + k) / per;
 }
 
+// the same with the rotated pass's three row classes inside every chunk:
+// key = 3 * chunk + (0: more than 64 entries, 1: 33..64, 2: at most 32)
+__global__ void k_chunk_class_keys(const int* __restrict__ rows, const int* __restrict__ ptr, int n, int per,
+                                   int* __restrict__ keys) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) {
+    const int r = __ldg(rows + k);
+    const int deg = __ldg(ptr + r + 1) - __ldg(ptr + r);
+    keys[k] = 3 * (r / per) + (deg > 64 ? 0 : (deg > 32 ? 1 : 2));
+  }
+}
+
 __global__ void k_iota_i32(int64_t n, int* __restrict__ dst) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) dst[k] = (int)k;

@@ -104,9 +104,18 @@ IALS_DEVI int butterfly16_col(int lane) {
 // rows lrows[row0 ..) in tiles of G (all with n <= NG): the rotated pass's
 // fixed side F~ (n_fixed x 128, ld 128) is p.fixed, the rotated projection p~
 // is p.proj, W[:, pi] Q is p.wq, alpha0 * eigenvalues p.rot_lam; d~ -> drow
+// (tot / bucket: the host epoch's chunked first pass -- the rows are bucket
+// `bucket` of the grouped light list, whose bucket sizes tot[] live on the device)
 template <int G>
-__global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, int n_rows, int* queue) {
+__global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, int n_rows, int* queue,
+                                                     const int* tot = nullptr, int bucket = 0) {
   using L = WbLay<G>;
+  if (tot) {
+    int off = 0;
+    for (int k = 0; k < bucket; ++k) off += tot[k];
+    row0 = off;
+    n_rows = tot[bucket];
+  }
   constexpr int B = L::B;
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = tc_smem_base(smem_raw);

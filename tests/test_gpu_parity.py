@@ -424,7 +424,7 @@ def test_wider_last_block_matches_oracle(ials):
         assert relf(got, want) < TOL and relmax(got, want) < TOL
 
 
-@pytest.mark.parametrize("d,b", [(16, 8), (128, 128), (96, 48)])
+@pytest.mark.parametrize("d,b", [(16, 8), (128, 128), (96, 48), (256, 128)])
 def test_dropin_host64_bit_identical_to_device_epoch(ials, d, b):
     """ialspp_epoch on the caller's float64 NumPy model (ials_epoch_host64:
     f64 copies + casts on the GPU, overlapped with the epoch) equals the
