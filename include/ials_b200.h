@@ -350,6 +350,9 @@ int ials_shard_user_pass_rot(ials_session* s, const ials_side* side, const ials_
  * With id == NULL and world == 1 the communicator is local (no NCCL). */
 int ials_comm_unique_id(void* id128);
 int ials_comm_create(ials_session* s, const void* id128, int32_t rank, int32_t world, ials_comm** out);
+/* The same over a communicator the host already has (nccl_comm: its ncclComm_t
+ * on this session's device); ials_comm_destroy then leaves it alive. */
+int ials_comm_wrap(ials_session* s, void* nccl_comm, int32_t rank, int32_t world, ials_comm** out);
 int ials_comm_destroy(ials_comm* c);
 
 /* One rank's share of an iALS++ epoch (ialspp_epoch, solvers.py:340-375),

@@ -117,6 +117,7 @@ SIGNATURES = {
                                          c_p, c_sz, c_p, c_sz, c_p, c_sz, c_p]),
     "ials_comm_unique_id": (c_i32, [c_p]),
     "ials_comm_create": (c_i32, [c_p, c_p, c_i32, c_i32, ctypes.POINTER(c_p)]),
+    "ials_comm_wrap": (c_i32, [c_p, c_p, c_i32, c_i32, ctypes.POINTER(c_p)]),
     "ials_comm_destroy": (c_i32, [c_p]),
     "ials_epoch_sharded_bytes": (c_sz, [c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
     "ials_epoch_sharded": (c_i32, [c_p, c_p, ctypes.POINTER(IalsSide), ctypes.POINTER(IalsSched),

@@ -61,6 +61,7 @@ static const NcclApi* nccl_api() {
 
 struct ials_comm {
   void* nccl = nullptr;        // ncclComm_t (null at world size 1 without NCCL)
+  bool owned = true;           // created here (ials_comm_create) or the host's own (ials_comm_wrap)
   int rank = 0, world = 1, device = 0;
   cudaStream_t st = nullptr;   // the all-gathers' stream
   cudaEvent_t ev_go = nullptr, ev_done = nullptr;
@@ -115,12 +116,35 @@ int ials_comm_create(ials_session* s, const void* id128, int32_t rank, int32_t w
   return IALS_OK;
 }
 
+// the host's own ncclComm_t (ials_set_comm): not destroyed with the wrapper
+int ials_comm_wrap(ials_session* s, void* nccl_comm, int32_t rank, int32_t world, ials_comm** out) {
+  DevGuard _dg(s);
+  if (!s || !out || !nccl_comm || world < 1 || rank < 0 || rank >= world)
+    return fail(s, IALS_E_INVALID, "comm_wrap: bad arguments (rank %d of %d)", rank, world);
+  if (!nccl_api()) return fail(s, IALS_E_CUDA, "comm_wrap: libnccl.so.2 not found");
+  ials_comm* c = new ials_comm;
+  c->nccl = nccl_comm;
+  c->owned = false;
+  c->rank = rank;
+  c->world = world;
+  c->device = s->device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_go, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    ials_comm_destroy(c);
+    return fail(s, IALS_E_CUDA, "comm_wrap: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return IALS_OK;
+}
+
 int ials_comm_destroy(ials_comm* c) {
   if (!c) return IALS_OK;
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
-  if (c->nccl && nccl_api()) nccl_api()->CommDestroy(c->nccl);
+  if (c->nccl && c->owned && nccl_api()) nccl_api()->CommDestroy(c->nccl);
   if (c->ev_go) cudaEventDestroy(c->ev_go);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->st) cudaStreamDestroy(c->st);
