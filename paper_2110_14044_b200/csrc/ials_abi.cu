@@ -44,6 +44,14 @@ struct ials_session {
   unsigned long long* err;  // device error word (ULLONG_MAX = clean)
   unsigned long long* redo; // rows the fused tensor-core sweep handed to SIMT
   const struct ChunkPlan* chunk = nullptr;   // set by ials_epoch_host around its first user pass
+  // ials_epoch: a pass's entry-parallel cache update runs on its own stream beside
+  // the NEXT pass's GEMM phase (slab, projection, K-major copies: none of them
+  // touches the cache or the pass's per-row steps); the next sweep joins it
+  cudaStream_t cache_st = nullptr;
+  cudaEvent_t ev_cache_go = nullptr, ev_cache_done = nullptr;
+  bool defer_cache = false;     // set by the epoch around a side pass whose layout allows it
+  bool cache_pending = false;   // a deferred cache update has not been joined yet
+  float* last_drow = nullptr;   // the per-row steps of the last side pass (the back-rotation's input)
   char msg[512];
 };
 
@@ -225,11 +233,16 @@ int ials_check_singular(ials_session* s, void* stream, int64_t* row, int32_t* pi
 // Rows longer than the threshold are split into slices (partial Hessians
 // reduced in a fixed order): a one-warp row team at small block widths is
 // latency-bound on long rows, so it splits them early.
+// (IALS_HEAVY / IALS_SLICE override both for every width: measurements)
 int64_t ials_heavy_threshold(int32_t b) {
+  static const long long ov = getenv("IALS_HEAVY") ? atoll(getenv("IALS_HEAVY")) : 0;
+  if (ov > 0) return ov;
   const int bt = block_tile(b);
   return bt <= 16 ? 512 : bt == 32 ? 1024 : 4096;
 }
 int64_t ials_slice_len(int32_t b) {
+  static const long long ov = getenv("IALS_SLICE") ? atoll(getenv("IALS_SLICE")) : 0;
+  if (ov > 0) return ov;
   const int bt = block_tile(b);
   return bt <= 16 ? 256 : bt == 32 ? 512 : (bt == 256 ? 1024 : 2048);
 }
@@ -608,6 +621,15 @@ static int make_gather_map(ials_session* s, CUtensorMap* m, const float* ptr, ui
 
 // BT = 128, b > 32: fused tensor-core light rows (k_sweep_tc4, 4 CTAs/SM),
 // heavy rows on the SIMT slice kernels.
+// the caller's stream waits for a deferred cache update (see ials_session)
+static int join_cache(ials_session* s, cudaStream_t st) {
+  if (s->cache_pending) {
+    CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_cache_done, 0));
+    s->cache_pending = false;
+  }
+  return IALS_OK;
+}
+
 static int wb_attrs(ials_session* s) {
   static unsigned winit = 0;
   if (!(winit & dev_bit())) {
@@ -847,21 +869,36 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
     LAUNCH_CHECK(s);
   }
   if (p.n_light + p.n_slices > 0) {
+    cudaStream_t cst = st;
+    if (s->defer_cache) {   // beside the next pass's GEMM phase; joined by the next sweep
+      if (!s->cache_st) {
+        CUDA_TRY(s, cudaStreamCreateWithFlags(&s->cache_st, cudaStreamNonBlocking));
+        CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_cache_go, cudaEventDisableTiming));
+        CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_cache_done, cudaEventDisableTiming));
+      }
+      CUDA_TRY(s, cudaEventRecord(s->ev_cache_go, st));
+      CUDA_TRY(s, cudaStreamWaitEvent(s->cache_st, s->ev_cache_go, 0));
+      cst = s->cache_st;
+    }
     if (p.side.rows && nnz > 0) {   // entry-parallel: no per-row setup, full load balance
       const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);
       // walk the other side's order when this side's d is the smaller gather
       const bool swap = p.x_rows && p.x_cols && p.side.n_rows < p.side.n_fixed;
       if (swap) {
-        if (p.vec) k_pass_cache_flat<true, 8, true><<<(int)g, 256, 0, st>>>(p, nnz);
-        else k_pass_cache_flat<false, 8, true><<<(int)g, 256, 0, st>>>(p, nnz);
+        if (p.vec) k_pass_cache_flat<true, 8, true><<<(int)g, 256, 0, cst>>>(p, nnz);
+        else k_pass_cache_flat<false, 8, true><<<(int)g, 256, 0, cst>>>(p, nnz);
       } else {
-        if (p.vec) k_pass_cache_flat<true, 8, false><<<(int)g, 256, 0, st>>>(p, nnz);
-        else k_pass_cache_flat<false, 8, false><<<(int)g, 256, 0, st>>>(p, nnz);
+        if (p.vec) k_pass_cache_flat<true, 8, false><<<(int)g, 256, 0, cst>>>(p, nnz);
+        else k_pass_cache_flat<false, 8, false><<<(int)g, 256, 0, cst>>>(p, nnz);
       }
     } else {
-      k_pass_cache<<<p.n_light + p.n_slices, 256, 0, st>>>(p);
+      k_pass_cache<<<p.n_light + p.n_slices, 256, 0, cst>>>(p);
     }
     LAUNCH_CHECK(s);
+    if (s->defer_cache) {
+      CUDA_TRY(s, cudaEventRecord(s->ev_cache_done, s->cache_st));
+      s->cache_pending = true;
+    }
   }
   return IALS_OK;
 }
@@ -981,9 +1018,18 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
                           int32_t b0, int32_t b, const float* slab, float alpha0, float* cache,
                           int32_t side_id, char* ws, size_t ws_bytes, cudaStream_t st,
                           bool proj_ready = false, const float* proj_in = nullptr,
-                          const ials_side* other = nullptr, const RotPass* rot = nullptr) {
+                          const ials_side* other = nullptr, const RotPass* rot = nullptr,
+                          size_t defer_min_off = 0) {
+  // defer_min_off > 0 (ials_epoch): this pass's cache update may run beside the
+  // next pass's GEMM phase, whose projection overwrites the first defer_min_off
+  // bytes of the scratch: the per-row steps it reads are kept above them
   if (!side || !sched || !fixed || !own || !slab || !cache)
     return fail(s, IALS_E_INVALID, "side_pass: NULL argument");
+  {
+    const int jr = join_cache(s, st);   // the previous pass's deferred cache update
+    if (jr) return jr;
+  }
+  s->defer_cache = false;
   if (d < 1 || b < 1 || b0 < 0 || b0 + b > d || ldf < d || ldo < d)
     return fail(s, IALS_E_INVALID, "side_pass: bad block (d=%d b0=%d b=%d)", d, b0, b);
   const int bt = block_tile(b);
@@ -1033,7 +1079,18 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
   p.redo_cnt = reinterpret_cast<int*>(w);
   p.redo_rows = reinterpret_cast<int*>(w + 32);   // [0..7]: redo count, work queues
   w += al256(size_t(side->n_rows) * 4 + 32);
+  if (defer_min_off && bt == 128 && b > 16 && tc4_enabled()) {
+    // (only the fused tensor-core path has the separate cache kernel)
+    char* dr = std::max(w, ws + al256(defer_min_off));
+    const size_t tail = al256(size_t(side->n_rows) * b * 4) +
+                        (b <= kCompactMaxB ? al256(size_t(side->n_fixed) * compact_ld(b) * 4) : 0);
+    if (size_t(dr - ws) + tail <= ws_bytes) {
+      w = dr;
+      s->defer_cache = true;
+    }
+  }
   p.drow = reinterpret_cast<float*>(w);
+  s->last_drow = p.drow;
   w += al256(size_t(side->n_rows) * b * 4);
   if (b <= kCompactMaxB && side->n_fixed > 0) {
     // gather from a compact, L2-resident copy of fixed[:, b0:b0+b]
@@ -1908,7 +1965,11 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     if (rc) return rc;
   }
   CUDA_TRY(s, rec_event(0, st));
-  int rc = IALS_OK;
+  int rc = join_cache(s, st);   // (a failed earlier call may have left one pending)
+  if (rc) return rc;
+  // a pass's cache update beside the next pass's GEMM phase (IALS_DEFER_CACHE=0: in line)
+  static const bool kDefer = !(getenv("IALS_DEFER_CACHE") && getenv("IALS_DEFER_CACHE")[0] == '0');
+  const bool defer = kDefer && tc_gemm;
   // Host staging with the fused sweep: the first user pass runs chunk by
   // chunk of user rows, each chunk's sweep starting once its rows of W have
   // landed (with its predictions and projection), instead of after all of W.
@@ -2054,11 +2115,12 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     CUDA_TRY(s, rec_event(ek++, st));
     if (first_chunked) s->chunk = &plan;
     rc = side_pass_impl(s, users, user_sched, H, ldh, W, ldw, d, b0, bb, slab, alpha0, cache, 0,
-                        pws, pbytes, st, tc_gemm, nullptr, items, rot_u ? &rp : nullptr);
+                        pws, pbytes, st, tc_gemm, nullptr, items, rot_u ? &rp : nullptr,
+                        defer ? al256(size_t(items->n_rows) * b * 4) : 0);
     s->chunk = nullptr;
     if (rc) return rc;
     if (rot_u) {   // W[:, pi] -= d~ Q^T: the rows' steps back in the original basis
-      rc = gemm_nt(s, pass_drow(pws, users, user_sched, bb), users->n_rows, b, b, 0,
+      rc = gemm_nt(s, s->last_drow, users->n_rows, b, b, 0,
                    rw.Qm + size_t(zb) * b * b, b, b, b, 0, b, W + b0, ldw, -1.f, true, st);
       if (rc) return rc;
     }
@@ -2081,7 +2143,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     if (rc) return rc;
     CUDA_TRY(s, rec_event(ek++, st));
     rc = side_pass_impl(s, items, item_sched, W, ldw, H, ldh, d, b0, bb, slab, alpha0, cache, 1,
-                        pws, pbytes, st, tc_gemm, nullptr, users);
+                        pws, pbytes, st, tc_gemm, nullptr, users, nullptr,
+                        defer ? al256(size_t(users->n_rows) * b * 4) : 0);
     if (rc) return rc;
     if (host) {
       rc = host_cols_out(s, st, host, host->H_out, host->ldh, H, ldh, items->n_rows, d, b0, bb,
@@ -2098,6 +2161,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
     }
     CUDA_TRY(s, rec_event(ek++, st));
   }
+  rc = join_cache(s, st);   // the last pass's cache update
+  if (rc) return rc;
   if (rot) {   // the caller's stream covers the side stream's use of the workspace
     CUDA_TRY(s, cudaEventRecord(s->ev_rot1, s->rot_st));
     CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_rot1, 0));

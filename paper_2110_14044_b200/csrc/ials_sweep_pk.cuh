@@ -278,7 +278,10 @@ IALS_DEVI void pk_accumulate(const SweepParams& p, char* smem, PkState& st, doub
 // (tc4_factor with per-slot diagonal warps, per-slot shared state and
 // full-width trailing MMAs).  Returns with packed L (per slot), 1/pivots in
 // OFF_ID and the forward-solved right-hand side in OFF_YF.
-template <int G, class L = PkLay<G>>
+// UNIT_DIAG (the Woodbury tiles): the matrices in TMEM are C - I; the identity
+// is added to a diagonal entry when its own row reads it for its panel (the
+// trailing updates are additive, and nothing else reads the diagonal).
+template <int G, class L = PkLay<G>, bool UNIT_DIAG = false>
 IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t row_addr, int tid,
                          const int b) {
   float* ys = reinterpret_cast<float*>(smem + L::OFF_Y);
@@ -300,6 +303,11 @@ IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t
     float v[8];
     tmem_ld8(row_addr + g * L::NG + c0, v);
     tmem_wait_ld();
+    if (UNIT_DIAG) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (c0 + j == i) v[j] += 1.f;
+    }
     if (warp == ((g * L::NG + c0) >> 5)) {   // this warp holds slot g's diagonal block
       const int base = (g * L::NG + c0) & 31;
       float* SG = reinterpret_cast<float*>(smem + L::OFF_LI) + g * 80;   // free until the backward solve

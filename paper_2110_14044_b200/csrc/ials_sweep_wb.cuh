@@ -14,17 +14,16 @@
 //
 // Thread t = g * NG + k <-> TMEM lane t <-> entry k of slot g (k < n_g <= NG).
 //   pass 1  per 16-column chunk of b: each thread loads its entry's 16 values
-//           of F~ (L2-resident, 64 B), forms y = s x, the chunk's hi/lo
-//           operand row and its share of Y^T rho (a warp butterfly gives the
-//           per-column sums); one thread issues C += Y_c Y_c^T (M = N = 128,
+//           of F~ (L2-resident, 64 B), forms y = s x and the chunk's hi/lo
+//           operand row; one thread issues C += Y_c Y_c^T (M = N = 128,
 //           K = 16, 3xTF32) into TMEM initialised to I;
-//   z = s p~ + Y^T rho (fp64); u = Y z = Y (s p~) + Y Y^T rho: the first
-//   term accumulates in pass 1 (each thread's own entry), the second is
-//   (C - I) rho from the thread's TMEM row of C, so the row is read only
-//   twice; the blocked Cholesky of the G matrices C and the solves (the
-//   packed sweep's, on the max(n_g) leading rows); pass 2: Y^T v by the same
-//   butterfly, then d~ = s z - s^2 (X^T v) -> drow (the back-rotation GEMM
-//   applies Q).  (u = Y q + (C - I) rho carries the 3xTF32 error of C times
+//   u = Y z = Y (s p~) + Y Y^T rho: the first term accumulates in pass 1
+//   (each thread's own entry), the second is (C - I) rho from the thread's
+//   TMEM row of C -- z itself is never formed; the blocked Cholesky of the G
+//   matrices C and the solves (the packed sweep's, on the max(n_g) leading
+//   rows); pass 2: d~ = s z - s^2 X^T v = s^2 (p~ - X^T (v - rho)), the one
+//   transposed product by a warp butterfly per 16 columns -> drow (the
+//   back-rotation GEMM applies Q).  (u = Y q + (C - I) rho carries the 3xTF32 error of C times
 //   |rho| instead of |z|: ~1e-7 absolute on d, far inside 1e-3 of the rows.)
 // Work per row: 2 n_r b loads from L2 and an n_r/8-panel chain.
 #pragma once
@@ -196,18 +195,10 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       SZ[s * B + tid] = (float)((double)sv * (double)sv * pt);
     }
     reinterpret_cast<float*>(smem + L::OFF_RHO)[tid] = rho;
-    {  // TMEM := I
-#pragma unroll 1
-      for (int c8 = 0; c8 < 16; ++c8) {
-        float w8[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) w8[j] = (8 * c8 + j == tid) ? 1.f : 0.f;
-        tmem_st8(row_addr + 8 * c8, w8);
-      }
-      tmem_wait_st();
-    }
+    // (TMEM is not initialised: the tile's first MMA overwrites it, and it holds
+    // Y Y^T = C - I; the factorisation adds the identity as it reads the diagonal)
     tc_fence_before();
-    __syncthreads();   // S, Z visible; TMEM initialised
+    __syncthreads();   // S, Z visible; the previous tile's TMEM reads are done
     // ---- pass 1: C += Y_c Y_c^T, Y^T rho
     float x[16], xn[16];
     auto load16 = [&](float (&v)[16], int c0) {   // two 32-byte loads (rows are 512 B aligned)
@@ -238,13 +229,6 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
         y[j] = x[j] * S[g * B + c0 + j];
         uq = fmaf(x[j], SZ[g * B + c0 + j], uq);
         yy = fmaf(y[j], y[j], yy);
-      }
-      {
-        float zr[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) zr[j] = y[j] * rho;
-        const float cs = butterfly16(zr, lane);
-        if (!(lane & 1)) ZP[warp * B + c0 + butterfly16_col(lane)] = cs;
       }
       if (pend & (1u << ob)) {   // buffer ob was read by chunk ch - 2's MMAs
         mbar_wait(bar + ob, (st.ph >> ob) & 1u);
@@ -277,7 +261,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
         for (int ks = 0; ks < 2; ++ks) {
           const uint64_t ah = make_sdesc(hi + ks * 256, 128, 512, kSwizzleNone);
           const uint64_t al = make_sdesc(lo + ks * 256, 128, 512, kSwizzleNone);
-          umma_tf32(st.tmem, ah, ah, idesc, 1);
+          umma_tf32(st.tmem, ah, ah, idesc, (ch | ks) != 0);   // the tile's first MMA overwrites
           umma_tf32(st.tmem, ah, al, idesc, 1);
           umma_tf32(st.tmem, al, ah, idesc, 1);
         }
@@ -294,14 +278,6 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
         st.ph ^= 1u << ob;
       }
     tc_fence_after();
-    // z = s p~ + Y^T rho (the slot's warps' partials), column tid of every slot
-#pragma unroll
-    for (int s = 0; s < G; ++s) {
-      float part = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4 / G; ++w) part += ZP[(s * (4 / G) + w) * B + tid];
-      Z[s * B + tid] += (double)part;
-    }
     const int task_next = *next;
     int nrow = -1;
     if (tid < G && task_next < n_tiles) nrow = tile_row(task_next, tid);
@@ -324,14 +300,16 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     __syncthreads();
     // ---- v = C^-1 u on the leading nmax rows of every slot
     const int nb = (nmax + 7) & ~7;
-    pk_factor<G, L>(p, smem, st, row_addr, tid, nb);
+    pk_factor<G, L, true>(p, smem, st, row_addr, tid, nb);
     if (tid < G && task_next < n_tiles) put_tile(tb ^ 1, tid, nrow);
     pk_block_inverses<G, L>(smem, tid, nb);
     __syncthreads();
     pk_backward<G, L>(smem, tid, nb);
-    // ---- pass 2: X^T v (butterfly per 16 columns), d~ = s z - s^2 X^T v
+    // ---- pass 2: d~ = s z - s^2 X^T v with z = s p~ + s X^T rho, i.e.
+    // d~ = s^2 (p~ - X^T (v - rho)): ONE transposed product, X^T (v - rho)
+    // (butterfly per 16 columns), so pass 1 forms no column sums at all
     {
-      const float vk = valid ? ds[tid] : 0.f;
+      const float vk = valid ? ds[tid] - rho : 0.f;
       load16(x, 0);
 #pragma unroll 1
       for (int c0 = 0; c0 < B; c0 += 16) {
