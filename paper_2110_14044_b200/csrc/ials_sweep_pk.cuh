@@ -295,19 +295,14 @@ IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t
   float* lrow = reinterpret_cast<float*>(smem + L::OFF_L) + g * L::LPS + i * (i + 1) / 2;
   const int np = (b + 7) >> 3;
   float yi = ys[tid];
-  // lookahead as in tc4_factor: the trailing MMA of panel p is waited for one
-  // panel later; its update of the next panel's 8 columns is applied by the
-  // rows themselves (LN: the next diagonal block's rows of l, per slot)
-  float* LN = reinterpret_cast<float*>(smem + L::OFF_LI) + 512 + g * 64;
-  bool mma_pending = false;
-  float v[8];
-  tmem_ld8(row_addr + g * L::NG, v);
-  tmem_wait_ld();
   for (int pp = 0; pp < np; ++pp) {
     const int c0 = pp * 8;
     float* DG = reinterpret_cast<float*>(smem + L::OFF_DG + g * 640 + (pp & 1) * 320);
     float* RV = DG + 64;
     float* YP = DG + 72;
+    float v[8];
+    tmem_ld8(row_addr + g * L::NG + c0, v);
+    tmem_wait_ld();
     if (UNIT_DIAG) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -430,19 +425,6 @@ IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t
       *reinterpret_cast<float4*>(PAH + pa + 32) = make_float4(hi[4], hi[5], hi[6], hi[7]);
       *reinterpret_cast<float4*>(PAL + pa) = make_float4(lo[0], lo[1], lo[2], lo[3]);
       *reinterpret_cast<float4*>(PAL + pa + 32) = make_float4(lo[4], lo[5], lo[6], lo[7]);
-      if (i >= c0 + 8 && i < c0 + 16) {   // the slot's next diagonal block rows share their l
-        reinterpret_cast<float4*>(LN)[2 * (i - c0 - 8)] = make_float4(l[0], l[1], l[2], l[3]);
-        reinterpret_cast<float4*>(LN)[2 * (i - c0 - 8) + 1] = make_float4(l[4], l[5], l[6], l[7]);
-      }
-      if (mma_pending) {   // the previous panel's trailing update has landed in TMEM
-        mbar_wait(bar, st.ph & 1u);
-        st.ph ^= 1u;
-        tc_fence_after();
-      }
-      // the next panel's columns as of the previous MMAs, read before this
-      // panel's MMA (which also updates them) is issued
-      tmem_ld8(row_addr + g * L::NG + c0 + 8, v);
-      tmem_wait_ld();
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -459,26 +441,13 @@ IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t
         umma_tf32(st.tmem, al, ah, idesc_neg, 1);
         umma_commit(bar);
       }
-      mma_pending = true;
       record_block();
-      // this panel's update of the next panel's columns (rows above c0 + 8 have l = 0)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 a0 = reinterpret_cast<const float4*>(LN)[2 * j];
-        const float4 a1 = reinterpret_cast<const float4*>(LN)[2 * j + 1];
-        float t = v[j];
-        t = fmaf(-l[0], a0.x, t); t = fmaf(-l[1], a0.y, t); t = fmaf(-l[2], a0.z, t); t = fmaf(-l[3], a0.w, t);
-        t = fmaf(-l[4], a1.x, t); t = fmaf(-l[5], a1.y, t); t = fmaf(-l[6], a1.z, t); t = fmaf(-l[7], a1.w, t);
-        v[j] = t;
-      }
+      mbar_wait(bar, st.ph & 1u);
+      st.ph ^= 1u;
+      tc_fence_after();
     } else {
       record_block();
     }
-  }
-  if (mma_pending) {   // the last trailing update: TMEM quiescent, barrier phase consumed
-    mbar_wait(bar, st.ph & 1u);
-    st.ph ^= 1u;
-    tc_fence_after();
   }
   __syncthreads();
 }

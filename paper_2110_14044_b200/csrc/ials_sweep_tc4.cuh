@@ -332,22 +332,14 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
   const int np = (b + 7) >> 3;
   (void)row;
   float yi = ys[i];
-  // Lookahead: the trailing MMA of panel p is off the critical path.  Its
-  // update of the NEXT panel's 8 columns is applied by the rows themselves
-  // (v_next -= l . l_j over the panel's 8 columns, l_j = the next diagonal
-  // block's rows, shared through LN), on values read from TMEM before the MMA
-  // is issued; the MMA is only waited for one panel later, before the
-  // following panel's columns are read.
-  float* LN = reinterpret_cast<float*>(smem + L::OFF_LI) + 128;   // [8][8], beside the block staging
-  bool mma_pending = false;
-  float v[8];
-  tmem_ld8(row_addr, v);
-  tmem_wait_ld();
   for (int pp = 0; pp < np; ++pp) {
     const int c0 = pp * 8;
     float* DG = reinterpret_cast<float*>(smem + L::OFF_DG + (pp & 1) * 320);
     float* RV = reinterpret_cast<float*>(smem + L::OFF_RV + (pp & 1) * 320);
     float* YP = reinterpret_cast<float*>(smem + L::OFF_YP + (pp & 1) * 320);
+    float v[8];
+    tmem_ld8(row_addr + c0, v);
+    tmem_wait_ld();
     if (watch && pp == 8) acc[6] = clock64();
     if (warp == (c0 >> 5)) {
       // the diagonal block's rows are lanes base..base+7 of this warp: they
@@ -481,19 +473,6 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
       *reinterpret_cast<float4*>(PAH + pa + 32) = make_float4(hi[4], hi[5], hi[6], hi[7]);
       *reinterpret_cast<float4*>(PAL + pa) = make_float4(lo[0], lo[1], lo[2], lo[3]);
       *reinterpret_cast<float4*>(PAL + pa + 32) = make_float4(lo[4], lo[5], lo[6], lo[7]);
-      if (i >= c0 + 8 && i < c0 + 16) {   // the next diagonal block's rows share their l
-        reinterpret_cast<float4*>(LN)[2 * (i - c0 - 8)] = make_float4(l[0], l[1], l[2], l[3]);
-        reinterpret_cast<float4*>(LN)[2 * (i - c0 - 8) + 1] = make_float4(l[4], l[5], l[6], l[7]);
-      }
-      if (mma_pending) {   // the previous panel's trailing update has landed in TMEM
-        mbar_wait(bar, st.ph & 1u);
-        st.ph ^= 1u;
-        tc_fence_after();
-      }
-      // the next panel's columns as of the previous MMAs, read before this
-      // panel's MMA (which also updates them) is issued
-      tmem_ld8(row_addr + c0 + 8, v);
-      tmem_wait_ld();
       fence_proxy_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -512,27 +491,14 @@ IALS_DEVI void tc4_factor(const SweepParams& p, char* smem, Tc4State& st, uint32
         umma_tf32(st.tmem + cs, al, bh, idesc_neg, 1);
         umma_commit(bar);
       }
-      mma_pending = true;
       record_block();
-      // this panel's update of the next panel's columns (rows above c0 + 8 have l = 0)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 a0 = reinterpret_cast<const float4*>(LN)[2 * j];
-        const float4 a1 = reinterpret_cast<const float4*>(LN)[2 * j + 1];
-        float t = v[j];
-        t = fmaf(-l[0], a0.x, t); t = fmaf(-l[1], a0.y, t); t = fmaf(-l[2], a0.z, t); t = fmaf(-l[3], a0.w, t);
-        t = fmaf(-l[4], a1.x, t); t = fmaf(-l[5], a1.y, t); t = fmaf(-l[6], a1.z, t); t = fmaf(-l[7], a1.w, t);
-        v[j] = t;
-      }
+      mbar_wait(bar, st.ph & 1u);
       if (watch && pp == 8) acc[5] = clock64();
+      st.ph ^= 1u;
+      tc_fence_after();
     } else {
       record_block();
     }
-  }
-  if (mma_pending) {   // the last trailing update: TMEM quiescent, barrier phase consumed
-    mbar_wait(bar, st.ph & 1u);
-    st.ph ^= 1u;
-    tc_fence_after();
   }
   __syncthreads();
   if (watch) {
