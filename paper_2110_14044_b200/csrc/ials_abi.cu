@@ -1849,7 +1849,11 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   // so the pass scratch below it keeps all of ws_bytes - tcb
   char* tc_start = reinterpret_cast<char*>(
       (reinterpret_cast<uintptr_t>(ws) + (ws_bytes - std::min(tcb, ws_bytes)) + 1023) & ~uintptr_t(1023));
-  const bool tc_gemm = tc4_enabled() && block_tile(b) == 128 && b > 16 && d % 4 == 0 &&
+  // (b 8..16 keeps its FP32 SIMT sweep but takes the GEMMs: the slab and the
+  // projection are bandwidth-bound reads of W / H, 145 + 68 us per block and side
+  // on the SIMT kernels at d = 256, b = 16 against ~90 us here)
+  const bool tc_sweep = tc4_enabled() && block_tile(b) == 128 && b > 16;
+  const bool tc_gemm = tc4_enabled() && (tc_sweep || (b >= 8 && b <= 16 && b % 4 == 0)) && d % 4 == 0 &&
                        ldw % 4 == 0 && ldh % 4 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(H) % 16 == 0 && pbytes >= tcb &&
                        tc_start - pws >= (long long)pass_need && get_encode(s) == IALS_OK;
@@ -1972,7 +1976,7 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   // L2 / HBM bandwidth), and it moves sweep work into the "gramian" phase events,
   // which would flatter the sweep's roofline fraction: off by default.
   static const bool kDefer = getenv("IALS_DEFER_CACHE") && getenv("IALS_DEFER_CACHE")[0] == '1';
-  const bool defer = kDefer && tc_gemm;
+  const bool defer = kDefer && tc_gemm && tc_sweep;
   // Host staging with the fused sweep: the first user pass runs chunk by
   // chunk of user rows, each chunk's sweep starting once its rows of W have
   // landed (with its predictions and projection), instead of after all of W.
@@ -1989,7 +1993,8 @@ static int epoch_impl(ials_session* s, const ials_side* users, const ials_sched*
   // each chunk runs its own b x b sweep and Woodbury tiles; IALS_HOST_CHUNKS_ROT=0
   // keeps the rotated first pass whole)
   static const bool kChunkRot = !(getenv("IALS_HOST_CHUNKS_ROT") && getenv("IALS_HOST_CHUNKS_ROT")[0] == '0');
-  bool chunked = host && tc_gemm && nl > 0 && kChunks > 1 && U >= kChunks && (!rot || (kChunkRot && b == 128));
+  bool chunked = host && tc_gemm && tc_sweep && nl > 0 && kChunks > 1 && U >= kChunks &&
+                 (!rot || (kChunkRot && b == 128));
   if (chunked) {
     int su, spu, si, spi;
     gram_plan(std::max(users->n_rows, 1), d, &su, &spu);
