@@ -303,7 +303,7 @@ IALS_DEVI void pk_factor(const SweepParams& p, char* smem, PkState& st, uint32_t
     float v[8];
     tmem_ld8(row_addr + g * L::NG + c0, v);
     tmem_wait_ld();
-    if (UNIT_DIAG) {
+    if (UNIT_DIAG && i >= c0 && i < c0 + 8) {   // (only the diagonal block's rows hold a diagonal entry)
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (c0 + j == i) v[j] += 1.f;

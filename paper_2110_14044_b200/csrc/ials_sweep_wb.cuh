@@ -219,7 +219,6 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     load16(x, 0);
     uint32_t pend = 0;
     float uq = 0.f;   // y_k . (s p~) = x_k . (s^2 p~)
-    float yy = 0.f;   // |y_k|^2: (C - I)_kk, kept out of the TMEM diagonal 1 + |y_k|^2
     for (int ch = 0; ch < L::NCH; ++ch) {
       const int c0 = ch * L::KCH, ob = ch & 1;
       if (ch + 1 < L::NCH) load16(xn, c0 + L::KCH);
@@ -228,7 +227,6 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
       for (int j = 0; j < 16; ++j) {
         y[j] = x[j] * S[g * B + c0 + j];
         uq = fmaf(x[j], SZ[g * B + c0 + j], uq);
-        yy = fmaf(y[j], y[j], yy);
       }
       if (pend & (1u << ob)) {   // buffer ob was read by chunk ch - 2's MMAs
         mbar_wait(bar + ob, (st.ph >> ob) & 1u);
@@ -281,19 +279,19 @@ __global__ void __launch_bounds__(128, 4) k_sweep_wb(SweepParams p, int row0, in
     const int task_next = *next;
     int nrow = -1;
     if (tid < G && task_next < n_tiles) nrow = tile_row(task_next, tid);
-    // u_k = y_k . (s p~) + sum_j (C - I)_kj rho_j over the slot's entries; the
-    // diagonal term from |y_k|^2 itself (in TMEM it is 1 + |y_k|^2, whose
-    // rounding would lose |y_k|^2's low bits when the rows are small)
+    // u_k = y_k . (s p~) + sum_j (C - I)_kj rho_j over the slot's entries: the
+    // thread's TMEM row of Y Y^T (the diagonal |y_k|^2 included: TMEM holds
+    // C - I, so it carries no added identity whose rounding would hide it)
     {
       const float* RH = reinterpret_cast<const float*>(smem + L::OFF_RHO) + g * L::NG;
-      float cr = yy * rho;
+      float cr = 0.f;
 #pragma unroll
       for (int c32 = 0; c32 < L::NG; c32 += 32) {
         float cv[32];
         tmem_ld32(row_addr + g * L::NG + c32, cv);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) cr = fmaf((c32 + j == k) ? 0.f : cv[j], RH[c32 + j], cr);
+        for (int j = 0; j < 32; ++j) cr = fmaf(cv[j], RH[c32 + j], cr);
       }
       ys[tid] = valid ? uq + cr : 0.f;
     }

@@ -265,6 +265,45 @@ def test_sharded_path_gpu_ops_single_rank(ials, d, b, native):
     assert relmax(cache, ref_cache) < TOL
 
 
+@pytest.mark.parametrize("world,rank,b", [(3, 1, 16), (4, 0, 128), (2, 1, 7)])
+def test_shard_apply_block_remote_rows_and_change(ials, world, rank, b):
+    """k_apply_block, the only kernel whose work depends on the world size: from
+    an all-gathered (padded) receive buffer it writes the OTHER ranks' rows of
+    X[:, b0:b0+b] and forms new - old for every row (old of the local rows from
+    the pre-sweep copy, of the remote rows from X itself).  Uneven shards, an
+    empty one, a strided X."""
+    import ctypes
+    import torch
+    from paper_2110_14044_b200.distributed import GpuOps
+    rng = np.random.default_rng(world * 10 + rank)
+    sizes = [int(x) for x in rng.integers(0, 40, world)]
+    sizes[(rank + 1) % world] = 0                       # an empty shard
+    sizes[rank] = max(sizes[rank], 5)
+    cuts = np.concatenate([[0], np.cumsum(sizes)])
+    bounds = [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+    n, nmax, ld, b0 = int(cuts[-1]), max(max(sizes), 1), 3 * b + 5, b + 2
+    X0 = rng.standard_normal((n, ld)).astype(np.float32)
+    new = rng.standard_normal((n, b)).astype(np.float32)
+    recv = np.full((world * nmax, b), np.nan, dtype=np.float32)      # padding must never be read
+    for r, (lo, hi) in enumerate(bounds):
+        recv[r * nmax: r * nmax + hi - lo] = new[lo:hi]
+    lo, hi = bounds[rank]
+    old_local = rng.standard_normal((hi - lo, b)).astype(np.float32)  # the pre-sweep rows
+    X = X0.copy()
+    X[lo:hi, b0:b0 + b] = new[lo:hi]                                  # the sweep updated the local rows in place
+    want_delta = new - X0[:, b0:b0 + b]
+    want_delta[lo:hi] = new[lo:hi] - old_local
+    want_X = X0.copy()
+    want_X[:, b0:b0 + b] = new
+    ops = GpuOps("cuda:0")
+    Xd = torch.from_numpy(X).cuda()
+    delta = ops.apply_block(torch.from_numpy(recv).cuda(), nmax, bounds, rank,
+                            torch.from_numpy(old_local).cuda(), Xd, b0, b)
+    torch.cuda.synchronize()
+    assert np.array_equal(Xd.cpu().numpy(), want_X)
+    assert np.array_equal(delta.cpu().numpy(), want_delta)
+
+
 @pytest.mark.parametrize("d,b,nccl", [(64, 16, False), (256, 128, False), (256, 128, True), (96, 48, True)])
 def test_sharded_native_epoch_equals_python_orchestration(ials, d, b, nccl):
     """ials_epoch_sharded (the multi-GPU epoch behind the C ABI) launches the
