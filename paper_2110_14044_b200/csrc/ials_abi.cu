@@ -27,6 +27,7 @@
 #include "ials_gemm_tc.cuh"
 #include "ials_sweep_b1.cuh"
 #include "ials_sweep_wide.cuh"
+#include "ials_sweep_w32.cuh"
 
 using namespace ials;
 
@@ -238,6 +239,12 @@ int64_t ials_heavy_threshold(int32_t b) {
   static const long long ov = getenv("IALS_HEAVY") ? atoll(getenv("IALS_HEAVY")) : 0;
   if (ov > 0) return ov;
   const int bt = block_tile(b);
+  // narrow blocks in the 128 tile: a long row is one warp's (b <= 32, the
+  // warp-per-row sweep) or one tile slot's serial chain, while its slices spread
+  // over the machine (measured at the configs[1] / [2] shapes: 512 at b = 32,
+  // 15.6 -> 11.1 ms with the warp-per-row sweep; 2048 at b = 64)
+  if (bt == 128 && b <= 32) return 512;
+  if (bt == 128 && b <= 64) return 2048;
   return bt <= 16 ? 512 : bt == 32 ? 1024 : 4096;
 }
 int64_t ials_slice_len(int32_t b) {
@@ -630,6 +637,13 @@ static int join_cache(ials_session* s, cudaStream_t st) {
   return IALS_OK;
 }
 
+// b 17..32: the warp-per-row FP32 sweep instead of the packed tensor-core one
+// (IALS_W32=0 keeps the packed sweep)
+static bool w32_enabled() {
+  static const bool on = !(getenv("IALS_W32") && getenv("IALS_W32")[0] == '0');
+  return on;
+}
+
 static int wb_attrs(ials_session* s) {
   static unsigned winit = 0;
   if (!(winit & dev_bit())) {
@@ -733,6 +747,26 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           k_sweep_pk<2, true><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
         else
           k_sweep_pk<2, false><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
+      } else if (w32_enabled() && p.vec) {
+        // b 17..32: one row per warp, FP32 SIMT (ials_sweep_w32.cuh)
+        static int w32_sm = 0;
+        static unsigned w32_init = 0;
+        if (!(w32_init & dev_bit())) {
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32Lay::BYTES));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32Lay::BYTES));
+          w32_init |= dev_bit();
+        }
+        if (w32_sm == 0) {
+          CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w32_sm, k_sweep_w32<true>, W32Lay::NT,
+                                                                   W32Lay::BYTES));
+          if (w32_sm < 1) w32_sm = 1;
+        }
+        q.queue = p.redo_cnt + 2;   // zeroed with the redo count (and per chunk)
+        const int wgrid = std::min((n_b + W32Lay::NW - 1) / W32Lay::NW, w32_sm * kNumSMs);
+        if (unit)
+          k_sweep_w32<true><<<wgrid, W32Lay::NT, W32Lay::BYTES, st>>>(q);
+        else
+          k_sweep_w32<false><<<wgrid, W32Lay::NT, W32Lay::BYTES, st>>>(q);
       } else {
         if (unit)
           k_sweep_pk<4, true><<<grid, 128, PkLay<4>::BYTES, st>>>(q, fmap, use_tma);

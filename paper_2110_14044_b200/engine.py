@@ -141,12 +141,13 @@ class DeviceSide:
 
     def schedule(self, b: int) -> Schedule:
         """Light rows in descending degree; heavy rows split into fixed slices."""
-        bt = block_tile(b)
+        lib = _lib.load()
+        # keyed by what the plan depends on: the library's heavy-row threshold
+        # and slice length for this width
+        bt = (int(lib.ials_heavy_threshold(b)), int(lib.ials_slice_len(b)))
         if bt in self._sched:
             return self._sched[bt]
-        lib = _lib.load()
-        plan = plan_schedule(self.ptr.cpu().numpy(), int(lib.ials_heavy_threshold(b)),
-                             int(lib.ials_slice_len(b)))
+        plan = plan_schedule(self.ptr.cpu().numpy(), bt[0], bt[1])
         to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(self.device)
         t = {k: to(v) for k, v in plan.items()}
         deg_light = self.counts[plan["light"]]   # descending: the counts are prefix lengths
