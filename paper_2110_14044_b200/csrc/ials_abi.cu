@@ -28,6 +28,7 @@
 #include "ials_sweep_b1.cuh"
 #include "ials_sweep_wide.cuh"
 #include "ials_sweep_w32.cuh"
+#include "ials_sweep_w16.cuh"
 
 using namespace ials;
 
@@ -644,6 +645,13 @@ static bool w32_enabled() {
   return on;
 }
 
+// b 4..16: the two-rows-per-warp FP32 sweep instead of the generic SIMT one
+// (IALS_W16=0 keeps k_sweep_light<8 | 16>)
+static bool w16_enabled() {
+  static const bool on = !(getenv("IALS_W16") && getenv("IALS_W16")[0] == '0');
+  return on;
+}
+
 static int wb_attrs(ials_session* s) {
   static unsigned winit = 0;
   if (!(winit & dev_bit())) {
@@ -944,7 +952,34 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
   int rc = set_smem_attrs<BT>(s);
   if (rc) return rc;
   const int threads = L::NT * L::RPC;
-  if (p.n_light > 0) {
+  // b 4..16 (16-byte sub-rows): two rows per warp, FP32 SIMT (ials_sweep_w16.cuh); the
+  // cache update is the entry-parallel pass over drow, heavy rows included
+  const bool w16 = BT <= 16 && p.b >= 4 && p.vec && p.side.rows && !p.rot && nnz > 0 && w16_enabled();
+  if (w16 && p.n_light > 0) {
+    static int w16_sm = 0;
+    static unsigned w16_init = 0;
+    const bool unit = !p.side.weights && !p.side.labels;
+    if (!(w16_init & dev_bit())) {
+      CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w16<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W16Lay::BYTES));
+      CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w16<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W16Lay::BYTES));
+      w16_init |= dev_bit();
+    }
+    if (w16_sm == 0) {
+      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w16_sm, k_sweep_w16<true>, W16Lay::NT,
+                                                               W16Lay::BYTES));
+      if (w16_sm < 1) w16_sm = 1;
+    }
+    SweepParams q = p;
+    q.queue = p.redo_cnt + 3;
+    CUDA_TRY(s, cudaMemsetAsync(q.queue, 0, sizeof(int), st));
+    const int tasks = (p.n_light + 1) / 2;
+    const int wgrid = std::min((tasks + W16Lay::NW - 1) / W16Lay::NW, w16_sm * kNumSMs);
+    if (unit)
+      k_sweep_w16<true><<<wgrid, W16Lay::NT, W16Lay::BYTES, st>>>(q);
+    else
+      k_sweep_w16<false><<<wgrid, W16Lay::NT, W16Lay::BYTES, st>>>(q);
+    LAUNCH_CHECK(s);
+  } else if (p.n_light > 0) {
     static int per_sm = 0;
     if (per_sm == 0) {
       CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_light<BT>,
@@ -964,7 +999,23 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     LAUNCH_CHECK(s);
     k_heavy_solve<BT><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
     LAUNCH_CHECK(s);
-    k_heavy_cache<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    if (!w16) {
+      k_heavy_cache<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+      LAUNCH_CHECK(s);
+    }
+  }
+  if (w16 && p.n_light + p.n_heavy > 0) {
+    const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);
+    // walk the other side's order when this side's d is the smaller gather
+    const bool swap = p.x_rows && p.x_cols && p.side.n_rows < p.side.n_fixed;
+    static const bool lpe8 = getenv("IALS_W16_LPE8") != nullptr;   // (measurements)
+    if (lpe8) {
+      if (swap) k_pass_cache_flat<true, 8, true><<<(int)g, 256, 0, st>>>(p, nnz);
+      else k_pass_cache_flat<true, 8, false><<<(int)g, 256, 0, st>>>(p, nnz);
+    } else {   // 4 lanes x 16 bytes cover a 16-wide sub-row
+      if (swap) k_pass_cache_flat<true, 4, true, 16><<<(int)g, 256, 0, st>>>(p, nnz);
+      else k_pass_cache_flat<true, 4, false, 16><<<(int)g, 256, 0, st>>>(p, nnz);
+    }
     LAUNCH_CHECK(s);
   }
   return IALS_OK;

@@ -912,9 +912,11 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
 // side is the smaller one -- the item pass, whose fixed W[:, pi] is 70 MB at
 // L1 and 292 MB at msd).  Each entry's sum is the same fixed-order chain of
 // the same products (fma is commutative in its factors): bit-identical.
-template <bool VEC, int LPE, bool SWAP>
-__global__ void __launch_bounds__(256, LPE == 8 ? 4 : 2) k_pass_cache_flat(SweepParams p, long long nnz) {
-  constexpr int EPW = 32 / LPE, NQ = 128 / (4 * LPE);   // entries per warp step, float4 per lane
+// BMAX: the widest block the instantiation serves (b <= 16 with LPE = 4: one
+// float4 per lane, 8 entries per warp step).
+template <bool VEC, int LPE, bool SWAP, int BMAX = 128>
+__global__ void __launch_bounds__(256, (LPE == 8 || BMAX <= 16) ? 4 : 2) k_pass_cache_flat(SweepParams p, long long nnz) {
+  constexpr int EPW = 32 / LPE, NQ = BMAX / (4 * LPE);   // entries per warp step, float4 per lane
   const int lane = threadIdx.x & 31, g = lane % LPE, sub = lane / LPE;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);

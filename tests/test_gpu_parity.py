@@ -566,3 +566,52 @@ def test_rotated_user_pass_matches_unrotated(ials, d):
     orc.train(w0, h0, csr, 0.1, 1e-3, 1.0, 128, 3)
     for got, want in ((out[1].user_factors, w0), (out[1].item_factors, h0)):
         assert relf(got, want) < TOL and relmax(got, want) < TOL
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("d,b", [(16, 16), (48, 16), (24, 8), (36, 12), (8, 4), (40, 16)])
+def test_two_rows_per_warp_sweep_vs_oracle(ials, d, b, weighted):
+    """b = 4..16 (k_sweep_w16: a light row per half-warp, heavy rows by slices,
+    the entry-parallel cache update over both): 2 epochs vs the f64 oracle at
+    rel 1e-3 -- an odd number of light rows (the last pair is half empty),
+    padded widths (b < 16), a remainder block (d = 40: 16, 16, 8), items above
+    the heavy threshold, unit and weighted entries; and the generic SIMT sweep
+    (IALS_W16=0 is read once per process, so it is compared through the
+    oracle only)."""
+    from oracle import ialspp_oracle as orc
+    U, I, users, items = _heavy_instance(4001, 300, 40, 1.2, 5 + b)
+    labels = weights = None
+    if weighted:
+        rng = np.random.default_rng(b)
+        labels = rng.uniform(0.5, 2.0, users.size)
+        weights = rng.uniform(0.25, 4.0, users.size)
+    data = ials.InteractionDataset(U, I, users, items, labels, weights)
+    assert data.item_counts.max() > 512   # heavy items at this width
+    cfg = ials.SolverConfig(dim=d, block_size=b, unobserved_weight=0.1, reg=1e-3,
+                            reg_exponent=1.0, epochs=2, seed=2)
+    m = ials.init_model(cfg, U, I)
+    m.user_factors[:] = m.user_factors.astype(np.float32)
+    m.item_factors[:] = m.item_factors.astype(np.float32)
+    w, h = m.user_factors.copy(), m.item_factors.copy()
+    _, reports = ials.train(m, data, cfg, log_loss=True)
+    csr = orc.build_csr(U, I, users, items, labels, weights)
+    orc.train(w, h, csr, 0.1, 1e-3, 1.0, b, 2)
+    assert relf(m.user_factors, w) < TOL and relf(m.item_factors, h) < TOL
+    assert relmax(m.user_factors, w) < TOL and relmax(m.item_factors, h) < TOL
+    want = orc.loss(w, h, csr, 0.1, 1e-3, 1.0)
+    assert abs(reports[-1].loss - want) / want < TOL
+
+
+def test_two_rows_per_warp_sweep_names_singular_row(ials):
+    """An empty user row with alpha0 = 0 and nu = 1 has a zero Hessian
+    (reference tests/test_solvers.py:82-91); at b = 8 it is the lone row of the
+    last pair of the degree-sorted list."""
+    users = np.concatenate([np.zeros(5, np.int64), np.full(3, 2)])
+    items = np.concatenate([np.arange(5), np.arange(3)])
+    data = ials.InteractionDataset(3, 6, users, items)
+    cfg = ials.SolverConfig(dim=8, block_size=8, unobserved_weight=0.0, reg=0.1, reg_exponent=1.0)
+    model = ials.init_model(cfg, 3, 6)
+    cache = ials.compute_predictions(model, data)
+    with pytest.raises(ials.SingularMatrixError) as err:
+        ials.block_update(model, data, cache, cfg, np.arange(8), side="user")
+    assert err.value.row == 1 and err.value.pivot == 0
