@@ -28,7 +28,9 @@
 #include "ials_sweep_b1.cuh"
 #include "ials_sweep_wide.cuh"
 #include "ials_sweep_w32.cuh"
+#include "ials_sweep_w32m.cuh"
 #include "ials_sweep_w16.cuh"
+#include "ials_heavy_w.cuh"
 
 using namespace ials;
 
@@ -126,6 +128,8 @@ int64_t ials_launch_count(void) { return g_launches.load(std::memory_order_relax
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static bool tc4_enabled();
+static bool w16_enabled();
+static bool hw_enabled();
 // Register/shared tile width of a block of b columns.  With the fused
 // tensor-core sweep (the default) widths 33..64 also use the 128 tile (the
 // padding is idle tensor-core work; the factorisation chain is half of the
@@ -252,6 +256,8 @@ int64_t ials_slice_len(int32_t b) {
   static const long long ov = getenv("IALS_SLICE") ? atoll(getenv("IALS_SLICE")) : 0;
   if (ov > 0) return ov;
   const int bt = block_tile(b);
+  // (b <= 16 with the half-warp slice kernel and the parallel slice reduction of
+  // ials_heavy_w.cuh: a 1024-entry slice is a 240 us serial chain, 256 stays)
   return bt <= 16 ? 256 : bt == 32 ? 512 : (bt == 256 ? 1024 : 2048);
 }
 
@@ -652,6 +658,35 @@ static bool w16_enabled() {
   return on;
 }
 
+// heavy-row slices of b <= 32 in the warp-per-row register layout
+// (ials_heavy_w.cuh; IALS_HW=0 keeps k_heavy_partial<bt> / k_heavy_partial_pk<4>)
+static bool hw_enabled() {
+  static const bool on = !(getenv("IALS_HW") && getenv("IALS_HW")[0] == '0');
+  return on;
+}
+template <int NB>
+static int launch_heavy_w(ials_session* s, const SweepParams& p, int bt, cudaStream_t st) {
+  using L = WHLay<NB>;
+  static int per_sm = 0;
+  static unsigned init = 0;
+  if (!(init & dev_bit())) {
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_w<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_w<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    init |= dev_bit();
+  }
+  if (per_sm == 0) {
+    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_heavy_partial_w<NB, true>, L::NT, L::BYTES));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const bool unit = !p.side.weights && !p.side.labels;
+  const int per_cta = L::NW * L::G;
+  const int grid = std::min((p.n_slices + per_cta - 1) / per_cta, per_sm * kNumSMs);
+  if (unit) k_heavy_partial_w<NB, true><<<grid, L::NT, L::BYTES, st>>>(p, bt);
+  else k_heavy_partial_w<NB, false><<<grid, L::NT, L::BYTES, st>>>(p, bt);
+  LAUNCH_CHECK(s);
+  return IALS_OK;
+}
+
 static int wb_attrs(ials_session* s) {
   static unsigned winit = 0;
   if (!(winit & dev_bit())) {
@@ -756,25 +791,28 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         else
           k_sweep_pk<2, false><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
       } else if (w32_enabled() && p.vec) {
-        // b 17..32: one row per warp, FP32 SIMT (ials_sweep_w32.cuh)
+        // b 17..32: one row per warp (ials_sweep_w32m.cuh: the Hessian by warp-level
+        // 3xTF32 MMA tiles; IALS_W32_MMA=0: the FP32 SIMT tiles of ials_sweep_w32.cuh)
+        static const bool mma = !(getenv("IALS_W32_MMA") && getenv("IALS_W32_MMA")[0] == '0');
         static int w32_sm = 0;
         static unsigned w32_init = 0;
+        auto kern = mma ? (unit ? k_sweep_w32m<true> : k_sweep_w32m<false>)
+                        : (unit ? k_sweep_w32<true> : k_sweep_w32<false>);
+        const int wbytes = mma ? W32mLay::BYTES : W32Lay::BYTES;
         if (!(w32_init & dev_bit())) {
           CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32Lay::BYTES));
           CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32Lay::BYTES));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32mLay::BYTES));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32mLay::BYTES));
           w32_init |= dev_bit();
         }
         if (w32_sm == 0) {
-          CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w32_sm, k_sweep_w32<true>, W32Lay::NT,
-                                                                   W32Lay::BYTES));
+          CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w32_sm, kern, W32Lay::NT, wbytes));
           if (w32_sm < 1) w32_sm = 1;
         }
         q.queue = p.redo_cnt + 2;   // zeroed with the redo count (and per chunk)
         const int wgrid = std::min((n_b + W32Lay::NW - 1) / W32Lay::NW, w32_sm * kNumSMs);
-        if (unit)
-          k_sweep_w32<true><<<wgrid, W32Lay::NT, W32Lay::BYTES, st>>>(q);
-        else
-          k_sweep_w32<false><<<wgrid, W32Lay::NT, W32Lay::BYTES, st>>>(q);
+        kern<<<wgrid, W32Lay::NT, wbytes, st>>>(q);
       } else {
         if (unit)
           k_sweep_pk<4, true><<<grid, 128, PkLay<4>::BYTES, st>>>(q, fmap, use_tma);
@@ -814,6 +852,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
       }
     }
   }
+  bool heavy_reduced = false;
   if (p.n_heavy > 0) {
     static unsigned hinit = 0;
     if (!(hinit & dev_bit())) {
@@ -844,7 +883,15 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         pinit |= dev_bit();
       }
       const int hg = std::min((p.n_slices + G - 1) / G, 4 * kNumSMs);
-      if (G == 2) {
+      if (G == 4 && p.vec && w32_enabled() && hw_enabled()) {
+        rc = launch_heavy_w<32>(s, p, 32, hst);
+        if (rc) return rc;
+        if (p.n_slices > p.n_heavy) {
+          k_heavy_reduce<32><<<p.n_heavy, HRLay<32>::NT, 0, hst>>>(p);
+          LAUNCH_CHECK(s);
+          heavy_reduced = true;
+        }
+      } else if (G == 2) {
         if (unit) k_heavy_partial_pk<2, true><<<hg, 128, PkLay<2>::BYTES, hst>>>(p, fmap, use_tma);
         else k_heavy_partial_pk<2, false><<<hg, 128, PkLay<2>::BYTES, hst>>>(p, fmap, use_tma);
       } else {
@@ -864,7 +911,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
       k_heavy_solve<64, true><<<(p.n_heavy + L64::RPC - 1) / L64::RPC, L64::NT * L64::RPC, L64::CTA_BYTES, st>>>(p);
     } else {
       using L32 = Lay<32>;
-      k_heavy_solve<32, true><<<(p.n_heavy + L32::RPC - 1) / L32::RPC, L32::NT * L32::RPC, L32::CTA_BYTES, st>>>(p);
+      SweepParams ph = p;
+      ph.heavy_reduced = heavy_reduced ? 1 : 0;
+      k_heavy_solve<32, true><<<(p.n_heavy + L32::RPC - 1) / L32::RPC, L32::NT * L32::RPC, L32::CTA_BYTES, st>>>(ph);
     }
     LAUNCH_CHECK(s);
   }
@@ -955,6 +1004,26 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
   // b 4..16 (16-byte sub-rows): two rows per warp, FP32 SIMT (ials_sweep_w16.cuh); the
   // cache update is the entry-parallel pass over drow, heavy rows included
   const bool w16 = BT <= 16 && p.b >= 4 && p.vec && p.side.rows && !p.rot && nnz > 0 && w16_enabled();
+  // the long rows' slice partials (ials_heavy_w.cuh) run beside the light rows on the
+  // second stream (disjoint rows, the cache only read), joined before their solve
+  const bool hw = w16 && p.n_heavy > 0 && hw_enabled();
+  const bool fork = hw && p.n_light > 0;
+  if (hw) {
+    cudaStream_t hst = st;
+    if (fork) {
+      if (!s->aux_st) {
+        CUDA_TRY(s, cudaStreamCreateWithFlags(&s->aux_st, cudaStreamNonBlocking));
+        CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(s, cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+      }
+      hst = s->aux_st;
+      CUDA_TRY(s, cudaEventRecord(s->ev_fork, st));
+      CUDA_TRY(s, cudaStreamWaitEvent(hst, s->ev_fork, 0));
+    }
+    rc = launch_heavy_w<16>(s, p, BT, hst);
+    if (rc) return rc;
+    if (fork) CUDA_TRY(s, cudaEventRecord(s->ev_join, hst));
+  }
   if (w16 && p.n_light > 0) {
     static int w16_sm = 0;
     static unsigned w16_init = 0;
@@ -995,9 +1064,19 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     LAUNCH_CHECK(s);
   }
   if (p.n_heavy > 0) {
-    k_heavy_partial<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
-    LAUNCH_CHECK(s);
-    k_heavy_solve<BT><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+    if (!hw) {
+      k_heavy_partial<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
+      LAUNCH_CHECK(s);
+    } else if (fork) {
+      CUDA_TRY(s, cudaStreamWaitEvent(st, s->ev_join, 0));
+    }
+    SweepParams ph = p;
+    if (hw && BT <= 32 && p.n_slices > p.n_heavy) {   // some row has several slices
+      k_heavy_reduce<(BT <= 32 ? BT : 32)><<<p.n_heavy, HRLay<(BT <= 32 ? BT : 32)>::NT, 0, st>>>(p);
+      LAUNCH_CHECK(s);
+      ph.heavy_reduced = 1;
+    }
+    k_heavy_solve<BT><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(ph);
     LAUNCH_CHECK(s);
     if (!w16) {
       k_heavy_cache<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);

@@ -89,6 +89,7 @@ struct SweepParams {
   const int* x_pos;        //   cache pass may walk it instead (k_pass_cache_flat<., ., true>)
   const int* chunk_tot;    // if set (k_sweep_tc4): light rows grouped by row chunk, chunk_tot[k]
   int chunk;               //   rows in chunk k; this launch sweeps chunk `chunk` only
+  int heavy_reduced;       // k_heavy_solve reads one slot per heavy row (k_heavy_reduce ran)
 };
 
 template <int BT>
@@ -734,7 +735,10 @@ __global__ void __launch_bounds__(Lay<BT>::NT* Lay<BT>::RPC)
   Tiles<BT> T;
   T.init(tid >> 5, tid & 31);
   double gacc = 0.0;
-  for (int sl = p.heavy_slice0[h]; sl < p.heavy_slice0[h + 1]; ++sl) {
+  // (heavy_reduced: k_heavy_reduce already summed the row's slices into the first slot)
+  const int sl_first = p.heavy_slice0[h];
+  const int sl_end = p.heavy_reduced ? min(sl_first + 1, p.heavy_slice0[h + 1]) : p.heavy_slice0[h + 1];
+  for (int sl = sl_first; sl < sl_end; ++sl) {
     const float* hp = p.hpart + (size_t)sl * BT * BT;
 #pragma unroll
     for (int t = 0; t < L::TPW; ++t) {
