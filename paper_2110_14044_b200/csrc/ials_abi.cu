@@ -30,6 +30,7 @@
 #include "ials_sweep_w32.cuh"
 #include "ials_sweep_w32m.cuh"
 #include "ials_sweep_w16.cuh"
+#include "ials_sweep_w16m.cuh"
 #include "ials_heavy_w.cuh"
 
 using namespace ials;
@@ -664,25 +665,35 @@ static bool hw_enabled() {
   static const bool on = !(getenv("IALS_HW") && getenv("IALS_HW")[0] == '0');
   return on;
 }
+// (IALS_W_MMA=0: the FP32 SIMT tiles instead of the warp-level 3xTF32 MMA tiles, in the
+// b <= 16 sweep and in the slice kernels; IALS_W32_MMA=0 the same for the b 17..32 sweep)
+static bool wmma_enabled() {
+  static const bool on = !(getenv("IALS_W_MMA") && getenv("IALS_W_MMA")[0] == '0');
+  return on;
+}
 template <int NB>
 static int launch_heavy_w(ials_session* s, const SweepParams& p, int bt, cudaStream_t st) {
-  using L = WHLay<NB>;
+  const bool mma = wmma_enabled();
+  const bool unit = !p.side.weights && !p.side.labels;
+  auto kern = mma ? (unit ? k_heavy_partial_wm<NB, true> : k_heavy_partial_wm<NB, false>)
+                  : (unit ? k_heavy_partial_w<NB, true> : k_heavy_partial_w<NB, false>);
+  const int bytes = mma ? WHmLay<NB>::BYTES : WHLay<NB>::BYTES;
   static int per_sm = 0;
   static unsigned init = 0;
   if (!(init & dev_bit())) {
-    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_w<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
-    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_w<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_w<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, WHLay<NB>::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_w<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, WHLay<NB>::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_wm<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, WHmLay<NB>::BYTES));
+    CUDA_TRY(s, cudaFuncSetAttribute(k_heavy_partial_wm<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, WHmLay<NB>::BYTES));
     init |= dev_bit();
   }
   if (per_sm == 0) {
-    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_heavy_partial_w<NB, true>, L::NT, L::BYTES));
+    CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WHLay<NB>::NT, bytes));
     if (per_sm < 1) per_sm = 1;
   }
-  const bool unit = !p.side.weights && !p.side.labels;
-  const int per_cta = L::NW * L::G;
+  const int per_cta = WHLay<NB>::NW * WHLay<NB>::G;
   const int grid = std::min((p.n_slices + per_cta - 1) / per_cta, per_sm * kNumSMs);
-  if (unit) k_heavy_partial_w<NB, true><<<grid, L::NT, L::BYTES, st>>>(p, bt);
-  else k_heavy_partial_w<NB, false><<<grid, L::NT, L::BYTES, st>>>(p, bt);
+  kern<<<grid, WHLay<NB>::NT, bytes, st>>>(p, bt);
   LAUNCH_CHECK(s);
   return IALS_OK;
 }
@@ -1028,14 +1039,21 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     static int w16_sm = 0;
     static unsigned w16_init = 0;
     const bool unit = !p.side.weights && !p.side.labels;
+    const bool mma = wmma_enabled();
+    auto kern = mma ? (unit ? k_sweep_w16m<true> : k_sweep_w16m<false>)
+                    : (unit ? k_sweep_w16<true> : k_sweep_w16<false>);
+    const int wbytes = mma ? W16mLay::BYTES : W16Lay::BYTES;
     if (!(w16_init & dev_bit())) {
       CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w16<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W16Lay::BYTES));
       CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w16<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W16Lay::BYTES));
+      for (auto k : {k_sweep_w16m<true>, k_sweep_w16m<false>}) {
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, W16mLay::BYTES));
+        CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
       w16_init |= dev_bit();
     }
     if (w16_sm == 0) {
-      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w16_sm, k_sweep_w16<true>, W16Lay::NT,
-                                                               W16Lay::BYTES));
+      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w16_sm, kern, W16Lay::NT, wbytes));
       if (w16_sm < 1) w16_sm = 1;
     }
     SweepParams q = p;
@@ -1043,10 +1061,7 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     CUDA_TRY(s, cudaMemsetAsync(q.queue, 0, sizeof(int), st));
     const int tasks = (p.n_light + 1) / 2;
     const int wgrid = std::min((tasks + W16Lay::NW - 1) / W16Lay::NW, w16_sm * kNumSMs);
-    if (unit)
-      k_sweep_w16<true><<<wgrid, W16Lay::NT, W16Lay::BYTES, st>>>(q);
-    else
-      k_sweep_w16<false><<<wgrid, W16Lay::NT, W16Lay::BYTES, st>>>(q);
+    kern<<<wgrid, W16Lay::NT, wbytes, st>>>(q);
     LAUNCH_CHECK(s);
   } else if (p.n_light > 0) {
     static int per_sm = 0;

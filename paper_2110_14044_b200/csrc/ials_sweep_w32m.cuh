@@ -50,6 +50,79 @@ IALS_DEVI void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// One 16-entry stage of a 32-wide row into the six lower-triangle tiles
+// ([0] (0,0) [1] (0,1) [2..5] (1,0..3)); xb: [16][XLD = 40] staged sub-rows, aw: the
+// stage's 16 entry weights (read only when !UNIT).
+template <bool UNIT>
+IALS_DEVI void w32m_stage(float (&acc)[6][4], const float* xb, const float* aw, int g, int t4) {
+  constexpr int XLD = 40;
+#pragma unroll
+  for (int c8 = 0; c8 < 16; c8 += 8) {
+    const float* xc = xb + c8 * XLD;
+    uint32_t hi[4][2], lo[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) tf32_split(xc[(t4 + 4 * h) * XLD + 8 * j + g], hi[j][h], lo[j][h]);
+    uint32_t ahi[4][2], alo[4][2];   // the A copy: a_k x_k for weighted entries
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (UNIT) {
+          ahi[j][h] = hi[j][h];
+          alo[j][h] = lo[j][h];
+        } else {
+          tf32_split(aw[c8 + t4 + 4 * h] * xc[(t4 + 4 * h) * XLD + 8 * j + g], ahi[j][h], alo[j][h]);
+        }
+      }
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb) {
+      const uint32_t Ah[4] = {ahi[2 * mb][0], ahi[2 * mb + 1][0], ahi[2 * mb][1], ahi[2 * mb + 1][1]};
+      const uint32_t Al[4] = {alo[2 * mb][0], alo[2 * mb + 1][0], alo[2 * mb][1], alo[2 * mb + 1][1]};
+#pragma unroll
+      for (int nb = 0; nb < 2 + 2 * mb; ++nb) {
+        float(&d)[4] = acc[2 * mb + nb];
+        mma_tf32(d, Al, hi[nb][0], hi[nb][1]);
+        mma_tf32(d, Ah, lo[nb][0], lo[nb][1]);
+        mma_tf32(d, Ah, hi[nb][0], hi[nb][1]);
+      }
+    }
+  }
+}
+
+// One 16-entry stage of a 16-wide row into its two tiles (columns 0..7, 8..15);
+// xb: [16][XLD = 24] staged sub-rows (24 = -8 mod 32: conflict-free fragments).
+template <bool UNIT>
+IALS_DEVI void w16m_stage(float (&acc)[2][4], const float* xb, const float* aw, int g, int t4) {
+  constexpr int XLD = 24;
+#pragma unroll
+  for (int c8 = 0; c8 < 16; c8 += 8) {
+    const float* xc = xb + c8 * XLD;
+    uint32_t hi[2][2], lo[2][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) tf32_split(xc[(t4 + 4 * h) * XLD + 8 * j + g], hi[j][h], lo[j][h]);
+    uint32_t Ah[4] = {hi[0][0], hi[1][0], hi[0][1], hi[1][1]};
+    uint32_t Al[4] = {lo[0][0], lo[1][0], lo[0][1], lo[1][1]};
+    if (!UNIT) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float a = aw[c8 + t4 + 4 * h];
+        tf32_split(a * xc[(t4 + 4 * h) * XLD + g], Ah[2 * h], Al[2 * h]);
+        tf32_split(a * xc[(t4 + 4 * h) * XLD + 8 + g], Ah[2 * h + 1], Al[2 * h + 1]);
+      }
+    }
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      mma_tf32(acc[nb], Al, hi[nb][0], hi[nb][1]);
+      mma_tf32(acc[nb], Ah, lo[nb][0], lo[nb][1]);
+      mma_tf32(acc[nb], Ah, hi[nb][0], hi[nb][1]);
+    }
+  }
+}
+
 template <bool UNIT>
 __global__ void __launch_bounds__(W32mLay::NT, 3) k_sweep_w32m(SweepParams p) {
   using L = W32mLay;
@@ -153,40 +226,7 @@ __global__ void __launch_bounds__(W32mLay::NT, 3) k_sweep_w32m(SweepParams p) {
       __syncwarp();
       const float* xb = X + buf * L::KC * L::XLD;
       float gs = 0.f;
-#pragma unroll
-      for (int c8 = 0; c8 < L::KC; c8 += 8) {
-        const float* xc = xb + c8 * L::XLD;
-        uint32_t hi[4][2], lo[4][2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) tf32_split(xc[(t4 + 4 * h) * L::XLD + 8 * j + g], hi[j][h], lo[j][h]);
-        uint32_t ahi[4][2], alo[4][2];   // the A copy: a_k x_k for weighted entries
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (UNIT) {
-              ahi[j][h] = hi[j][h];
-              alo[j][h] = lo[j][h];
-            } else {
-              const float a = AW[buf * L::KC + c8 + t4 + 4 * h];
-              tf32_split(a * xc[(t4 + 4 * h) * L::XLD + 8 * j + g], ahi[j][h], alo[j][h]);
-            }
-          }
-#pragma unroll
-        for (int mb = 0; mb < 2; ++mb) {
-          const uint32_t Ah[4] = {ahi[2 * mb][0], ahi[2 * mb + 1][0], ahi[2 * mb][1], ahi[2 * mb + 1][1]};
-          const uint32_t Al[4] = {alo[2 * mb][0], alo[2 * mb + 1][0], alo[2 * mb][1], alo[2 * mb + 1][1]};
-#pragma unroll
-          for (int nb = 0; nb < 2 + 2 * mb; ++nb) {
-            float(&d)[4] = acc[2 * mb + nb];
-            mma_tf32(d, Al, hi[nb][0], hi[nb][1]);
-            mma_tf32(d, Ah, lo[nb][0], lo[nb][1]);
-            mma_tf32(d, Ah, hi[nb][0], hi[nb][1]);
-          }
-        }
-      }
+      w32m_stage<UNIT>(acc, xb, AW + buf * L::KC, g, t4);
 #pragma unroll
       for (int k = 0; k < L::KC; k += 4) {
         const float4 rh = *reinterpret_cast<const float4*>(RHO + buf * L::KC + k);
