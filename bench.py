@@ -338,8 +338,10 @@ def run_ours(args, cfg_key):
         "traffic_unit": "DRAM bytes per side pass (dram__bytes_read.sum + dram__bytes_write.sum, ncu)",
         "traffic_source": traffic_src,
         "algorithmic_bytes_per_side_pass": rl["Q_sw"] / (2 * rl["B"]),
-        "kernel": "block sweep per side pass (b 33..128: k_sweep_tc4 + k_heavy_partial_tc4/solve + "
-                  "k_pass_cache; else k_sweep_light + k_heavy_*)",
+        "kernel": "block sweep per side pass (b 65..128: k_sweep_tc4 [+ k_sweep_wb on rotated user passes] + "
+                  "k_heavy_partial_tc4 / k_heavy_solve + k_pass_cache_flat; b 33..64: k_sweep_pk<2>; "
+                  "b 17..32: k_sweep_w32m + k_heavy_partial_wm<32>; b 4..16: k_sweep_w16m + "
+                  "k_heavy_partial_wm<16>; b = 1: k_sweep_b1 + k_b1_cache_flat; b = 256: k_sweep_light<256>)",
         "per_launch_algorithmic": (rl["F_sw"] if roof["unit"] == "TFLOP/s" else rl["Q_sw"]) / (2 * rl["B"]),
         "avg_launch_ms": round(sweep_ms / (2 * rl["B"]), 4),
         "peak_source": ("nominal FP32 (148 SM x 128 x 2 x measured SM clock; MEASURED_PEAKS.json has "

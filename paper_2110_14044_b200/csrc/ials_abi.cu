@@ -807,7 +807,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         static const bool mma = !(getenv("IALS_W32_MMA") && getenv("IALS_W32_MMA")[0] == '0');
         static int w32_sm = 0;
         static unsigned w32_init = 0;
-        auto kern = mma ? (unit ? k_sweep_w32m<true> : k_sweep_w32m<false>)
+        static const bool occ4 = getenv("IALS_W32_OCC") && getenv("IALS_W32_OCC")[0] == '4';   // (measurement)
+        auto kern = mma ? (occ4 ? (unit ? k_sweep_w32m<true, 4> : k_sweep_w32m<false, 4>)
+                                : (unit ? k_sweep_w32m<true> : k_sweep_w32m<false>))
                         : (unit ? k_sweep_w32<true> : k_sweep_w32<false>);
         const int wbytes = mma ? W32mLay::BYTES : W32Lay::BYTES;
         if (!(w32_init & dev_bit())) {
@@ -815,6 +817,10 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32Lay::BYTES));
           CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32mLay::BYTES));
           CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32mLay::BYTES));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32mLay::BYTES));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, W32mLay::BYTES));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<true, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+          CUDA_TRY(s, cudaFuncSetAttribute(k_sweep_w32m<false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
           w32_init |= dev_bit();
         }
         if (w32_sm == 0) {
@@ -1345,6 +1351,13 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
     LAUNCH_CHECK(s);
   }
   if (b == 1) {  // scalar blocks: the iCD special case
+    // the smaller side (items): the cache update walks the other side's entry order
+    // (coalesced cache and ids, d in L1 / L2) instead of scattering through `pos`
+    // (IALS_B1_FLAT: 0 = in the sweep, 2 = both sides entry-parallel; measured at the
+    // configs[2] shape: 116.7 / 78.9 / 79.9 ms an epoch for 0 / 1 / 2)
+    static const int b1_mode = getenv("IALS_B1_FLAT") ? atoi(getenv("IALS_B1_FLAT")) : 1;
+    const bool b1_swap = b1_mode >= 1 && p.x_rows && p.x_cols && side->n_rows < side->n_fixed && side->nnz > 0;
+    p.b1_flat = b1_swap || (b1_mode >= 2 && side->rows && side->nnz > 0);
     if (p.n_light > 0) {
       k_sweep_b1<<<std::min((p.n_light + 7) / 8, kNumSMs * 16), 256, 0, st>>>(p);
       LAUNCH_CHECK(s);
@@ -1355,7 +1368,15 @@ static int side_pass_impl(ials_session* s, const ials_side* side, const ials_sch
       LAUNCH_CHECK(s);
       k_b1_solve<<<(p.n_heavy + 7) / 8, 256, 0, st>>>(p);
       LAUNCH_CHECK(s);
-      k_b1_cache<<<g, 256, 0, st>>>(p);
+      if (!p.b1_flat) {
+        k_b1_cache<<<g, 256, 0, st>>>(p);
+        LAUNCH_CHECK(s);
+      }
+    }
+    if (p.b1_flat) {
+      const long long g = std::min<long long>((side->nnz + 1023) / 1024, 32LL * kNumSMs);
+      if (b1_swap) k_b1_cache_flat<true><<<(int)g, 256, 0, st>>>(p, side->nnz);
+      else k_b1_cache_flat<false><<<(int)g, 256, 0, st>>>(p, side->nnz);
       LAUNCH_CHECK(s);
     }
     return IALS_OK;

@@ -90,6 +90,7 @@ struct SweepParams {
   const int* chunk_tot;    // if set (k_sweep_tc4): light rows grouped by row chunk, chunk_tot[k]
   int chunk;               //   rows in chunk k; this launch sweeps chunk `chunk` only
   int heavy_reduced;       // k_heavy_solve reads one slot per heavy row (k_heavy_reduce ran)
+  int b1_flat;             // b = 1: the sweep leaves the cache to k_b1_cache_flat
 };
 
 template <int BT>

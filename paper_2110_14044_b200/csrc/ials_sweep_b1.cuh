@@ -79,6 +79,7 @@ IALS_DEVI float b1_solve(const SweepParams& p, int row, float hh, double gg) {
   }
   const float dl = (float)(g / (double)Hs);
   *w -= dl;
+  p.drow[row] = dl;   // the entry-parallel cache kernel (k_b1_cache_flat) reads d by row
   return dl;
 }
 
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(256) k_sweep_b1(SweepParams p) {
     float dl = 0.f;
     if (lane == 0) dl = b1_solve(p, row, hh, gg);
     dl = __shfl_sync(0xffffffffu, dl, 0);
-    b1_cache(p, e0 + lane, e1, 32, dl);
+    if (!p.b1_flat) b1_cache(p, e0 + lane, e1, 32, dl);
   }
 }
 
@@ -154,6 +155,48 @@ __global__ void __launch_bounds__(256) k_b1_cache(SweepParams p) {
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int sl = gw; sl < p.n_slices; sl += nw)
     b1_cache(p, p.slice_begin[sl] + lane, p.slice_end[sl], 32, p.hdelta[p.slice_heavy[sl]]);
+}
+
+// The pass's cache update walked in the OTHER side's entry order (x_rows = the
+// fixed side's row of each entry, x_cols = this side's row, x_pos = the cache
+// slot, NULL when that order is the cache's own): yhat -= f_u d_i with the
+// cache and the ids streamed, f_u constant along a run and d (n_rows floats)
+// resident in L1 / L2 -- the item pass otherwise scatters 4-byte updates over
+// the cache through `pos`, a 32-byte sector each.  Four entries per thread in
+// flight; every entry is written once (no atomics, deterministic).
+template <bool SWAP>
+__global__ void __launch_bounds__(256) k_b1_cache_flat(SweepParams p, long long nnz) {
+  // SWAP: the other side's order; else this side's own order (rows = this side's row of
+  // each entry), which only takes the update off the row's serial chain
+  const int* __restrict__ FI = SWAP ? p.x_rows : p.side.cols;   // fixed-side id
+  const int* __restrict__ DI = SWAP ? p.x_cols : p.side.rows;   // this side's row (d index)
+  const int* __restrict__ PS = SWAP ? p.x_pos : p.side.pos;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; e + 3 * stride < nnz; e += 4 * stride) {
+    int u[4], i[4];
+    long long pos[4];
+    float f[4], dv[4], c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u[k] = __ldg(FI + e + k * stride);
+      i[k] = __ldg(DI + e + k * stride);
+      pos[k] = PS ? (long long)__ldg(PS + e + k * stride) : e + k * stride;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      f[k] = __ldg(p.fixed + (size_t)u[k] * p.ldf + p.fb0);
+      dv[k] = p.drow[i[k]];
+      c[k] = p.cache[pos[k]];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p.cache[pos[k]] = c[k] - f[k] * dv[k];
+  }
+  for (; e < nnz; e += stride) {
+    const int u = __ldg(FI + e), i = __ldg(DI + e);
+    const long long pos = PS ? (long long)__ldg(PS + e) : e;
+    p.cache[pos] -= __ldg(p.fixed + (size_t)u * p.ldf + p.fb0) * p.drow[i];
+  }
 }
 
 }  // namespace ials

@@ -123,8 +123,8 @@ IALS_DEVI void w16m_stage(float (&acc)[2][4], const float* xb, const float* aw, 
   }
 }
 
-template <bool UNIT>
-__global__ void __launch_bounds__(W32mLay::NT, 3) k_sweep_w32m(SweepParams p) {
+template <bool UNIT, int MINB = 3>
+__global__ void __launch_bounds__(W32mLay::NT, MINB) k_sweep_w32m(SweepParams p) {
   using L = W32mLay;
   extern __shared__ __align__(16) float w32m_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
