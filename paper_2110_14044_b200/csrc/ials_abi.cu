@@ -32,6 +32,7 @@
 #include "ials_sweep_w16.cuh"
 #include "ials_sweep_w16m.cuh"
 #include "ials_heavy_w.cuh"
+#include "ials_sweep_w64m.cuh"
 
 using namespace ials;
 
@@ -698,6 +699,12 @@ static int launch_heavy_w(ials_session* s, const SweepParams& p, int bt, cudaStr
   return IALS_OK;
 }
 
+// b 33..64: the warp-pair sweep instead of the packed tcgen05 one (IALS_W64=0)
+static bool w64_enabled() {
+  static const bool on = !(getenv("IALS_W64") && getenv("IALS_W64")[0] == '0');
+  return on;
+}
+
 static int wb_attrs(ials_session* s) {
   static unsigned winit = 0;
   if (!(winit & dev_bit())) {
@@ -796,6 +803,27 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
         else
           k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
+      } else if (G == 2 && p.vec && w64_enabled()) {
+        // b 33..64: one row per pair of warps, the Hessian by warp-level 3xTF32 MMA tiles
+        // (ials_sweep_w64m.cuh; IALS_W64=0: the packed tcgen05 sweep)
+        static int w64_sm = 0;
+        static unsigned w64_init = 0;
+        if (!(w64_init & dev_bit())) {
+          for (auto k : {k_sweep_w64m<true>, k_sweep_w64m<false>}) {
+            CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, W64mLay::BYTES));
+            CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+          }
+          w64_init |= dev_bit();
+        }
+        if (w64_sm == 0) {
+          CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w64_sm, k_sweep_w64m<true>, W64mLay::NT,
+                                                                   W64mLay::BYTES));
+          if (w64_sm < 1) w64_sm = 1;
+        }
+        q.queue = p.redo_cnt + 2;   // zeroed with the redo count (and per chunk)
+        const int wgrid = std::min((n_b + W64mLay::TEAMS - 1) / W64mLay::TEAMS, w64_sm * kNumSMs);
+        if (unit) k_sweep_w64m<true><<<wgrid, W64mLay::NT, W64mLay::BYTES, st>>>(q);
+        else k_sweep_w64m<false><<<wgrid, W64mLay::NT, W64mLay::BYTES, st>>>(q);
       } else if (G == 2) {
         if (unit)
           k_sweep_pk<2, true><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
