@@ -32,7 +32,6 @@
 #include "ials_sweep_w16.cuh"
 #include "ials_sweep_w16m.cuh"
 #include "ials_heavy_w.cuh"
-#include "ials_sweep_w64m.cuh"
 
 using namespace ials;
 
@@ -668,6 +667,10 @@ static bool hw_enabled() {
 }
 // (IALS_W_MMA=0: the FP32 SIMT tiles instead of the warp-level 3xTF32 MMA tiles, in the
 // b <= 16 sweep and in the slice kernels; IALS_W32_MMA=0 the same for the b 17..32 sweep)
+// Cancellation limit (H_kk / pivot_k) of the warp-level MMA sweeps: their factorisation is
+// FP32 and only the 3xTF32 Hessian carries an error (~1e-6 of its entries), so the limit
+// sits above the packed tcgen05 sweep's 16 (whose trailing updates are 3xTF32 as well)
+static constexpr float kWarpCond = 64.f;
 static bool wmma_enabled() {
   static const bool on = !(getenv("IALS_W_MMA") && getenv("IALS_W_MMA")[0] == '0');
   return on;
@@ -697,12 +700,6 @@ static int launch_heavy_w(ials_session* s, const SweepParams& p, int bt, cudaStr
   kern<<<grid, WHLay<NB>::NT, bytes, st>>>(p, bt);
   LAUNCH_CHECK(s);
   return IALS_OK;
-}
-
-// b 33..64: the warp-pair sweep instead of the packed tcgen05 one (IALS_W64=0)
-static bool w64_enabled() {
-  static const bool on = !(getenv("IALS_W64") && getenv("IALS_W64")[0] == '0');
-  return on;
 }
 
 static int wb_attrs(ials_session* s) {
@@ -803,27 +800,6 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           k_sweep_tc4<true><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
         else
           k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
-      } else if (G == 2 && p.vec && w64_enabled()) {
-        // b 33..64: one row per pair of warps, the Hessian by warp-level 3xTF32 MMA tiles
-        // (ials_sweep_w64m.cuh; IALS_W64=0: the packed tcgen05 sweep)
-        static int w64_sm = 0;
-        static unsigned w64_init = 0;
-        if (!(w64_init & dev_bit())) {
-          for (auto k : {k_sweep_w64m<true>, k_sweep_w64m<false>}) {
-            CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, W64mLay::BYTES));
-            CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-          }
-          w64_init |= dev_bit();
-        }
-        if (w64_sm == 0) {
-          CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w64_sm, k_sweep_w64m<true>, W64mLay::NT,
-                                                                   W64mLay::BYTES));
-          if (w64_sm < 1) w64_sm = 1;
-        }
-        q.queue = p.redo_cnt + 2;   // zeroed with the redo count (and per chunk)
-        const int wgrid = std::min((n_b + W64mLay::TEAMS - 1) / W64mLay::TEAMS, w64_sm * kNumSMs);
-        if (unit) k_sweep_w64m<true><<<wgrid, W64mLay::NT, W64mLay::BYTES, st>>>(q);
-        else k_sweep_w64m<false><<<wgrid, W64mLay::NT, W64mLay::BYTES, st>>>(q);
       } else if (G == 2) {
         if (unit)
           k_sweep_pk<2, true><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
@@ -856,6 +832,7 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           if (w32_sm < 1) w32_sm = 1;
         }
         q.queue = p.redo_cnt + 2;   // zeroed with the redo count (and per chunk)
+        q.cond_max = kWarpCond;
         const int wgrid = std::min((n_b + W32Lay::NW - 1) / W32Lay::NW, w32_sm * kNumSMs);
         kern<<<wgrid, W32Lay::NT, wbytes, st>>>(q);
       } else {
@@ -1053,6 +1030,10 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
   // second stream (disjoint rows, the cache only read), joined before their solve
   const bool hw = w16 && p.n_heavy > 0 && hw_enabled();
   const bool fork = hw && p.n_light > 0;
+  // [0] the redo count (rows the MMA kernels' cancellation guards reject), [3] the light-row
+  // queue, [4] the redo launch's queue
+  if (w16) CUDA_TRY(s, cudaMemsetAsync(p.redo_cnt, 0, 8 * sizeof(int), st));
+  const bool guard = w16 && wmma_enabled();
   if (hw) {
     cudaStream_t hst = st;
     if (fork) {
@@ -1092,7 +1073,7 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     }
     SweepParams q = p;
     q.queue = p.redo_cnt + 3;
-    CUDA_TRY(s, cudaMemsetAsync(q.queue, 0, sizeof(int), st));
+    q.cond_max = kWarpCond;
     const int tasks = (p.n_light + 1) / 2;
     const int wgrid = std::min((tasks + W16Lay::NW - 1) / W16Lay::NW, w16_sm * kNumSMs);
     kern<<<wgrid, W16Lay::NT, wbytes, st>>>(q);
@@ -1125,12 +1106,31 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
       LAUNCH_CHECK(s);
       ph.heavy_reduced = 1;
     }
-    k_heavy_solve<BT><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(ph);
+    if (guard && hw)
+      k_heavy_solve<BT, true><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(ph);
+    else
+      k_heavy_solve<BT><<<(p.n_heavy + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(ph);
     LAUNCH_CHECK(s);
     if (!w16) {
       k_heavy_cache<BT><<<(p.n_slices + L::RPC - 1) / L::RPC, threads, L::CTA_BYTES, st>>>(p);
       LAUNCH_CHECK(s);
     }
+  }
+  if (guard && p.n_light + p.n_heavy > 0) {
+    // rows the cancellation guards rejected: the FP32 SIMT sweep over the device list
+    // (persistent grid, the count is read on the device; it updates their cache itself,
+    // the entry-parallel pass below sees d = 0 for them)
+    static int simt_sm = 0;
+    if (simt_sm == 0) {
+      CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&simt_sm, k_sweep_light<BT>, threads, L::CTA_BYTES));
+      if (simt_sm < 1) simt_sm = 1;
+    }
+    SweepParams q = p;
+    q.light_rows = p.redo_rows;
+    q.n_light_dev = p.redo_cnt;
+    q.queue = p.redo_cnt + 4;
+    k_sweep_light<BT><<<simt_sm * kNumSMs, threads, L::CTA_BYTES, st>>>(q);
+    LAUNCH_CHECK(s);
   }
   if (w16 && p.n_light + p.n_heavy > 0) {
     const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);

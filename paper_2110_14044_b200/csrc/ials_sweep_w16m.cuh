@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(W16mLay::NT, 4) k_sweep_w16m(SweepParams p) {
     __syncwarp();
     // lam_r on the diagonal (identity on the padding rows, where H and G are zero)
     HS[l16 * L::HLD + l16] += (l16 < b) ? lam : 1.f;
+    const float diag0 = HS[l16 * L::HLD + l16] + TPL[l16 * L::HLD + l16];   // for the cancellation guard
     float a[16];
 #pragma unroll
     for (int j4 = 0; j4 < 4; ++j4) {
@@ -206,9 +207,12 @@ __global__ void __launch_bounds__(W16mLay::NT, 4) k_sweep_w16m(SweepParams p) {
     for (int j4 = 0; j4 < 4; ++j4)
       reinterpret_cast<float4*>(HS + l16 * L::HLD)[j4] = make_float4(a[4 * j4], a[4 * j4 + 1], a[4 * j4 + 2], a[4 * j4 + 3]);
     __syncwarp();
-    // the first failing pivot of this half's row, if any: lane k kept 1/sqrt(pivot k)
-    const unsigned badmask = (__ballot_sync(FULL, !(rown > 0.f && rown < 3.0e38f)) >> (16 * half)) & 0xffffu;
-    const int bad = badmask ? __ffs(badmask) - 1 : -1;
+    // cancellation guard (lane k kept 1/sqrt(pivot k)): a pivot that lost more than
+    // cond_max of its diagonal, or is not positive and finite, sends this half's row to
+    // the FP32 SIMT sweep (the redo list), which also names a singular row
+    const unsigned flagged =
+        (__ballot_sync(FULL, l16 < b && !(rown > 0.f && rown < 3.0e38f && diag0 * (rown * rown) <= p.cond_max)) >>
+         (16 * half)) & 0xffffu;
     float dj = 0.f;
 #pragma unroll
     for (int k = 15; k >= 0; --k) {
@@ -218,8 +222,11 @@ __global__ void __launch_bounds__(W16mLay::NT, 4) k_sweep_w16m(SweepParams p) {
     }
     __syncwarp();   // HS (the staging buffers) is rewritten by the next row
     if (row >= 0) {
-      if (bad >= 0 && bad < b) {
-        if (l16 == 0) report_singular(p.err, p.side_id, row, bad);
+      if (flagged) {
+        if (l16 == 0) {
+          p.redo_rows[atomicAdd(p.redo_cnt, 1)] = row;
+          atomicAdd(p.redo_total, 1ull);
+        }
         if (l16 < b) p.drow[(size_t)row * b + l16] = 0.f;
       } else if (l16 < b) {
         p.own[(size_t)row * p.ldo + p.b0 + l16] = ow - dj;

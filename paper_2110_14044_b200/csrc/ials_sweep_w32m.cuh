@@ -19,7 +19,8 @@
 // so A and B share registers (unit weights; weighted entries scale A's copy).
 // Only the six tiles that meet the lower triangle are formed: (mb, nb) =
 // (0, 0..1), (1, 0..3); the factorisation never reads above the diagonal.
-// The gradient, assembly, Cholesky and solves are those of ials_sweep_w32.cuh.
+// The gradient, assembly, Cholesky and solves are those of ials_sweep_w32.cuh; a row
+// whose pivots cancel (H_kk / pivot_k > cond_max) is left to the FP32 SIMT sweep.
 #pragma once
 #include "ials_sweep_w32.cuh"
 
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(W32mLay::NT, MINB) k_sweep_w32m(SweepParams p)
     __syncwarp();
     // lam_r on the diagonal (identity on the padding rows, where H and G are zero)
     HS[lane * L::HLD + lane] += (lane < b) ? lam : 1.f;
+    const float diag0 = HS[lane * L::HLD + lane] + TPL[lane * L::HLD + lane];   // for the cancellation guard
     float a[32];
 #pragma unroll
     for (int j4 = 0; j4 < 8; ++j4) {
@@ -299,9 +301,12 @@ __global__ void __launch_bounds__(W32mLay::NT, MINB) k_sweep_w32m(SweepParams p)
     for (int j4 = 0; j4 < 8; ++j4)
       reinterpret_cast<float4*>(HS + lane * L::HLD)[j4] = make_float4(a[4 * j4], a[4 * j4 + 1], a[4 * j4 + 2], a[4 * j4 + 3]);
     __syncwarp();
-    // the first failing pivot, if any: lane k kept 1/sqrt(pivot k)
-    const unsigned badmask = __ballot_sync(0xffffffffu, !(rown > 0.f && rown < 3.0e38f));
-    const int bad = badmask ? __ffs(badmask) - 1 : -1;
+    // cancellation guard (lane k kept 1/sqrt(pivot k)): the 3xTF32 Hessian carries an
+    // error of ~1e-6 of its entries, so a pivot that lost more than cond_max of its
+    // diagonal -- or is not positive and finite -- sends the row to the FP32 SIMT sweep
+    // (the redo list), which also names a singular row
+    const unsigned flagged = __ballot_sync(
+        0xffffffffu, lane < b && !(rown > 0.f && rown < 3.0e38f && diag0 * (rown * rown) <= p.cond_max));
     float dj = 0.f;
 #pragma unroll
     for (int k = 31; k >= 0; --k) {
@@ -310,8 +315,11 @@ __global__ void __launch_bounds__(W32mLay::NT, MINB) k_sweep_w32m(SweepParams p)
       if (lane < k) t = fmaf(-HS[k * L::HLD + lane], dk, t);
     }
     __syncwarp();   // HS (the staging buffers) is rewritten by the next row
-    if (bad >= 0 && bad < b) {
-      if (lane == 0) report_singular(p.err, p.side_id, row, bad);
+    if (flagged) {
+      if (lane == 0) {
+        p.redo_rows[atomicAdd(p.redo_cnt, 1)] = row;
+        atomicAdd(p.redo_total, 1ull);
+      }
       if (lane < b) p.drow[(size_t)row * b + lane] = 0.f;
     } else if (lane < b) {
       p.own[(size_t)row * p.ldo + p.b0 + lane] = ow - dj;

@@ -146,7 +146,10 @@ def _heavy_instance(U, I, per_user, s, seed):
 @pytest.mark.parametrize("d,b,I", [(16, 8, 600), (32, 32, 600), (64, 64, 600), (128, 128, 600),
                                    (96, 48, 600), (256, 256, 600),
                                    # d > I: item Hessians with kappa ~ 4e3 in the first epoch
-                                   (64, 64, 60), (128, 128, 60)])
+                                   (64, 64, 60), (128, 128, 60),
+                                   # the same at the warp-level MMA widths (their cancellation
+                                   # guard hands such rows to the FP32 sweep)
+                                   (32, 32, 28), (16, 16, 15), (48, 24, 20)])
 def test_heavy_rows_vs_oracle(ials, d, b, I):
     """Items above the heavy threshold go through split-K slices."""
     from oracle import ialspp_oracle as orc
