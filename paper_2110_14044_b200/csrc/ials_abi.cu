@@ -32,6 +32,7 @@
 #include "ials_sweep_w16.cuh"
 #include "ials_sweep_w16m.cuh"
 #include "ials_heavy_w.cuh"
+#include "ials_heavy_w64.cuh"
 
 using namespace ials;
 
@@ -913,6 +914,23 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
           LAUNCH_CHECK(s);
           heavy_reduced = true;
         }
+      } else if (G == 2 && p.vec && hw_enabled() && wmma_enabled()) {
+        // b 33..64: a slice per pair of warps, warp-level 3xTF32 MMA tiles (ials_heavy_w64.cuh)
+        static int h64_sm = 0;
+        static unsigned h64_init = 0;
+        if (!(h64_init & dev_bit())) {
+          for (auto k : {k_heavy_partial_wm64<true>, k_heavy_partial_wm64<false>})
+            CUDA_TRY(s, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, WH64Lay::BYTES));
+          h64_init |= dev_bit();
+        }
+        if (h64_sm == 0) {
+          CUDA_TRY(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h64_sm, k_heavy_partial_wm64<true>, WH64Lay::NT,
+                                                                   WH64Lay::BYTES));
+          if (h64_sm < 1) h64_sm = 1;
+        }
+        const int g64 = std::min((p.n_slices + WH64Lay::TEAMS - 1) / WH64Lay::TEAMS, h64_sm * kNumSMs);
+        if (unit) k_heavy_partial_wm64<true><<<g64, WH64Lay::NT, WH64Lay::BYTES, hst>>>(p);
+        else k_heavy_partial_wm64<false><<<g64, WH64Lay::NT, WH64Lay::BYTES, hst>>>(p);
       } else if (G == 2) {
         if (unit) k_heavy_partial_pk<2, true><<<hg, 128, PkLay<2>::BYTES, hst>>>(p, fmap, use_tma);
         else k_heavy_partial_pk<2, false><<<hg, 128, PkLay<2>::BYTES, hst>>>(p, fmap, use_tma);
