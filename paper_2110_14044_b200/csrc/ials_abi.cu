@@ -802,6 +802,9 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
         else
           k_sweep_tc4<false><<<grid, 128, TcLay4::BYTES, st>>>(q, fmap, use_tma);
       } else if (G == 2) {
+        // (IALS_PK_COND: the light rows' cancellation limit at b 33..64, default the pass's)
+        static const float pk_cond = getenv("IALS_PK_COND") ? (float)atof(getenv("IALS_PK_COND")) : 0.f;
+        if (pk_cond > 1.f) q.cond_max = pk_cond;
         if (unit)
           k_sweep_pk<2, true><<<grid, 128, PkLay<2>::BYTES, st>>>(q, fmap, use_tma);
         else
