@@ -1018,7 +1018,22 @@ static int launch_sweep_tc4(ials_session* s, const SweepParams& p, long long nnz
       const long long g = std::min<long long>((nnz + 31) / 32, 16LL * kNumSMs);
       // walk the other side's order when this side's d is the smaller gather
       const bool swap = p.x_rows && p.x_cols && p.side.n_rows < p.side.n_fixed;
-      if (swap) {
+      // narrow blocks: 4 lanes per entry, 2 (b <= 32) or 4 (b <= 64) float4 each -- configs[1]
+      // epoch 8.89 -> 7.43 ms, sw-b64 26.6 -> 25.5 ms against the 8-lane 128-wide instantiation
+      // (IALS_CACHE_NARROW=0 keeps that one; IALS_CACHE_LPE=2: two lanes per entry at b <= 32,
+      // 7.52 vs 7.42 ms at configs[1])
+      static const bool narrow = !(getenv("IALS_CACHE_NARROW") && getenv("IALS_CACHE_NARROW")[0] == '0');
+      static const bool lpe2 = getenv("IALS_CACHE_LPE") && getenv("IALS_CACHE_LPE")[0] == '2';
+      if (narrow && p.vec && p.b <= 32 && lpe2) {
+        if (swap) k_pass_cache_flat<true, 2, true, 32><<<(int)g, 256, 0, cst>>>(p, nnz);
+        else k_pass_cache_flat<true, 2, false, 32><<<(int)g, 256, 0, cst>>>(p, nnz);
+      } else if (narrow && p.vec && p.b <= 32) {
+        if (swap) k_pass_cache_flat<true, 4, true, 32><<<(int)g, 256, 0, cst>>>(p, nnz);
+        else k_pass_cache_flat<true, 4, false, 32><<<(int)g, 256, 0, cst>>>(p, nnz);
+      } else if (narrow && p.vec && p.b <= 64) {
+        if (swap) k_pass_cache_flat<true, 4, true, 64><<<(int)g, 256, 0, cst>>>(p, nnz);
+        else k_pass_cache_flat<true, 4, false, 64><<<(int)g, 256, 0, cst>>>(p, nnz);
+      } else if (swap) {
         if (p.vec) k_pass_cache_flat<true, 8, true><<<(int)g, 256, 0, cst>>>(p, nnz);
         else k_pass_cache_flat<false, 8, true><<<(int)g, 256, 0, cst>>>(p, nnz);
       } else {
@@ -1158,10 +1173,16 @@ static int launch_sweep(ials_session* s, const SweepParams& p, long long nnz, cu
     // walk the other side's order when this side's d is the smaller gather
     const bool swap = p.x_rows && p.x_cols && p.side.n_rows < p.side.n_fixed;
     static const bool lpe8 = getenv("IALS_W16_LPE8") != nullptr;   // (measurements)
+    // two lanes x 2 float4 per entry (sw-b16 epoch 19.2 -> 17.4 ms against four lanes;
+    // IALS_CACHE_LPE=4 keeps four)
+    static const bool lpe2 = !(getenv("IALS_CACHE_LPE") && getenv("IALS_CACHE_LPE")[0] == '4');
     if (lpe8) {
       if (swap) k_pass_cache_flat<true, 8, true><<<(int)g, 256, 0, st>>>(p, nnz);
       else k_pass_cache_flat<true, 8, false><<<(int)g, 256, 0, st>>>(p, nnz);
-    } else {   // 4 lanes x 16 bytes cover a 16-wide sub-row
+    } else if (lpe2) {
+      if (swap) k_pass_cache_flat<true, 2, true, 16><<<(int)g, 256, 0, st>>>(p, nnz);
+      else k_pass_cache_flat<true, 2, false, 16><<<(int)g, 256, 0, st>>>(p, nnz);
+    } else {   // 4 lanes x 16 bytes
       if (swap) k_pass_cache_flat<true, 4, true, 16><<<(int)g, 256, 0, st>>>(p, nnz);
       else k_pass_cache_flat<true, 4, false, 16><<<(int)g, 256, 0, st>>>(p, nnz);
     }

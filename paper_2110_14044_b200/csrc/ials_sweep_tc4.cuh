@@ -913,9 +913,9 @@ __global__ void __launch_bounds__(256) k_pass_cache(SweepParams p) {
 // L1 and 292 MB at msd).  Each entry's sum is the same fixed-order chain of
 // the same products (fma is commutative in its factors): bit-identical.
 // BMAX: the widest block the instantiation serves (b <= 16 with LPE = 4: one
-// float4 per lane, 8 entries per warp step).
+// float4 per lane, 8 entries per warp step; b <= 32 with LPE = 4: two).
 template <bool VEC, int LPE, bool SWAP, int BMAX = 128>
-__global__ void __launch_bounds__(256, (LPE == 8 || BMAX <= 16) ? 4 : 2) k_pass_cache_flat(SweepParams p, long long nnz) {
+__global__ void __launch_bounds__(256, (LPE == 8 || BMAX <= 64) ? 4 : 2) k_pass_cache_flat(SweepParams p, long long nnz) {
   constexpr int EPW = 32 / LPE, NQ = BMAX / (4 * LPE);   // entries per warp step, float4 per lane
   const int lane = threadIdx.x & 31, g = lane % LPE, sub = lane / LPE;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
